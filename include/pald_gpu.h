@@ -1,0 +1,180 @@
+/*
+ * pald_gpu.h -- C ABI of the B200 (sm_100a) PaLD cohesion engine.
+ *
+ * This is the drop-in boundary for the O(n^3) hot path of the reference
+ * library (/root/reference/proj/include/pald). Every entry point names the
+ * reference interface it replaces. Plain pointers and sizes only; no torch
+ * or C++ types cross this boundary. The header-only C++ shim with the
+ * reference's own signatures (pald::gpu::blocked_pairwise<float>, ...)
+ * lives in include/pald_gpu.hpp and is the intended caller for C++ code.
+ *
+ * Semantics (identical to the reference):
+ *   Input  D: dense n x n fp32 distance matrix, row-major (element (x,y) at
+ *             x*ld + y). Zero diagonal, off-diagonal > 0, exactly symmetric
+ *             (types.hpp:45-65). Validated on the device unless
+ *             PALD_GPU_FLAG_SKIP_VALIDATION is set.
+ *   Output U: focus sizes u_xy, int32 n x n, symmetric, diagonal 0
+ *             (types.hpp:79-86). Bit-exact with the reference's strict-<
+ *             tie semantics, pairwise (blocked.hpp:101-122) or triplet
+ *             (blocked.hpp:195-238, U initialised to 2) as selected.
+ *   Output C: unnormalized cohesion, fp32 n x n (the fp32 instantiation of
+ *             CohesionMatrix, types.hpp:90-98). Pairwise C is bit-identical
+ *             to blocked_pairwise<float> / parallel_pairwise<float>
+ *             (ascending-partner summation order). Triplet C matches
+ *             blocked_triplet<double> within fp32 tolerance and has its
+ *             diagonal left 0 (apply fill_diagonal, reference.hpp:213-220).
+ *
+ * Return codes mirror the reference CLI's exception -> exit code map
+ * (tools/pald.cpp:406-415): 0 ok, 2 ValidationError, 3
+ * UnsupportedPolicyError, 4 IoError; 5 CUDA failure, 6 communicator
+ * failure. pald_gpu_last_error() gives the message (thread-local).
+ */
+#ifndef PALD_GPU_H_
+#define PALD_GPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PALD_GPU_ABI_VERSION 1
+
+/* Algorithm variant: blocked_pairwise / parallel_pairwise (blocked.hpp:368,
+ * parallel.hpp:159) vs blocked_triplet / parallel_triplet (blocked.hpp:424,
+ * parallel.hpp:257). */
+enum pald_gpu_algorithm { PALD_GPU_PAIRWISE = 0, PALD_GPU_TRIPLET = 1 };
+
+/* Policy, types.hpp:34. The GPU engine implements Strict; InclusiveSplit
+ * returns PALD_GPU_ERR_UNSUPPORTED (the triplet reference does the same,
+ * blocked.hpp:429-430). */
+enum pald_gpu_policy { PALD_GPU_STRICT = 0, PALD_GPU_INCLUSIVE_SPLIT = 1 };
+
+enum pald_gpu_status {
+  PALD_GPU_OK = 0,
+  PALD_GPU_ERR_VALIDATION = 2,
+  PALD_GPU_ERR_UNSUPPORTED = 3,
+  PALD_GPU_ERR_IO = 4,
+  PALD_GPU_ERR_CUDA = 5,
+  PALD_GPU_ERR_COMM = 6
+};
+
+enum pald_gpu_flags {
+  /* The caller guarantees D already passed DistanceMatrix validation
+   * (the C++ shim sets this: its DistanceMatrix is validated in double). */
+  PALD_GPU_FLAG_SKIP_VALIDATION = 1u,
+  /* Use the integer-key compare path even when the fp32 range allows the
+   * FFMA.SAT compare path (testing). */
+  PALD_GPU_FLAG_FORCE_EXACT = 2u
+};
+
+typedef struct pald_gpu_opts {
+  uint32_t struct_size;   /* sizeof(pald_gpu_opts) */
+  int32_t algorithm;      /* enum pald_gpu_algorithm */
+  int32_t policy;         /* enum pald_gpu_policy */
+  int32_t device;         /* CUDA device ordinal; -1 = current device */
+  /* Block-size hints of the reference drivers (b, b_focus, b_cohesion).
+   * Validated >= 1 exactly like blocked.hpp:372 / :431; the GPU tile shape
+   * is fixed (128 x 128 x 32), so they do not change results -- neither do
+   * they in the reference (C bits of blocked_pairwise<float> are
+   * independent of b). */
+  uint64_t block;
+  uint64_t block_focus;
+  uint64_t block_cohesion;
+  uint32_t flags;         /* enum pald_gpu_flags */
+  uint32_t reserved;
+} pald_gpu_opts;
+
+/* PhaseTimes, types.hpp:114-119, filled from CUDA events. */
+typedef struct pald_gpu_phase_times {
+  double focus_seconds;
+  double cohesion_seconds;
+  double overhead_seconds;
+  double total_seconds;
+} pald_gpu_phase_times;
+
+/* Fills defaults: pairwise, strict, current device, blocks 128, flags 0. */
+void pald_gpu_opts_init(pald_gpu_opts* opts);
+
+/* Thread-local message of the last failing call on this thread. */
+const char* pald_gpu_last_error(void);
+
+int pald_gpu_abi_version(void);
+
+/* One-shot host API. Replaces blocked_pairwise<float> /
+ * parallel_pairwise<float> (blocked.hpp:368-418, parallel.hpp:159-222) and
+ * blocked_triplet<float> / parallel_triplet<float> (blocked.hpp:424-477,
+ * parallel.hpp:257-320) after to_real<float> (blocked.hpp:91-96).
+ * D, U_out, C_out are HOST pointers, dense (ld = n). U_out may be NULL.
+ * Pinned host memory gives full-speed copies. Synchronous. */
+int pald_gpu_cohesion_f32(const float* D, uint64_t n, const pald_gpu_opts* opts,
+                          int32_t* U_out, float* C_out, pald_gpu_phase_times* times);
+
+/* Device API, asynchronous on `stream` (a cudaStream_t; NULL = legacy
+ * default stream) except for one small device->host read of the range
+ * check. dD, dU, dC are DEVICE pointers with leading dimensions (elements)
+ * ldd, ldu, ldc >= n. dU may be NULL. Uses a per-device cached workspace. */
+int pald_gpu_cohesion_f32_device(const float* dD, uint64_t ldd, uint64_t n,
+                                 const pald_gpu_opts* opts, int32_t* dU, uint64_t ldu,
+                                 float* dC, uint64_t ldc, void* stream);
+
+/* ---- Staged plan: the building blocks of the multi-GPU drivers --------
+ * A plan owns the device workspace for one n on one device. Pass 1
+ * (focus) covers the upper-triangular 128x128 pair tiles whose tile row is
+ * in [tile_row_begin, tile_row_end), writing U and W = 1/U for those tiles
+ * and their mirror images; pass 2 (cohesion) writes C rows
+ * [row_begin, row_end). Between the passes a multi-GPU driver sums U and W
+ * over ranks (each entry is written by exactly one rank; the rest are 0). */
+typedef struct pald_gpu_plan pald_gpu_plan;
+
+typedef struct pald_gpu_buffers {
+  int32_t* U;        /* device, n x ld, focus sizes */
+  float* W;          /* device, n x ld, 1/U (diagonal 0) */
+  float* C;          /* device, n x ld, unnormalized cohesion */
+  uint64_t ld;       /* leading dimension (elements) of U, W, C */
+  uint64_t n;
+  uint64_t tile;     /* pair-tile edge (points) */
+  uint64_t tiles_per_dim;
+  int32_t exact_path;  /* 1 when the integer-key compare path is in use */
+  int32_t reserved;
+} pald_gpu_buffers;
+
+int pald_gpu_plan_create(uint64_t n, const pald_gpu_opts* opts, pald_gpu_plan** out);
+int pald_gpu_plan_destroy(pald_gpu_plan* plan);
+/* Validates (unless skipped), range-checks and lays out D (device pointer,
+ * leading dimension ldd). Synchronizes `stream` once to read the range
+ * check. Zeroes U, W. */
+int pald_gpu_plan_load(pald_gpu_plan* plan, const float* dD, uint64_t ldd, void* stream);
+/* Same, from a host pointer (dense, ld = n). */
+int pald_gpu_plan_load_host(pald_gpu_plan* plan, const float* D, void* stream);
+int pald_gpu_plan_focus(pald_gpu_plan* plan, uint64_t tile_row_begin, uint64_t tile_row_end,
+                        void* stream);
+int pald_gpu_plan_cohesion(pald_gpu_plan* plan, uint64_t row_begin, uint64_t row_end,
+                           void* stream);
+int pald_gpu_plan_buffers(const pald_gpu_plan* plan, pald_gpu_buffers* out);
+/* Kernel launches issued by this plan so far (evidence counter). */
+uint64_t pald_gpu_plan_launches(const pald_gpu_plan* plan);
+
+/* Fraction of pass-1 work in tile rows [0, r) -- used to split the
+ * triangular tile grid across ranks with equal work. */
+double pald_gpu_focus_work_prefix(uint64_t n, uint64_t tile_rows);
+
+/* ---- Epilogue and input helpers ---------------------- */
+/* fill_diagonal, reference.hpp:213-220: c_xx = sum_{y != x} 1/u_xy,
+ * accumulated in double in ascending y and written as double to
+ * diag_out[x] (device pointer, n doubles). */
+int pald_gpu_fill_diagonal(const int32_t* dU, uint64_t ldu, uint64_t n, double* diag_out,
+                           void* stream);
+/* Euclidean distances of a point cloud (ingest.hpp:303-322): each pair
+ * once, sum of squared differences in double in coordinate order (no
+ * contraction), sqrt in double, rounded to fp32; diagonal 0. Device
+ * pointers; points row-major n x dim doubles. */
+int pald_gpu_points_to_distances(const double* dP, uint64_t n, uint64_t dim, float* dD,
+                                 uint64_t ldd, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PALD_GPU_H_ */

@@ -1,0 +1,246 @@
+// ref_bridge.cpp -- C entry points over the UNMODIFIED reference library.
+//
+// TEST / BASELINE INFRASTRUCTURE ONLY. Compiled by oracle/Makefile against
+// the reference headers where they lie (/root/reference/proj/include; read
+// only, never copied) into oracle/_ref/libpald_ref*.so. Used to
+//   * generate golden vectors (tests/golden/make_golden.py),
+//   * validate the C restatement in oracle/pald_oracle.c,
+//   * time the reference CPU implementation (bench.py cpu_baseline and
+//     --impl reference).
+// Every function forwards to the reference symbol it names; the only logic
+// here is marshalling (and, for the bounded timing sample, the x-block-row
+// prefix of the parallel_pairwise driver loop, parallel.hpp:178-215).
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "pald/pald.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+pald::DistanceMatrix make_d(const double* d, uint64_t n) {
+  return pald::DistanceMatrix(n, std::vector<double>(d, d + n * n));
+}
+
+void out_result(const pald::PaldResult& r, int32_t* u, double* c) {
+  const size_t nn = r.focus.sizes.size();
+  if (u) std::memcpy(u, r.focus.sizes.data(), sizeof(int32_t) * nn);
+  if (c) std::memcpy(c, r.cohesion.values.data(), sizeof(double) * nn);
+}
+
+void out_times(const pald::PhaseTimes& t, double* times) {
+  if (!times) return;
+  times[0] = t.focus_seconds;
+  times[1] = t.cohesion_seconds;
+  times[2] = t.overhead_seconds;
+  times[3] = t.total_seconds;
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const pald::UnsupportedPolicyError& e) {
+    g_err = e.what();
+    return 3;
+  } catch (const pald::IoError& e) {
+    g_err = e.what();
+    return 4;
+  } catch (const pald::Error& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+pald::Policy pol(int p) { return p == 0 ? pald::Policy::Strict : pald::Policy::InclusiveSplit; }
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+// detail::random_distances, blocked.hpp:522-529
+int ref_random_distances(uint64_t n, uint64_t seed, double* out) {
+  return guarded([&] {
+    const auto d = pald::detail::random_distances(n, seed);
+    std::memcpy(out, d.values().data(), sizeof(double) * n * n);
+  });
+}
+
+// DistanceMatrix validation, types.hpp:45-65
+int ref_validate(const double* d, uint64_t n) {
+  return guarded([&] { (void)make_d(d, n); });
+}
+
+// focus_size, reference.hpp:31-45
+int ref_focus_size(const double* d, uint64_t n, uint64_t x, uint64_t y, int policy, int* out) {
+  return guarded([&] { *out = pald::focus_size(make_d(d, n), x, y, pol(policy)); });
+}
+
+// pairwise_entrywise, reference.hpp:104-147
+int ref_pairwise_entrywise(const double* d, uint64_t n, int policy, int32_t* u, double* c) {
+  return guarded([&] { out_result(pald::pairwise_entrywise(make_d(d, n), pol(policy)), u, c); });
+}
+
+// triplet_entrywise, reference.hpp:154-208
+int ref_triplet_entrywise(const double* d, uint64_t n, int validate_ties, int32_t* u, double* c) {
+  return guarded([&] { out_result(pald::triplet_entrywise(make_d(d, n), validate_ties != 0), u, c); });
+}
+
+// oracle_cohesion, reference.hpp:73-99 (normalized; no-ties oracle only)
+int ref_oracle_cohesion(const double* d, uint64_t n, int policy, double* c) {
+  return guarded([&] {
+    const auto r = pald::oracle_cohesion(make_d(d, n), pol(policy));
+    std::memcpy(c, r.values.data(), sizeof(double) * n * n);
+  });
+}
+
+// blocked_pairwise<Real>, blocked.hpp:368-418
+int ref_blocked_pairwise(const double* d, uint64_t n, uint64_t b, int policy, int use_float,
+                         int32_t* u, double* c, double* times) {
+  return guarded([&] {
+    pald::PhaseTimes t;
+    const auto dm = make_d(d, n);
+    if (use_float) out_result(pald::blocked_pairwise<float>(dm, b, pol(policy), &t), u, c);
+    else out_result(pald::blocked_pairwise<double>(dm, b, pol(policy), &t), u, c);
+    out_times(t, times);
+  });
+}
+
+// blocked_triplet<Real>, blocked.hpp:424-477
+int ref_blocked_triplet(const double* d, uint64_t n, uint64_t bf, uint64_t bc, int policy,
+                        int use_float, int32_t* u, double* c, double* times) {
+  return guarded([&] {
+    pald::PhaseTimes t;
+    const auto dm = make_d(d, n);
+    if (use_float) out_result(pald::blocked_triplet<float>(dm, bf, bc, pol(policy), &t), u, c);
+    else out_result(pald::blocked_triplet<double>(dm, bf, bc, pol(policy), &t), u, c);
+    out_times(t, times);
+  });
+}
+
+// parallel_pairwise<Real>, parallel.hpp:159-222
+int ref_parallel_pairwise(const double* d, uint64_t n, uint64_t b, int workers, int policy,
+                          int use_float, int32_t* u, double* c, double* times) {
+  return guarded([&] {
+    pald::PhaseTimes t;
+    const auto dm = make_d(d, n);
+    const pald::ParallelPlan plan{workers, true};
+    if (use_float) out_result(pald::parallel_pairwise<float>(dm, b, plan, pol(policy), &t), u, c);
+    else out_result(pald::parallel_pairwise<double>(dm, b, plan, pol(policy), &t), u, c);
+    out_times(t, times);
+  });
+}
+
+// parallel_triplet<Real>, parallel.hpp:257-320
+int ref_parallel_triplet(const double* d, uint64_t n, uint64_t bf, uint64_t bc, int workers,
+                         int policy, int use_float, int32_t* u, double* c, double* times) {
+  return guarded([&] {
+    pald::PhaseTimes t;
+    const auto dm = make_d(d, n);
+    const pald::ParallelPlan plan{workers, true};
+    if (use_float)
+      out_result(pald::parallel_triplet<float>(dm, bf, bc, plan, pol(policy), &t), u, c);
+    else
+      out_result(pald::parallel_triplet<double>(dm, bf, bc, plan, pol(policy), &t), u, c);
+    out_times(t, times);
+  });
+}
+
+// fill_diagonal / normalize / local_depths, reference.hpp:213-241
+int ref_fill_diagonal(const int32_t* u, uint64_t n, double* c) {
+  return guarded([&] {
+    pald::FocusSizeMatrix f(n);
+    std::memcpy(f.sizes.data(), u, sizeof(int32_t) * n * n);
+    pald::CohesionMatrix cm(n);
+    std::memcpy(cm.values.data(), c, sizeof(double) * n * n);
+    pald::fill_diagonal(f, cm);
+    std::memcpy(c, cm.values.data(), sizeof(double) * n * n);
+  });
+}
+
+int ref_normalize_and_depths(double* c, uint64_t n, double* depths) {
+  return guarded([&] {
+    pald::CohesionMatrix cm(n);
+    std::memcpy(cm.values.data(), c, sizeof(double) * n * n);
+    pald::normalize(cm);
+    const auto ld = pald::local_depths(cm);
+    std::memcpy(c, cm.values.data(), sizeof(double) * n * n);
+    std::memcpy(depths, ld.depths.data(), sizeof(double) * n);
+  });
+}
+
+// default_block_config, blocked.hpp:510-518 (cache_bytes 0 = detect)
+int ref_default_block_config(uint64_t element_bytes, uint64_t cache_bytes, uint64_t* out3) {
+  return guarded([&] {
+    const auto cfg = cache_bytes ? pald::default_block_config(element_bytes, cache_bytes)
+                                 : pald::default_block_config(element_bytes);
+    out3[0] = cfg.b;
+    out3[1] = cfg.b_focus;
+    out3[2] = cfg.b_cohesion;
+  });
+}
+
+// Bounded timing sample of parallel_pairwise<float>: the driver loop of
+// parallel.hpp:178-215 run for the x-blocks x0 < x_limit only, with the
+// reference's own ThreadPool, worker_range, pair_block_focus and
+// pair_block_cohesion. The caller extrapolates by the exact fraction of
+// pair work covered. D is the fp32 matrix (to_real already applied).
+// Returns the seconds of the timed loop in *seconds.
+int ref_parallel_pairwise_prefix_f32(const float* dd, uint64_t n, uint64_t b, int workers,
+                                     uint64_t x_limit, double* seconds, int32_t* u_out,
+                                     float* c_out) {
+  return guarded([&] {
+    using pald::detail::worker_range;
+    const int p = workers;
+    std::vector<float> c(n * n, 0.0f);
+    std::vector<int32_t> u(n * n, 0);
+    std::vector<std::vector<int32_t>> partial(p, std::vector<int32_t>(b * b));
+    std::vector<float> recip(b * b);
+    pald::ThreadPool pool(p);
+    const double t0 = pald::detail::PhaseClock::now();
+    for (uint64_t x0 = 0; x0 < n && x0 < x_limit; x0 += b) {
+      const uint64_t x1 = std::min<uint64_t>(x0 + b, n);
+      for (uint64_t y0 = x0; y0 < n; y0 += b) {
+        const uint64_t y1 = std::min<uint64_t>(y0 + b, n);
+        const uint64_t ys = y1 - y0, cells = (x1 - x0) * ys;
+        pool.run([&](int w) {
+          auto [z0, z1] = worker_range(n, p, w);
+          std::fill(partial[w].begin(), partial[w].begin() + cells, 0);
+          pald::detail::pair_block_focus(dd, n, pald::Policy::Strict, x0, x1, y0, y1, z0, z1,
+                                         partial[w].data());
+        });
+        for (int w = 1; w < p; ++w)
+          for (uint64_t i = 0; i < cells; ++i) partial[0][i] += partial[w][i];
+        for (uint64_t x = x0; x < x1; ++x) {
+          const uint64_t ybeg = (y0 > x + 1) ? y0 : x + 1;
+          for (uint64_t y = ybeg; y < y1; ++y) {
+            const int32_t cnt = partial[0][(x - x0) * ys + (y - y0)];
+            u[x * n + y] = u[y * n + x] = cnt;
+            recip[(x - x0) * ys + (y - y0)] = 1.0f / static_cast<float>(cnt);
+          }
+        }
+        pool.run([&](int w) {
+          auto [z0, z1] = worker_range(n, p, w);
+          pald::detail::pair_block_cohesion(dd, n, pald::Policy::Strict,
+                                            pald::UpdateStyle::Masked, x0, x1, y0, y1, z0, z1,
+                                            recip.data(), c.data());
+        });
+      }
+    }
+    *seconds = pald::detail::PhaseClock::now() - t0;
+    if (u_out) std::memcpy(u_out, u.data(), sizeof(int32_t) * n * n);
+    if (c_out) std::memcpy(c_out, c.data(), sizeof(float) * n * n);
+  });
+}
+
+}  // extern "C"

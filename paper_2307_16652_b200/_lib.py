@@ -1,0 +1,135 @@
+"""ctypes binding of the C ABI (include/pald_gpu.h).
+
+This is the only way the Python mirror reaches the GPU: there is no CPU
+fallback. If the sm_100a library is missing, loading fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+from ._build import LIB_PATH
+
+PAIRWISE, TRIPLET = 0, 1
+STRICT, INCLUSIVE_SPLIT = 0, 1
+FLAG_SKIP_VALIDATION = 1
+FLAG_FORCE_EXACT = 2
+
+OK, ERR_VALIDATION, ERR_UNSUPPORTED, ERR_IO, ERR_CUDA, ERR_COMM = 0, 2, 3, 4, 5, 6
+
+# Every symbol include/pald_gpu.h declares (checked by tests/test_abi.py).
+EXPORTED_SYMBOLS = (
+    "pald_gpu_opts_init",
+    "pald_gpu_last_error",
+    "pald_gpu_abi_version",
+    "pald_gpu_cohesion_f32",
+    "pald_gpu_cohesion_f32_device",
+    "pald_gpu_plan_create",
+    "pald_gpu_plan_destroy",
+    "pald_gpu_plan_load",
+    "pald_gpu_plan_load_host",
+    "pald_gpu_plan_focus",
+    "pald_gpu_plan_cohesion",
+    "pald_gpu_plan_buffers",
+    "pald_gpu_plan_launches",
+    "pald_gpu_focus_work_prefix",
+    "pald_gpu_fill_diagonal",
+    "pald_gpu_points_to_distances",
+)
+
+
+class Opts(C.Structure):
+    _fields_ = [
+        ("struct_size", C.c_uint32),
+        ("algorithm", C.c_int32),
+        ("policy", C.c_int32),
+        ("device", C.c_int32),
+        ("block", C.c_uint64),
+        ("block_focus", C.c_uint64),
+        ("block_cohesion", C.c_uint64),
+        ("flags", C.c_uint32),
+        ("reserved", C.c_uint32),
+    ]
+
+
+class PhaseTimes(C.Structure):
+    _fields_ = [
+        ("focus_seconds", C.c_double),
+        ("cohesion_seconds", C.c_double),
+        ("overhead_seconds", C.c_double),
+        ("total_seconds", C.c_double),
+    ]
+
+
+class Buffers(C.Structure):
+    _fields_ = [
+        ("U", C.c_void_p),
+        ("W", C.c_void_p),
+        ("C", C.c_void_p),
+        ("ld", C.c_uint64),
+        ("n", C.c_uint64),
+        ("tile", C.c_uint64),
+        ("tiles_per_dim", C.c_uint64),
+        ("exact_path", C.c_int32),
+        ("reserved", C.c_int32),
+    ]
+
+
+_lib = None
+
+
+def load(path: Path | None = None) -> C.CDLL:
+    """Load libpald_gpu.so (building it first if the sources are newer)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        try:
+            from ._build import build
+
+            build()
+        except Exception as e:  # no nvcc on this host
+            raise RuntimeError(
+                f"{p} is missing and could not be built ({e}); the PaLD engine has no CPU fallback"
+            ) from e
+    lib = C.CDLL(str(p))
+    vp, u64, i32 = C.c_void_p, C.c_uint64, C.c_int
+    sig = {
+        "pald_gpu_opts_init": (None, [C.POINTER(Opts)]),
+        "pald_gpu_last_error": (C.c_char_p, []),
+        "pald_gpu_abi_version": (i32, []),
+        "pald_gpu_cohesion_f32": (i32, [vp, u64, C.POINTER(Opts), vp, vp, C.POINTER(PhaseTimes)]),
+        "pald_gpu_cohesion_f32_device": (i32, [vp, u64, u64, C.POINTER(Opts), vp, u64, vp, u64, vp]),
+        "pald_gpu_plan_create": (i32, [u64, C.POINTER(Opts), C.POINTER(vp)]),
+        "pald_gpu_plan_destroy": (i32, [vp]),
+        "pald_gpu_plan_load": (i32, [vp, vp, u64, vp]),
+        "pald_gpu_plan_load_host": (i32, [vp, vp, vp]),
+        "pald_gpu_plan_focus": (i32, [vp, u64, u64, vp]),
+        "pald_gpu_plan_cohesion": (i32, [vp, u64, u64, vp]),
+        "pald_gpu_plan_buffers": (i32, [vp, C.POINTER(Buffers)]),
+        "pald_gpu_plan_launches": (u64, [vp]),
+        "pald_gpu_focus_work_prefix": (C.c_double, [u64, u64]),
+        "pald_gpu_fill_diagonal": (i32, [vp, u64, u64, vp, vp]),
+        "pald_gpu_points_to_distances": (i32, [vp, u64, u64, vp, u64, vp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = lib
+    return lib
+
+
+def last_error() -> str:
+    msg = load().pald_gpu_last_error()
+    return msg.decode() if msg else ""
+
+
+def make_opts(algorithm: int = PAIRWISE, policy: int = STRICT, device: int = -1, block: int = 128,
+              block_focus: int = 128, block_cohesion: int = 128, flags: int = 0) -> Opts:
+    o = Opts()
+    load().pald_gpu_opts_init(C.byref(o))
+    o.algorithm, o.policy, o.device = algorithm, policy, device
+    o.block, o.block_focus, o.block_cohesion, o.flags = block, block_focus, block_cohesion, flags
+    return o

@@ -1,0 +1,602 @@
+// pald_gpu.cu -- host side of the C ABI declared in include/pald_gpu.h.
+//
+// Owns device workspaces ("plans"), the input range check / layout kernels,
+// the launch schedule over the pair-tile grid, CUDA-event phase timing and
+// the error mapping of the reference (types.hpp:14-25 -> status codes).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/pald_gpu.h"
+#include "pald_kernels.cuh"
+
+using namespace pald_gpu;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int set_error(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define PALD_CUDA(expr)                                                                  \
+  do {                                                                                   \
+    cudaError_t e_ = (expr);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return set_error(PALD_GPU_ERR_CUDA, "CUDA error %s at %s:%d (%s)",                 \
+                       cudaGetErrorString(e_), __FILE__, __LINE__, #expr);               \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// Range check / validation of the fp32 input (types.hpp:45-65 semantics,
+// evaluated on the fp32 values).
+struct Stats {
+  uint32_t min_pos_bits;   // smallest positive off-diagonal value (bits)
+  uint32_t max_bits;       // largest off-diagonal value (bits, non-NaN)
+  uint32_t diag_nonzero;
+  uint32_t offdiag_not_positive;  // 0, negative or NaN
+  uint32_t offdiag_zero;
+  uint32_t has_inf;
+  uint32_t has_nan;
+  uint32_t asymmetric;
+};
+
+__global__ void stats_kernel(const float* __restrict__ d, uint64_t ldd, int n, int check_sym,
+                             Stats* out) {
+  uint32_t mn = 0xffffffffu, mx = 0u, flags = 0u;
+  for (int r = blockIdx.x; r < n; r += gridDim.x) {
+    const float* row = d + (size_t)r * ldd;
+    for (int c = threadIdx.x; c < n; c += blockDim.x) {
+      const float v = row[c];
+      const uint32_t bits = __float_as_uint(v);
+      if (r == c) {
+        if ((bits & 0x7fffffffu) != 0u) flags |= 1u;
+        continue;
+      }
+      if (!(v > 0.f)) flags |= 2u;
+      if (v == 0.f) flags |= 4u;
+      if (isinf(v)) flags |= 8u;
+      if (isnan(v)) flags |= 16u;
+      if (v > 0.f) {
+        mn = min(mn, bits);
+        mx = max(mx, bits);
+      }
+      if (check_sym && r < c) {
+        const float t = d[(size_t)c * ldd + r];
+        if (__float_as_uint(t) != bits) flags |= 32u;
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    flags |= __shfl_xor_sync(0xffffffffu, flags, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&out->min_pos_bits, mn);
+    atomicMax(&out->max_bits, mx);
+    if (flags & 1u) atomicOr(&out->diag_nonzero, 1u);
+    if (flags & 2u) atomicOr(&out->offdiag_not_positive, 1u);
+    if (flags & 4u) atomicOr(&out->offdiag_zero, 1u);
+    if (flags & 8u) atomicOr(&out->has_inf, 1u);
+    if (flags & 16u) atomicOr(&out->has_nan, 1u);
+    if (flags & 32u) atomicOr(&out->asymmetric, 1u);
+  }
+}
+
+// Lays D out for the tile kernels: fast path -> fp32 scaled by 2^p (exact)
+// and its successor nu; exact path -> keys 2*bits and key+1. Diagonal is
+// canonicalised to +0 (types.hpp:51 accepts -0.0).
+__global__ void layout_kernel(const float* __restrict__ d, uint64_t ldd, int n, uint64_t ld,
+                              int fast, int p2, uint32_t* __restrict__ ds,
+                              uint32_t* __restrict__ dnu) {
+  for (int r = blockIdx.x; r < n; r += gridDim.x) {
+    for (int c = threadIdx.x; c < n; c += blockDim.x) {
+      float v = d[(size_t)r * ldd + c];
+      if (r == c) v = 0.f;
+      const uint32_t out = fast ? __float_as_uint(scalbnf(v, p2)) : 2u * (__float_as_uint(v) & 0x7fffffffu);
+      ds[(size_t)r * ld + c] = out;
+      dnu[(size_t)r * ld + c] = out + 1u;
+    }
+  }
+}
+
+__global__ void fill_diagonal_kernel(const int32_t* __restrict__ u, uint64_t ldu, int n,
+                                     double* __restrict__ out) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n) return;
+  double s = 0.0;
+  const int32_t* row = u + (size_t)x * ldu;
+  for (int y = 0; y < n; ++y)
+    if (y != x) s = __dadd_rn(s, __ddiv_rn(1.0, (double)row[y]));
+  out[x] = s;
+}
+
+__global__ void points_kernel(const double* __restrict__ p, int n, int dim, float* __restrict__ d,
+                              uint64_t ldd) {
+  for (int r = blockIdx.x; r < n; r += gridDim.x) {
+    for (int c = threadIdx.x; c < n; c += blockDim.x) {
+      float out = 0.f;
+      if (r != c) {
+        // each unordered pair evaluated in the same (min, max) order so D is
+        // exactly symmetric (ingest.hpp:303-322)
+        const int a = min(r, c), b = max(r, c);
+        double s = 0.0;
+        for (int k = 0; k < dim; ++k) {
+          const double diff = __dsub_rn(p[(size_t)a * dim + k], p[(size_t)b * dim + k]);
+          s = __dadd_rn(s, __dmul_rn(diff, diff));
+        }
+        out = __double2float_rn(__dsqrt_rn(s));
+      }
+      d[(size_t)r * ldd + c] = out;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+int make_map(CUtensorMap* map, const void* base, uint64_t n, uint64_t ld) {
+  auto encode = get_encode();
+  if (!encode) return set_error(PALD_GPU_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {n, n};
+  cuuint64_t strides[1] = {ld * 4};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kTile), static_cast<cuuint32_t>(kBK)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims,
+                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(PALD_GPU_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return PALD_GPU_OK;
+}
+
+template <int PASS, bool A_NU, bool B_NU, bool T_NU, bool ZD, bool FAST>
+int launch_tile(const CUtensorMap& md, const CUtensorMap& mnu, const CUtensorMap& mw,
+                const KernelArgs& a, int grid, cudaStream_t s) {
+  auto k = pald_tile_kernel<PASS, A_NU, B_NU, T_NU, ZD, FAST>;
+  static bool attr_done[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!attr_done[dev & 63]) {
+    PALD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes(PASS)));
+    attr_done[dev & 63] = true;
+  }
+  k<<<grid, kThreads, smem_bytes(PASS), s>>>(md, mnu, mw, a);
+  PALD_CUDA(cudaGetLastError());
+  return PALD_GPU_OK;
+}
+
+uint64_t round_up(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
+
+int check_opts(const pald_gpu_opts* o) {
+  if (!o) return set_error(PALD_GPU_ERR_VALIDATION, "null options");
+  if (o->struct_size != sizeof(pald_gpu_opts))
+    return set_error(PALD_GPU_ERR_VALIDATION, "pald_gpu_opts.struct_size mismatch (%u != %zu)",
+                     o->struct_size, sizeof(pald_gpu_opts));
+  if (o->algorithm != PALD_GPU_PAIRWISE && o->algorithm != PALD_GPU_TRIPLET)
+    return set_error(PALD_GPU_ERR_VALIDATION, "unknown algorithm %d", o->algorithm);
+  if (o->policy != PALD_GPU_STRICT && o->policy != PALD_GPU_INCLUSIVE_SPLIT)
+    return set_error(PALD_GPU_ERR_VALIDATION, "unknown policy %d", o->policy);
+  // blocked.hpp:429-431, parallel.hpp:262-265 check policy before sizes.
+  if (o->algorithm == PALD_GPU_TRIPLET) {
+    if (o->policy != PALD_GPU_STRICT)
+      return set_error(PALD_GPU_ERR_UNSUPPORTED, "the triplet algorithm supports the strict policy only");
+    if (o->block_focus < 1 || o->block_cohesion < 1)
+      return set_error(PALD_GPU_ERR_VALIDATION, "triplet block sizes must be >= 1");
+  } else {
+    if (o->block < 1) return set_error(PALD_GPU_ERR_VALIDATION, "pairwise block size must be >= 1");
+    if (o->policy != PALD_GPU_STRICT)
+      return set_error(PALD_GPU_ERR_UNSUPPORTED,
+                       "the GPU engine implements the strict policy only (InclusiveSplit pending)");
+  }
+  return PALD_GPU_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+struct pald_gpu_plan {
+  int device = 0;
+  uint64_t n = 0, ld = 0, nb = 0;
+  int algorithm = 0;
+  uint32_t flags = 0;
+  uint32_t* ds = nullptr;
+  uint32_t* dnu = nullptr;
+  int32_t* u = nullptr;
+  float* w = nullptr;
+  float* c = nullptr;
+  Stats* stats = nullptr;
+  Stats* stats_host = nullptr;
+  CUtensorMap tm_d, tm_dnu, tm_w;
+  bool loaded = false;
+  bool exact = false;
+  uint64_t launches = 0;
+
+  ~pald_gpu_plan() {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    cudaFree(ds);
+    cudaFree(dnu);
+    cudaFree(u);
+    cudaFree(w);
+    cudaFree(c);
+    cudaFree(stats);
+    cudaFreeHost(stats_host);
+    cudaSetDevice(prev);
+  }
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (dev >= 0 && dev != prev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+int plan_alloc(pald_gpu_plan* p) {
+  const size_t bytes = p->n * p->ld * 4;
+  PALD_CUDA(cudaMalloc(&p->ds, bytes));
+  PALD_CUDA(cudaMalloc(&p->dnu, bytes));
+  PALD_CUDA(cudaMalloc(&p->u, bytes));
+  PALD_CUDA(cudaMalloc(&p->w, bytes));
+  PALD_CUDA(cudaMalloc(&p->c, bytes));
+  PALD_CUDA(cudaMemset(p->ds, 0, bytes));
+  PALD_CUDA(cudaMemset(p->dnu, 0, bytes));
+  PALD_CUDA(cudaMemset(p->c, 0, bytes));
+  PALD_CUDA(cudaMalloc(&p->stats, sizeof(Stats)));
+  PALD_CUDA(cudaMallocHost(&p->stats_host, sizeof(Stats)));
+  int rc;
+  if ((rc = make_map(&p->tm_d, p->ds, p->n, p->ld))) return rc;
+  if ((rc = make_map(&p->tm_dnu, p->dnu, p->n, p->ld))) return rc;
+  if ((rc = make_map(&p->tm_w, p->w, p->n, p->ld))) return rc;
+  return PALD_GPU_OK;
+}
+
+int grid_rows(uint64_t n) { return (int)std::min<uint64_t>(n, 148ull * 16); }
+
+int plan_load_impl(pald_gpu_plan* p, const float* dD, uint64_t ldd, cudaStream_t s) {
+  const int n = (int)p->n;
+  Stats init{};
+  init.min_pos_bits = 0xffffffffu;
+  *p->stats_host = init;
+  PALD_CUDA(cudaMemcpyAsync(p->stats, p->stats_host, sizeof(Stats), cudaMemcpyHostToDevice, s));
+  const bool validate = !(p->flags & PALD_GPU_FLAG_SKIP_VALIDATION);
+  stats_kernel<<<grid_rows(p->n), 256, 0, s>>>(dD, ldd, n, validate ? 1 : 0, p->stats);
+  PALD_CUDA(cudaGetLastError());
+  ++p->launches;
+  PALD_CUDA(cudaMemcpyAsync(p->stats_host, p->stats, sizeof(Stats), cudaMemcpyDeviceToHost, s));
+  PALD_CUDA(cudaStreamSynchronize(s));
+  const Stats st = *p->stats_host;
+  if (validate) {
+    if (st.diag_nonzero) return set_error(PALD_GPU_ERR_VALIDATION, "distance matrix diagonal entry is nonzero");
+    if (st.offdiag_not_positive)
+      return set_error(PALD_GPU_ERR_VALIDATION,
+                       "off-diagonal distance must be positive (duplicate points are rejected)");
+    if (st.asymmetric) return set_error(PALD_GPU_ERR_VALIDATION, "distance matrix not symmetric");
+  }
+  // Range check for the FFMA.SAT compare path: scale by 2^p2 so that the
+  // largest value lies in [0.5, 1); all values must stay >= 2^-102.
+  bool fast = !(p->flags & PALD_GPU_FLAG_FORCE_EXACT) && !st.offdiag_zero && !st.has_inf &&
+              !st.has_nan && st.min_pos_bits != 0xffffffffu;
+  int p2 = 0;
+  if (fast) {
+    float vmax, vmin;
+    uint32_t mb = st.max_bits, nbits = st.min_pos_bits;
+    std::memcpy(&vmax, &mb, 4);
+    std::memcpy(&vmin, &nbits, 4);
+    int e = 0;
+    std::frexp(vmax, &e);  // vmax = f * 2^e, f in [0.5, 1)
+    p2 = -e;
+    const double scaled_min = std::ldexp((double)vmin, p2);
+    if (!(scaled_min >= std::ldexp(1.0, -102))) fast = false;
+  }
+  p->exact = !fast;
+  layout_kernel<<<grid_rows(p->n), 256, 0, s>>>(dD, ldd, n, p->ld, fast ? 1 : 0, p2, p->ds,
+                                                       p->dnu);
+  PALD_CUDA(cudaGetLastError());
+  ++p->launches;
+  PALD_CUDA(cudaMemsetAsync(p->u, 0, p->n * p->ld * 4, s));
+  PALD_CUDA(cudaMemsetAsync(p->w, 0, p->n * p->ld * 4, s));
+  p->loaded = true;
+  return PALD_GPU_OK;
+}
+
+int plan_focus_impl(pald_gpu_plan* p, uint64_t tr0, uint64_t tr1, cudaStream_t s) {
+  if (!p->loaded) return set_error(PALD_GPU_ERR_VALIDATION, "plan has no distances loaded");
+  tr1 = std::min(tr1, p->nb);
+  if (tr0 >= tr1) return PALD_GPU_OK;
+  uint64_t tiles = 0;
+  for (uint64_t t = tr0; t < tr1; ++t) tiles += p->nb - t;
+  KernelArgs a{p->ds, p->u, p->w, p->c, (int)p->n, (int)p->ld, (int)p->nb, (int)tr0, (int)tr1};
+  int rc;
+  const bool tri = p->algorithm == PALD_GPU_TRIPLET;
+  if (!p->exact) {
+    rc = tri ? launch_tile<0, true, true, true, false, true>(p->tm_d, p->tm_dnu, p->tm_w, a, (int)tiles, s)
+             : launch_tile<0, false, false, false, false, true>(p->tm_d, p->tm_dnu, p->tm_w, a, (int)tiles, s);
+  } else {
+    rc = tri ? launch_tile<0, true, true, true, false, false>(p->tm_d, p->tm_dnu, p->tm_w, a, (int)tiles, s)
+             : launch_tile<0, false, false, false, false, false>(p->tm_d, p->tm_dnu, p->tm_w, a, (int)tiles, s);
+  }
+  if (rc == PALD_GPU_OK) ++p->launches;
+  return rc;
+}
+
+int plan_cohesion_impl(pald_gpu_plan* p, uint64_t row0, uint64_t row1, cudaStream_t s) {
+  if (!p->loaded) return set_error(PALD_GPU_ERR_VALIDATION, "plan has no distances loaded");
+  row1 = std::min(row1, p->n);
+  if (row0 >= row1) return PALD_GPU_OK;
+  if (row0 % kTile != 0 || (row1 % kTile != 0 && row1 != p->n))
+    return set_error(PALD_GPU_ERR_VALIDATION, "cohesion row range must be aligned to %d", kTile);
+  const uint64_t tr0 = row0 / kTile, tr1 = (row1 + kTile - 1) / kTile;
+  const uint64_t tiles = (tr1 - tr0) * p->nb;
+  KernelArgs a{p->ds, p->u, p->w, p->c, (int)p->n, (int)p->ld, (int)p->nb, (int)tr0, (int)tr1};
+  int rc;
+  const bool tri = p->algorithm == PALD_GPU_TRIPLET;
+  if (!p->exact) {
+    rc = tri ? launch_tile<1, true, true, false, true, true>(p->tm_d, p->tm_dnu, p->tm_w, a, (int)tiles, s)
+             : launch_tile<1, false, true, false, false, true>(p->tm_d, p->tm_dnu, p->tm_w, a, (int)tiles, s);
+  } else {
+    rc = tri ? launch_tile<1, true, true, false, true, false>(p->tm_d, p->tm_dnu, p->tm_w, a, (int)tiles, s)
+             : launch_tile<1, false, true, false, false, false>(p->tm_d, p->tm_dnu, p->tm_w, a, (int)tiles, s);
+  }
+  if (rc == PALD_GPU_OK) ++p->launches;
+  return rc;
+}
+
+// One cached plan per device for the one-shot APIs.
+struct Cache {
+  std::mutex mu;
+  std::unique_ptr<pald_gpu_plan> plan[64];
+};
+Cache& cache() {
+  static Cache c;
+  return c;
+}
+
+int get_cached_plan(int dev, uint64_t n, const pald_gpu_opts* o, pald_gpu_plan** out) {
+  auto& slot = cache().plan[dev & 63];
+  if (!slot || slot->n != n) {
+    slot.reset();
+    pald_gpu_plan* p = nullptr;
+    int rc = pald_gpu_plan_create(n, o, &p);
+    if (rc) return rc;
+    slot.reset(p);
+  }
+  slot->algorithm = o->algorithm;
+  slot->flags = o->flags;
+  slot->loaded = false;
+  *out = slot.get();
+  return PALD_GPU_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+extern "C" {
+
+void pald_gpu_opts_init(pald_gpu_opts* o) {
+  std::memset(o, 0, sizeof(*o));
+  o->struct_size = sizeof(pald_gpu_opts);
+  o->algorithm = PALD_GPU_PAIRWISE;
+  o->policy = PALD_GPU_STRICT;
+  o->device = -1;
+  o->block = o->block_focus = o->block_cohesion = kTile;
+}
+
+const char* pald_gpu_last_error(void) { return g_last_error.c_str(); }
+
+int pald_gpu_abi_version(void) { return PALD_GPU_ABI_VERSION; }
+
+double pald_gpu_focus_work_prefix(uint64_t n, uint64_t tile_rows) {
+  const uint64_t nb = (n + kTile - 1) / kTile;
+  const double total = (double)nb * (nb + 1) / 2.0;
+  double pre = 0;
+  for (uint64_t t = 0; t < std::min(tile_rows, nb); ++t) pre += (double)(nb - t);
+  return pre / total;
+}
+
+int pald_gpu_plan_create(uint64_t n, const pald_gpu_opts* o, pald_gpu_plan** out) {
+  int rc = check_opts(o);
+  if (rc) return rc;
+  if (!out) return set_error(PALD_GPU_ERR_VALIDATION, "null plan output");
+  if (n < 2) return set_error(PALD_GPU_ERR_VALIDATION, "distance matrix needs n >= 2, got n=%llu", (unsigned long long)n);
+  if (n > (1ull << 24)) return set_error(PALD_GPU_ERR_VALIDATION, "n=%llu exceeds 2^24 (fp32 focus counts)", (unsigned long long)n);
+  int dev = o->device;
+  if (dev < 0) PALD_CUDA(cudaGetDevice(&dev));
+  DeviceGuard g(dev);
+  int major = 0;
+  PALD_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  if (major < 10) return set_error(PALD_GPU_ERR_CUDA, "device %d is not sm_100-class", dev);
+  std::unique_ptr<pald_gpu_plan> p(new pald_gpu_plan());
+  p->device = dev;
+  p->n = n;
+  p->ld = round_up(n, 32);
+  p->nb = (n + kTile - 1) / kTile;
+  p->algorithm = o->algorithm;
+  p->flags = o->flags;
+  if ((rc = plan_alloc(p.get()))) return rc;
+  *out = p.release();
+  return PALD_GPU_OK;
+}
+
+int pald_gpu_plan_destroy(pald_gpu_plan* p) {
+  delete p;
+  return PALD_GPU_OK;
+}
+
+int pald_gpu_plan_load(pald_gpu_plan* p, const float* dD, uint64_t ldd, void* stream) {
+  if (!p || !dD) return set_error(PALD_GPU_ERR_VALIDATION, "null argument");
+  if (ldd < p->n) return set_error(PALD_GPU_ERR_VALIDATION, "ldd < n");
+  DeviceGuard g(p->device);
+  return plan_load_impl(p, dD, ldd, static_cast<cudaStream_t>(stream));
+}
+
+int pald_gpu_plan_load_host(pald_gpu_plan* p, const float* D, void* stream) {
+  if (!p || !D) return set_error(PALD_GPU_ERR_VALIDATION, "null argument");
+  DeviceGuard g(p->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // Stage the dense host matrix in the C buffer (free until pass 2).
+  PALD_CUDA(cudaMemcpy2DAsync(p->c, p->ld * 4, D, p->n * 4, p->n * 4, p->n, cudaMemcpyHostToDevice, s));
+  return plan_load_impl(p, p->c, p->ld, s);
+}
+
+int pald_gpu_plan_focus(pald_gpu_plan* p, uint64_t tr0, uint64_t tr1, void* stream) {
+  if (!p) return set_error(PALD_GPU_ERR_VALIDATION, "null plan");
+  DeviceGuard g(p->device);
+  return plan_focus_impl(p, tr0, tr1, static_cast<cudaStream_t>(stream));
+}
+
+int pald_gpu_plan_cohesion(pald_gpu_plan* p, uint64_t r0, uint64_t r1, void* stream) {
+  if (!p) return set_error(PALD_GPU_ERR_VALIDATION, "null plan");
+  DeviceGuard g(p->device);
+  return plan_cohesion_impl(p, r0, r1, static_cast<cudaStream_t>(stream));
+}
+
+int pald_gpu_plan_buffers(const pald_gpu_plan* p, pald_gpu_buffers* out) {
+  if (!p || !out) return set_error(PALD_GPU_ERR_VALIDATION, "null argument");
+  out->U = p->u;
+  out->W = p->w;
+  out->C = p->c;
+  out->ld = p->ld;
+  out->n = p->n;
+  out->tile = kTile;
+  out->tiles_per_dim = p->nb;
+  out->exact_path = p->exact ? 1 : 0;
+  out->reserved = 0;
+  return PALD_GPU_OK;
+}
+
+uint64_t pald_gpu_plan_launches(const pald_gpu_plan* p) { return p ? p->launches : 0; }
+
+int pald_gpu_cohesion_f32_device(const float* dD, uint64_t ldd, uint64_t n,
+                                 const pald_gpu_opts* o, int32_t* dU, uint64_t ldu, float* dC,
+                                 uint64_t ldc, void* stream) {
+  int rc = check_opts(o);
+  if (rc) return rc;
+  if (!dD || !dC) return set_error(PALD_GPU_ERR_VALIDATION, "null device pointer");
+  if (ldd < n || ldc < n || (dU && ldu < n)) return set_error(PALD_GPU_ERR_VALIDATION, "leading dimension < n");
+  int dev = o->device;
+  if (dev < 0) PALD_CUDA(cudaGetDevice(&dev));
+  DeviceGuard g(dev);
+  std::lock_guard<std::mutex> lk(cache().mu);
+  pald_gpu_plan* p = nullptr;
+  if ((rc = get_cached_plan(dev, n, o, &p))) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if ((rc = plan_load_impl(p, dD, ldd, s))) return rc;
+  if ((rc = plan_focus_impl(p, 0, p->nb, s))) return rc;
+  if ((rc = plan_cohesion_impl(p, 0, n, s))) return rc;
+  if (dU) PALD_CUDA(cudaMemcpy2DAsync(dU, ldu * 4, p->u, p->ld * 4, n * 4, n, cudaMemcpyDeviceToDevice, s));
+  PALD_CUDA(cudaMemcpy2DAsync(dC, ldc * 4, p->c, p->ld * 4, n * 4, n, cudaMemcpyDeviceToDevice, s));
+  return PALD_GPU_OK;
+}
+
+int pald_gpu_cohesion_f32(const float* D, uint64_t n, const pald_gpu_opts* o, int32_t* U_out,
+                          float* C_out, pald_gpu_phase_times* times) {
+  int rc = check_opts(o);
+  if (rc) return rc;
+  if (!D || !C_out) return set_error(PALD_GPU_ERR_VALIDATION, "null host pointer");
+  if (n < 2) return set_error(PALD_GPU_ERR_VALIDATION, "distance matrix needs n >= 2, got n=%llu", (unsigned long long)n);
+  int dev = o->device;
+  if (dev < 0) PALD_CUDA(cudaGetDevice(&dev));
+  DeviceGuard g(dev);
+  std::lock_guard<std::mutex> lk(cache().mu);
+  const auto t_start = std::chrono::steady_clock::now();
+  pald_gpu_plan* p = nullptr;
+  if ((rc = get_cached_plan(dev, n, o, &p))) return rc;
+  cudaStream_t s = nullptr;
+  PALD_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  struct StreamGuard {
+    cudaStream_t s;
+    ~StreamGuard() { cudaStreamDestroy(s); }
+  } sg{s};
+  cudaEvent_t ev[4];
+  for (auto& e : ev) PALD_CUDA(cudaEventCreate(&e));
+  struct EvGuard {
+    cudaEvent_t* e;
+    ~EvGuard() {
+      for (int i = 0; i < 4; ++i) cudaEventDestroy(e[i]);
+    }
+  } eg{ev};
+  PALD_CUDA(cudaEventRecord(ev[0], s));
+  if ((rc = pald_gpu_plan_load_host(p, D, s))) return rc;
+  PALD_CUDA(cudaEventRecord(ev[1], s));
+  if ((rc = plan_focus_impl(p, 0, p->nb, s))) return rc;
+  PALD_CUDA(cudaEventRecord(ev[2], s));
+  if ((rc = plan_cohesion_impl(p, 0, n, s))) return rc;
+  PALD_CUDA(cudaEventRecord(ev[3], s));
+  if (U_out) PALD_CUDA(cudaMemcpy2DAsync(U_out, n * 4, p->u, p->ld * 4, n * 4, n, cudaMemcpyDeviceToHost, s));
+  PALD_CUDA(cudaMemcpy2DAsync(C_out, n * 4, p->c, p->ld * 4, n * 4, n, cudaMemcpyDeviceToHost, s));
+  PALD_CUDA(cudaStreamSynchronize(s));
+  if (times) {
+    float f = 0, c = 0;
+    PALD_CUDA(cudaEventElapsedTime(&f, ev[1], ev[2]));
+    PALD_CUDA(cudaEventElapsedTime(&c, ev[2], ev[3]));
+    const double total =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+    times->focus_seconds += f * 1e-3;
+    times->cohesion_seconds += c * 1e-3;
+    times->overhead_seconds += std::max(0.0, total - (f + c) * 1e-3);
+    times->total_seconds = total;
+  }
+  return PALD_GPU_OK;
+}
+
+int pald_gpu_fill_diagonal(const int32_t* dU, uint64_t ldu, uint64_t n, double* diag_out,
+                           void* stream) {
+  if (!dU || !diag_out) return set_error(PALD_GPU_ERR_VALIDATION, "null device pointer");
+  fill_diagonal_kernel<<<(unsigned)((n + 127) / 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      dU, ldu, (int)n, diag_out);
+  PALD_CUDA(cudaGetLastError());
+  return PALD_GPU_OK;
+}
+
+int pald_gpu_points_to_distances(const double* dP, uint64_t n, uint64_t dim, float* dD,
+                                 uint64_t ldd, void* stream) {
+  if (!dP || !dD) return set_error(PALD_GPU_ERR_VALIDATION, "null device pointer");
+  if (n < 2) return set_error(PALD_GPU_ERR_VALIDATION, "point cloud needs at least 2 points");
+  if (dim < 1) return set_error(PALD_GPU_ERR_VALIDATION, "points need at least one coordinate");
+  if (ldd < n) return set_error(PALD_GPU_ERR_VALIDATION, "ldd < n");
+  points_kernel<<<grid_rows(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(dP, (int)n, (int)dim, dD, ldd);
+  PALD_CUDA(cudaGetLastError());
+  return PALD_GPU_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,165 @@
+"""Device-resident engine: a staged plan over the C ABI, with torch as the
+memory/stream plumbing.
+
+``Engine`` wraps ``pald_gpu_plan`` (include/pald_gpu.h). Its buffers are
+exposed to torch as zero-copy views through ``__cuda_array_interface__`` so
+that torch.distributed (NCCL) can reduce/gather them in the multi-GPU
+driver (paper_2307_16652_b200.distributed).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _lib
+from .api import _raise_for
+
+
+class _DeviceView:
+    """Minimal __cuda_array_interface__ exporter over plan-owned memory."""
+
+    def __init__(self, ptr: int, shape, typestr: str, strides, owner):
+        self._owner = owner  # keeps the plan alive while a view exists
+        self.__cuda_array_interface__ = {
+            "shape": tuple(shape),
+            "typestr": typestr,
+            "data": (int(ptr), False),
+            "strides": tuple(strides),
+            "version": 3,
+        }
+
+
+class Engine:
+    """One PaLD problem of size n on one GPU.
+
+    Steps (each asynchronous on ``stream`` unless noted):
+      load(D)                 validate + range check (one small sync) + layout
+      focus(tr0, tr1)         pass 1 over pair-tile rows [tr0, tr1)
+      cohesion(r0, r1)        pass 2 over C rows [r0, r1)
+    Views: ``U``, ``W``, ``C`` (n x n, strided by ld).
+    """
+
+    def __init__(self, n: int, algorithm: str = "pairwise", device: int | None = None,
+                 force_exact: bool = False, skip_validation: bool = False):
+        self.lib = _lib.load()
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = int(device)
+        self.n = int(n)
+        self.algorithm = algorithm
+        alg = {"pairwise": _lib.PAIRWISE, "triplet": _lib.TRIPLET}[algorithm]
+        flags = (_lib.FLAG_FORCE_EXACT if force_exact else 0) | (
+            _lib.FLAG_SKIP_VALIDATION if skip_validation else 0)
+        opts = _lib.make_opts(algorithm=alg, device=self.device, flags=flags)
+        self._plan = C.c_void_p()
+        _raise_for(self.lib.pald_gpu_plan_create(self.n, C.byref(opts), C.byref(self._plan)))
+        b = _lib.Buffers()
+        _raise_for(self.lib.pald_gpu_plan_buffers(self._plan, C.byref(b)))
+        self.ld = int(b.ld)
+        self.tile = int(b.tile)
+        self.tiles_per_dim = int(b.tiles_per_dim)
+        self._ptrs = (b.U, b.W, b.C)
+
+    def __del__(self):
+        plan = getattr(self, "_plan", None)
+        if plan is not None and plan.value:
+            self.lib.pald_gpu_plan_destroy(plan)
+            self._plan = None
+
+    # -- views ---------------------------------------------------------
+    def _view(self, ptr: int, typestr: str, dtype) -> torch.Tensor:
+        n, ld = self.n, self.ld
+        v = _DeviceView(ptr, (n, n), typestr, (ld * 4, 4), self)
+        return torch.as_tensor(v, device=f"cuda:{self.device}")
+
+    @property
+    def U(self) -> torch.Tensor:
+        return self._view(self._ptrs[0], "<i4", torch.int32)
+
+    @property
+    def W(self) -> torch.Tensor:
+        return self._view(self._ptrs[1], "<f4", torch.float32)
+
+    @property
+    def C(self) -> torch.Tensor:
+        return self._view(self._ptrs[2], "<f4", torch.float32)
+
+    def full_U(self) -> torch.Tensor:
+        """The whole ld-strided U buffer as a flat tensor (for collectives)."""
+        v = _DeviceView(self._ptrs[0], (self.n * self.ld,), "<i4", (4,), self)
+        return torch.as_tensor(v, device=f"cuda:{self.device}")
+
+    def full_W(self) -> torch.Tensor:
+        v = _DeviceView(self._ptrs[1], (self.n * self.ld,), "<f4", (4,), self)
+        return torch.as_tensor(v, device=f"cuda:{self.device}")
+
+    def row_block_C(self, r0: int, r1: int) -> torch.Tensor:
+        v = _DeviceView(self._ptrs[2] + r0 * self.ld * 4, ((r1 - r0) * self.ld,), "<f4", (4,), self)
+        return torch.as_tensor(v, device=f"cuda:{self.device}")
+
+    # -- steps -----------------------------------------------------------
+    @staticmethod
+    def _stream(stream) -> int:
+        if stream is None:
+            stream = torch.cuda.current_stream()
+        return stream.cuda_stream
+
+    def load(self, D: torch.Tensor, stream=None) -> None:
+        if D.dtype != torch.float32 or not D.is_cuda or D.dim() != 2:
+            raise TypeError("D must be a 2-D float32 CUDA tensor")
+        if D.shape[0] != self.n or D.shape[1] != self.n or D.stride(1) != 1:
+            raise ValueError("D must be n x n with unit column stride")
+        _raise_for(self.lib.pald_gpu_plan_load(self._plan, D.data_ptr(), D.stride(0),
+                                               self._stream(stream)))
+
+    def load_host(self, D, stream=None) -> None:
+        """D: C-contiguous float32 host array/tensor (pinned for full speed)."""
+        ptr = D.data_ptr() if isinstance(D, torch.Tensor) else D.ctypes.data
+        _raise_for(self.lib.pald_gpu_plan_load_host(self._plan, ptr, self._stream(stream)))
+
+    def focus(self, tile_row_begin: int = 0, tile_row_end: int | None = None, stream=None) -> None:
+        if tile_row_end is None:
+            tile_row_end = self.tiles_per_dim
+        _raise_for(self.lib.pald_gpu_plan_focus(self._plan, tile_row_begin, tile_row_end,
+                                                self._stream(stream)))
+
+    def cohesion(self, row_begin: int = 0, row_end: int | None = None, stream=None) -> None:
+        if row_end is None:
+            row_end = self.n
+        _raise_for(self.lib.pald_gpu_plan_cohesion(self._plan, row_begin, row_end,
+                                                   self._stream(stream)))
+
+    def run(self, D: torch.Tensor, stream=None) -> None:
+        self.load(D, stream)
+        self.focus(stream=stream)
+        self.cohesion(stream=stream)
+
+    @property
+    def exact_path(self) -> bool:
+        b = _lib.Buffers()
+        _raise_for(self.lib.pald_gpu_plan_buffers(self._plan, C.byref(b)))
+        return bool(b.exact_path)
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.pald_gpu_plan_launches(self._plan))
+
+
+def points_to_distances(points: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Euclidean D of a float64 CUDA point cloud (ingest.hpp:303-322) on the GPU."""
+    lib = _lib.load()
+    if points.dtype != torch.float64 or not points.is_cuda:
+        raise TypeError("points must be a float64 CUDA tensor")
+    points = points.contiguous()
+    n, dim = points.shape
+    if out is None:
+        out = torch.empty((n, n), dtype=torch.float32, device=points.device)
+    s = (stream or torch.cuda.current_stream(points.device)).cuda_stream
+    _raise_for(lib.pald_gpu_points_to_distances(points.data_ptr(), n, dim, out.data_ptr(),
+                                                out.stride(0), s))
+    return out
+
+
+def work_prefix(n: int, tile_rows: int) -> float:
+    return float(_lib.load().pald_gpu_focus_work_prefix(n, tile_rows))

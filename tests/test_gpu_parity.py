@@ -1,0 +1,74 @@
+"""GPU parity: the sm_100a engine (through the C ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star):
+  * U bit-exact (pairwise and triplet, strict-< ties included);
+  * pairwise C bit-exact vs the fp32 reference order (blocked_pairwise<float>,
+    restated in oracle/pald_oracle.c) -- stronger than the 1e-5 bar;
+  * triplet C: max rel_diff (helpers.hpp:30-33 convention) <= 1e-5 vs the
+    fp64 oracle, row sums within 1e-5.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from helpers import int_upper, max_rel_diff, random_upper
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+def run_gpu(d: np.ndarray, algorithm: str, force_exact: bool = False):
+    from paper_2307_16652_b200 import _lib
+    from paper_2307_16652_b200.api import _raise_for
+
+    lib = _lib.load()
+    alg = _lib.PAIRWISE if algorithm == "pairwise" else _lib.TRIPLET
+    flags = _lib.FLAG_FORCE_EXACT if force_exact else 0
+    opts = _lib.make_opts(algorithm=alg, flags=flags)
+    d = np.ascontiguousarray(d, np.float32)
+    n = d.shape[0]
+    u = np.empty((n, n), np.int32)
+    c = np.empty((n, n), np.float32)
+    _raise_for(lib.pald_gpu_cohesion_f32(d.ctypes.data, n, C.byref(opts), u.ctypes.data,
+                                         c.ctypes.data, None))
+    return u, c
+
+
+SIZES = [2, 3, 5, 16, 33, 65, 127, 128, 129, 200, 257]
+
+
+@pytest.mark.parametrize("exact", [False, True])
+@pytest.mark.parametrize("n", SIZES)
+def test_pairwise_bit_exact_random(oracle, n, exact):
+    d = random_upper(n, 1000 + n)
+    u_ref, c_ref = oracle.pairwise_f32(d)
+    u, c = run_gpu(d, "pairwise", exact)
+    assert np.array_equal(u, u_ref)
+    assert np.array_equal(c.view(np.uint32), c_ref.view(np.uint32))
+
+
+@pytest.mark.parametrize("exact", [False, True])
+@pytest.mark.parametrize("n", [16, 65, 130, 300])
+def test_pairwise_bit_exact_ties(oracle, n, exact):
+    d = int_upper(n, 77 + n)
+    u_ref, c_ref = oracle.pairwise_f32(d)
+    u, c = run_gpu(d, "pairwise", exact)
+    assert np.array_equal(u, u_ref)
+    assert np.array_equal(c.view(np.uint32), c_ref.view(np.uint32))
+
+
+@pytest.mark.parametrize("exact", [False, True])
+@pytest.mark.parametrize("n,kind", [(3, "rand"), (5, "rand"), (33, "rand"), (65, "ties"),
+                                    (129, "rand"), (200, "ties"), (257, "rand")])
+def test_triplet(oracle, n, kind, exact):
+    d = random_upper(n, 2000 + n) if kind == "rand" else int_upper(n, 3000 + n)
+    u_ref, c_ref = oracle.triplet_f64(d)
+    u, c = run_gpu(d, "triplet", exact)
+    assert np.array_equal(u, u_ref)
+    assert max_rel_diff(c, c_ref) <= TOL
+    assert np.all(np.diagonal(c) == 0.0)
+    rs_ref = c_ref.sum(1)
+    rs = c.astype(np.float64).sum(1)
+    assert np.max(np.abs(rs - rs_ref) / np.maximum(rs_ref, 1.0)) <= TOL
