@@ -1,0 +1,481 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 PaLD engine (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Metric (BASELINE.json): PaLD cohesion triplets/s = n^3 / t, plus the
+fraction of the B200 ALU-issue roofline. Workload: BASELINE.json config 5
+(pairwise, n = 32768, points i.i.d. U[0,1)^3, fp32 Euclidean D), the config
+the metric is quoted on for 1-8 GPUs; it fits one GPU. A step is one full
+pass of the hot path over that input: range check + layout of D, pass 1
+(focus sizes U and W = 1/U), pass 2 (cohesion C), plus -- for N > 1 -- the
+NCCL exchange of U/W between the passes and the all-gather of C.
+
+* ``value``     device-resident throughput (D already in HBM), time = max over
+                ranks of the CUDA-event step time.
+* ``e2e``       the same metric through the reference-facing C ABI call
+                (pald_gpu_cohesion_f32) with pinned HOST buffers: H2D of D and
+                D2H of U and C inside the timed region (rank 0 / N = 1 path).
+* ``roofline``  dominant kernel (pass 2, cohesion): algorithmic ops per
+                launch / its CUDA-event duration vs. the issue peak
+                148 SM x 128 lanes x sm_max_mhz (MEASURED_PEAKS.json).
+* ``cpu_baseline`` the UNMODIFIED reference (oracle/_ref, parallel_pairwise
+                <float>) on the host cores, bounded prefix sample.
+
+``--impl reference`` times the reference CPU implementation alone (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+REASONS = {
+    0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+    0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+    0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+}
+N_SM = 148
+LANES_PER_SM = 128
+
+
+def measured_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text())
+    return {"sm_max_mhz": 1965.0, "_fallback": True}
+
+
+def issue_peak(peaks: dict) -> float:
+    """lane-ops/s per GPU: 148 SMs x 4 SMSP x 32 lanes x f_SM."""
+    return N_SM * LANES_PER_SM * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+
+
+def alg_ops_pairwise(n: int) -> float:
+    """Reference cost model, costmodel.hpp:129-130: 6 * n * C(n,2)."""
+    return 6.0 * n * n * (n - 1) / 2.0
+
+
+def alg_ops_triplet(n: int) -> float:
+    """costmodel.hpp:145-146: 8 * C(n,3)."""
+    return 8.0 * n * (n - 1) * (n - 2) / 6.0
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = Path(f"/tmp/pald_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        if self.proc is None or not self.path.exists():
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons, power = [], [], set(), []
+        for line in self.path.read_text().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 4:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+                power.append(float(parts[2]))
+                mask = int(parts[3], 16)
+            except ValueError:
+                continue
+            for bit, name in REASONS.items():
+                if mask & bit and bit != 0x1:
+                    reasons.add(name)
+        self.path.unlink(missing_ok=True)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": max(power)}
+
+
+# ---------------------------------------------------------------------------
+def make_input(cfg_index: int, device, seed: int):
+    """fp32 D of a config on the GPU (points -> distances kernel for point
+    clouds; host generator + upload for random matrices)."""
+    import torch
+    from paper_2307_16652_b200 import datagen
+    from paper_2307_16652_b200.engine import points_to_distances
+
+    cfg = datagen.config(cfg_index)
+    pts = datagen.make_points(cfg, seed)
+    if pts is not None:
+        return points_to_distances(torch.from_numpy(pts).to(device)), cfg
+    return torch.from_numpy(datagen.make_distances(cfg, seed)).to(device), cfg
+
+
+def cpu_reference_sample(d_host: np.ndarray, budget_s: float, cores: int):
+    """Time the unmodified reference parallel_pairwise<float> on a prefix of
+    x-rows (ref_bridge.cpp ref_parallel_pairwise_prefix_f32) and extrapolate
+    by the exact fraction of pair work. Returns (triplets/s, info)."""
+    from oracle.oracle import Reference, pair_work_fraction
+
+    ref = Reference()
+    n = d_host.shape[0]
+    b = ref.default_block_config(4)[0]
+    # calibrate on a tiny prefix, then size the sample to ~budget_s
+    x_small = max(1, n // 2048)
+    t_small, _, _ = ref.parallel_pairwise_prefix_f32(d_host, b, cores, x_small)
+    frac_small = pair_work_fraction(n, x_small)
+    est_full = t_small / frac_small
+    target_frac = min(1.0, budget_s / est_full)
+    x_lim = 1
+    while x_lim < n and pair_work_fraction(n, x_lim) < target_frac:
+        x_lim = int(x_lim * 1.25) + 1
+    x_lim = min(x_lim, n)
+    t, _, _ = ref.parallel_pairwise_prefix_f32(d_host, b, cores, x_lim)
+    frac = pair_work_fraction(n, x_lim)
+    t_full = t / frac
+    return n ** 3 / t_full, {
+        "sample": f"parallel_pairwise<float> (b={b}, p={cores}) over x-rows [0,{x_lim}) of n={n}: "
+                  f"{frac:.5f} of the pair work in {t:.2f} s, extrapolated to {t_full:.1f} s",
+        "seconds_sample": t, "fraction": frac, "lib": ref.path.name,
+    }
+
+
+# ---------------------------------------------------------------------------
+def run_reference_arm(args) -> None:
+    """--impl reference: the reference CPU implementation on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2307_16652_b200 import datagen
+    from oracle.oracle import Reference, host_cores, pair_work_fraction
+
+    cfg = datagen.config(args.config)
+    cores = host_cores()
+    pts = datagen.make_points(cfg, args.seed)
+    d = datagen.distances_from_points(pts) if pts is not None else datagen.make_distances(cfg, args.seed)
+    ref = Reference()
+    n = cfg.n
+    b = ref.default_block_config(4)[0]
+    # size each step to ~args.ref_step_s seconds of CPU work
+    x_small = max(1, n // 4096)
+    t_small, _, _ = ref.parallel_pairwise_prefix_f32(d, b, cores, x_small)
+    est_full = t_small / pair_work_fraction(n, x_small)
+    x_lim = 1
+    while x_lim < n and pair_work_fraction(n, x_lim) < args.ref_step_s / est_full:
+        x_lim = int(x_lim * 1.25) + 1
+    x_lim = min(x_lim, n)
+    frac = pair_work_fraction(n, x_lim)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t, _, _ = ref.parallel_pairwise_prefix_f32(d, b, cores, x_lim)
+        if i >= args.warmup:
+            times.append(t / frac)
+    t_step = statistics.mean(times)
+    value = n ** 3 / t_step
+    line = {
+        "metric": "pald_cohesion_triplets_per_s", "value": value, "unit": "triplets/s",
+        "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg.name, "n": n, "algorithm": "pairwise", "seed": args.seed},
+        "cpu_baseline": {"value": value, "unit": "triplets/s", "cores": cores, "kind": "reference",
+                         "sample": f"each step: parallel_pairwise<float> (b={b}, p={cores}) over x-rows "
+                                   f"[0,{x_lim}) = {frac:.5f} of the pair work, extrapolated by that fraction",
+                         "lib": ref.path.name},
+        "e2e": {"value": value, "unit": "triplets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def load_traffic(kernel: str, n: int) -> float | None:
+    """dram bytes per launch of the dominant kernel from a committed ncu
+    --set full summary (profiles/ncu_summary.json), if one matches n."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if not p.exists():
+        return None
+    try:
+        j = json.loads(p.read_text())
+        ent = j.get("kernels", {}).get(kernel)
+        if ent and int(ent.get("n", -1)) == n:
+            return float(ent["dram_bytes"])
+    except Exception:
+        return None
+    return None
+
+
+def time_engine_steps(engine, runner, D, steps: int, warmup: int, dist_on: bool):
+    """Timed steps with per-phase CUDA events on the launching stream."""
+    import torch
+    import torch.distributed as dist
+
+    stream = torch.cuda.current_stream()
+    for _ in range(warmup):
+        runner.step(D)
+    torch.cuda.synchronize()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(steps)]
+    launches0 = engine.launches
+    if dist_on:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    p = runner.plan
+    for s in range(steps):
+        e = ev[s]
+        e[0].record(stream)
+        engine.load(D)
+        e[1].record(stream)
+        engine.focus(*p.focus_tiles)
+        e[2].record(stream)
+        runner.exchange_focus()
+        e[3].record(stream)
+        engine.cohesion(*p.cohesion_rows)
+        e[4].record(stream)
+        runner.gather_cohesion()
+        e[5].record(stream)
+    end.record(stream)
+    torch.cuda.synchronize()
+    if dist_on:
+        dist.barrier()
+    launches = engine.launches - launches0
+    total_ms = start.elapsed_time(end)
+    per = {k: [] for k in ("load", "focus", "exchange", "cohesion", "gather")}
+    for e in ev:
+        per["load"].append(e[0].elapsed_time(e[1]))
+        per["focus"].append(e[1].elapsed_time(e[2]))
+        per["exchange"].append(e[2].elapsed_time(e[3]))
+        per["cohesion"].append(e[3].elapsed_time(e[4]))
+        per["gather"].append(e[4].elapsed_time(e[5]))
+    avg = {k: statistics.mean(v) for k, v in per.items()}
+    return total_ms / steps, avg, launches
+
+
+def e2e_host(n: int, D_dev, steps: int, warmup: int):
+    """pald_gpu_cohesion_f32 (C ABI, host pointers) with pinned buffers."""
+    import ctypes as C
+
+    import torch
+    from paper_2307_16652_b200 import _lib
+    from paper_2307_16652_b200.api import _raise_for
+
+    lib = _lib.load()
+    opts = _lib.make_opts(algorithm=_lib.PAIRWISE)
+    d_h = torch.empty((n, n), dtype=torch.float32, pin_memory=True)
+    d_h.copy_(D_dev)
+    u_h = torch.empty((n, n), dtype=torch.int32, pin_memory=True)
+    c_h = torch.empty((n, n), dtype=torch.float32, pin_memory=True)
+    times = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        _raise_for(lib.pald_gpu_cohesion_f32(d_h.data_ptr(), n, C.byref(opts), u_h.data_ptr(),
+                                             c_h.data_ptr(), None))
+        t1 = time.perf_counter()
+        if i >= warmup:
+            times.append(t1 - t0)
+    t = statistics.mean(times)
+    checksum = float(c_h[:64].double().sum())
+    del d_h, u_h, c_h
+    return n ** 3 / t, t, checksum
+
+
+def secondary_configs(steps: int) -> dict:
+    """N=1: the other BASELINE.json configs (parity cases) timed device-resident."""
+    import torch
+    from paper_2307_16652_b200.engine import Engine
+
+    out = {}
+    peak = issue_peak(measured_peaks())
+    for idx, alg in ((3, "pairwise"), (1, "pairwise"), (2, "triplet"), (4, "pairwise"), (4, "triplet")):
+        D, cfg = make_input(idx, "cuda", 20230731)
+        n = cfg.n
+        eng = Engine(n, alg)
+        stream = torch.cuda.current_stream()
+        for _ in range(2):
+            eng.run(D)
+        torch.cuda.synchronize()
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
+        for e in evs:
+            e[0].record(stream)
+            eng.load(D)
+            e[1].record(stream)
+            eng.focus()
+            e[2].record(stream)
+            eng.cohesion()
+            e[3].record(stream)
+        torch.cuda.synchronize()
+        step = statistics.mean(e[0].elapsed_time(e[3]) for e in evs) / 1e3
+        foc = statistics.mean(e[1].elapsed_time(e[2]) for e in evs) / 1e3
+        coh = statistics.mean(e[2].elapsed_time(e[3]) for e in evs) / 1e3
+        w = alg_ops_pairwise(n) if alg == "pairwise" else alg_ops_triplet(n)
+        out[f"{cfg.name}:{alg}"] = {
+            "n": n, "algorithm": alg, "triplets_per_s": n ** 3 / step, "ms_per_step": step * 1e3,
+            "focus_ms": foc * 1e3, "cohesion_ms": coh * 1e3,
+            "issue_roofline_frac_step": w / (step * peak), "exact_path": eng.exact_path,
+        }
+        del eng, D
+        torch.cuda.empty_cache()
+    return out
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=5, help="BASELINE.json config index (1-5)")
+    ap.add_argument("--seed", type=int, default=20230731)
+    ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU baseline sample")
+    ap.add_argument("--ref-step-s", type=float, default=4.0, help="seconds per --impl reference step")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: at least 3 warm-up steps
+
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2307_16652_b200.distributed import ShardedRunner
+    from paper_2307_16652_b200.engine import Engine
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist_on = world > 1
+    torch.cuda.set_device(local)
+    if dist_on:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    D, cfg = make_input(args.config, torch.device("cuda", local), args.seed)
+    n = cfg.n
+    engine = Engine(n, "pairwise", device=local)
+    runner = ShardedRunner(engine)
+    peaks = measured_peaks()
+    peak = issue_peak(peaks)
+
+    with ClockSampler(local) as clocks:
+        step_ms, phases, launches = time_engine_steps(engine, runner, D, args.steps, args.warmup, dist_on)
+    clk = clocks.summary()
+
+    # max over ranks
+    t = torch.tensor([step_ms, phases["cohesion"], phases["focus"]], dtype=torch.float64, device="cuda")
+    if dist_on:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    step_ms_max = float(t[0])
+    value = n ** 3 / (step_ms_max / 1e3)
+
+    # dominant kernel: pass 2 (cohesion) on this rank's rows
+    r0, r1 = runner.plan.cohesion_rows
+    coh_ops = 2.0 * (r1 - r0) * n * n  # 3 cmp + 1 FMA per (x<y, z) = 2 per ordered (x, y, z)
+    coh_s = phases["cohesion"] / 1e3
+    achieved = coh_ops / coh_s
+    f0, f1 = runner.plan.focus_tiles
+    nb = engine.tiles_per_dim
+    pair_tiles = sum(nb - t for t in range(f0, f1))
+    focus_ops = 2.0 * pair_tiles * (engine.tile ** 2) / 2 * n  # 2 cmp per (x<y, z)
+
+    line = {
+        "metric": "pald_cohesion_triplets_per_s",
+        "value": value,
+        "unit": "triplets/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": step_ms_max,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic: seeded points i.i.d. U[0,1)^3 (numpy PCG64), fp32 Euclidean D computed on the GPU",
+        "config": {"workload": cfg.name, "n": n, "algorithm": "pairwise", "seed": args.seed,
+                   "parallelism": f"pair-tile sharding x{world}",
+                   "l2": "inputs larger than L2 (D = %.1f GiB > 126 MB)" % (n * n * 4 / 2 ** 30)},
+        "roofline": {
+            "bound": "issue", "kernel": "pald_tile_kernel<cohesion>",
+            "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Gop/s",
+            "frac": achieved / peak,
+            "traffic": load_traffic("cohesion", n),
+            "step_frac": alg_ops_pairwise(n) / (step_ms_max / 1e3 * world * peak),
+            "peak_source": "148 SM x 128 lanes x sm_max_mhz %.0f (MEASURED_PEAKS.json)" % peaks.get("sm_max_mhz", 1965),
+            "ops_per_launch": coh_ops, "launch_ms": phases["cohesion"],
+        },
+        "phases_ms": phases,
+        "focus_kernel": {"ops_per_launch": focus_ops, "launch_ms": phases["focus"],
+                         "frac": focus_ops / (phases["focus"] / 1e3) / peak},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "exact_path": engine.exact_path,
+    }
+
+    if rank == 0 and world == 1:
+        if not args.no_e2e:
+            try:
+                ev, et, _ = e2e_host(n, D, max(1, min(args.steps, 3)), 1)
+                line["e2e"] = {"value": ev, "unit": "triplets/s", "seconds_per_step": et,
+                               "h2d_bytes_per_step": n * n * 4, "d2h_bytes_per_step": 2 * n * n * 4,
+                               "path": "pald_gpu_cohesion_f32 (C ABI), pinned host buffers"}
+            except Exception as e:  # report, never hide
+                line["e2e"] = {"value": None, "error": repr(e)}
+        if not args.no_cpu_baseline:
+            try:
+                from oracle.oracle import host_cores
+
+                d_host = D.cpu().numpy()
+                cores = host_cores()
+                v, info = cpu_reference_sample(d_host, args.cpu_budget, cores)
+                line["cpu_baseline"] = {"value": v, "unit": "triplets/s", "cores": cores,
+                                        "kind": "reference", "sample": info["sample"], "lib": info["lib"]}
+                del d_host
+            except Exception as e:
+                line["cpu_baseline"] = {"value": None, "error": repr(e)}
+        if not args.no_secondary:
+            del engine, runner
+            torch.cuda.empty_cache()
+            line["secondary_configs"] = secondary_configs(3)
+    elif rank == 0:
+        line["e2e"] = {"value": None, "note": "host-buffer C-ABI path is single-GPU; see N=1 line"}
+
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist_on:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -194,7 +194,8 @@ int ref_default_block_config(uint64_t element_bytes, uint64_t cache_bytes, uint6
 // parallel.hpp:178-215 run for the x-blocks x0 < x_limit only, with the
 // reference's own ThreadPool, worker_range, pair_block_focus and
 // pair_block_cohesion. The caller extrapolates by the exact fraction of
-// pair work covered. D is the fp32 matrix (to_real already applied).
+// pair work covered (the last x-block is cut at x_limit, so the sample
+// can be smaller than one block). D is the fp32 matrix (to_real already applied).
 // Returns the seconds of the timed loop in *seconds.
 int ref_parallel_pairwise_prefix_f32(const float* dd, uint64_t n, uint64_t b, int workers,
                                      uint64_t x_limit, double* seconds, int32_t* u_out,
@@ -209,7 +210,7 @@ int ref_parallel_pairwise_prefix_f32(const float* dd, uint64_t n, uint64_t b, in
     pald::ThreadPool pool(p);
     const double t0 = pald::detail::PhaseClock::now();
     for (uint64_t x0 = 0; x0 < n && x0 < x_limit; x0 += b) {
-      const uint64_t x1 = std::min<uint64_t>(x0 + b, n);
+      const uint64_t x1 = std::min<uint64_t>(std::min<uint64_t>(x0 + b, n), x_limit);
       for (uint64_t y0 = x0; y0 < n; y0 += b) {
         const uint64_t y1 = std::min<uint64_t>(y0 + b, n);
         const uint64_t ys = y1 - y0, cells = (x1 - x0) * ys;

@@ -287,6 +287,9 @@ int plan_alloc(pald_gpu_plan* p) {
   if ((rc = make_map(&p->tm_d, p->ds, p->n, p->ld))) return rc;
   if ((rc = make_map(&p->tm_dnu, p->dnu, p->n, p->ld))) return rc;
   if ((rc = make_map(&p->tm_w, p->w, p->n, p->ld))) return rc;
+  // The memsets above run on the legacy default stream; callers may use
+  // non-blocking streams, so finish them before the plan is handed out.
+  PALD_CUDA(cudaDeviceSynchronize());
   return PALD_GPU_OK;
 }
 

@@ -1,0 +1,126 @@
+"""Multi-GPU PaLD: one process per GPU, torch.distributed (NCCL) plumbing.
+
+Work decomposition:
+  * D is replicated (every rank lays out the same fp32 matrix).
+  * Pass 1 (focus): the upper-triangular 128x128 pair-tile grid is split
+    into contiguous tile-row ranges of equal work (row t holds nb - t tiles;
+    the reference's analogue is the z-split of parallel.hpp:185-204). Each
+    rank writes U and W = 1/U for its tiles and their mirror images; every
+    entry is written by exactly one rank and is 0 elsewhere, so a SUM
+    all-reduce assembles both matrices exactly (integer / single nonzero).
+  * Pass 2 (cohesion): C rows are split into equal bands of tile rows (each
+    row costs the same n^2 work). No reduction is needed: each C row is a
+    complete in-order sum on one rank (bit-identical to 1 GPU), and the
+    bands are all-gathered.
+The exchange steps are real data dependencies (W between the passes, C at
+the end); nothing else crosses ranks.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+
+def focus_tile_split(nb: int, world: int) -> list[tuple[int, int]]:
+    """Contiguous tile-row ranges [t0, t1) of ~equal pass-1 work."""
+    total = nb * (nb + 1) // 2
+    bounds = [0]
+    acc = 0
+    t = 0
+    for k in range(1, world):
+        target = total * k / world
+        while t < nb and acc + (nb - t) / 2 <= target:
+            acc += nb - t
+            t += 1
+        bounds.append(t)
+    bounds.append(nb)
+    return [(bounds[i], bounds[i + 1]) for i in range(world)]
+
+
+def cohesion_row_split(n: int, tile: int, world: int) -> list[tuple[int, int]]:
+    """Contiguous, tile-aligned row bands [r0, r1) of ~equal pass-2 work."""
+    nb = (n + tile - 1) // tile
+    per = -(-nb // world)  # ceil
+    out = []
+    for k in range(world):
+        t0, t1 = min(nb, k * per), min(nb, (k + 1) * per)
+        out.append((min(n, t0 * tile), min(n, t1 * tile)))
+    return out
+
+
+@dataclass
+class ShardPlan:
+    rank: int
+    world: int
+    focus_tiles: tuple[int, int]
+    cohesion_rows: tuple[int, int]
+    band_rows: int  # padded rows per rank for the C all-gather
+
+
+def make_shard_plan(n: int, tile: int, rank: int, world: int) -> ShardPlan:
+    nb = (n + tile - 1) // tile
+    f = focus_tile_split(nb, world)
+    c = cohesion_row_split(n, tile, world)
+    band = max(r1 - r0 for r0, r1 in c)
+    return ShardPlan(rank, world, f[rank], c[rank], band)
+
+
+class ShardedRunner:
+    """Runs one full PaLD step across the ranks of ``group``.
+
+    ``engine`` is a paper_2307_16652_b200.engine.Engine (or any object with
+    the same load / focus / cohesion / full_U / full_W / row_block_C / C
+    interface -- the CPU tests use a gloo-backed stand-in).
+    """
+
+    def __init__(self, engine, group=None, gather_u: bool = True):
+        self.engine = engine
+        self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.plan = make_shard_plan(engine.n, engine.tile, self.rank, self.world)
+        self.gather_u = gather_u
+        ld = engine.ld
+        self._even = all(r1 - r0 == self.plan.band_rows
+                         for r0, r1 in cohesion_row_split(engine.n, engine.tile, self.world))
+        self._even = self._even and self.plan.band_rows * self.world == engine.n
+        if not self._even:
+            dev = engine.C.device
+            self._send = torch.zeros(self.plan.band_rows * ld, dtype=torch.float32, device=dev)
+            self._recv = torch.empty(self.world * self.plan.band_rows * ld, dtype=torch.float32, device=dev)
+
+    def exchange_focus(self) -> None:
+        if self.world == 1:
+            return
+        dist.all_reduce(self.engine.full_W(), op=dist.ReduceOp.SUM, group=self.group)
+        if self.gather_u:
+            dist.all_reduce(self.engine.full_U(), op=dist.ReduceOp.SUM, group=self.group)
+
+    def gather_cohesion(self) -> None:
+        if self.world == 1:
+            return
+        e, p = self.engine, self.plan
+        r0, r1 = p.cohesion_rows
+        if self._even:
+            full = e.row_block_C(0, e.n)
+            dist.all_gather_into_tensor(full, e.row_block_C(r0, r1), group=self.group)
+            return
+        ld = e.ld
+        self._send.zero_()
+        if r1 > r0:
+            self._send[: (r1 - r0) * ld].copy_(e.row_block_C(r0, r1))
+        dist.all_gather_into_tensor(self._recv, self._send, group=self.group)
+        for k, (a, b) in enumerate(cohesion_row_split(e.n, e.tile, self.world)):
+            if b > a:
+                src = self._recv[k * p.band_rows * ld: k * p.band_rows * ld + (b - a) * ld]
+                e.row_block_C(a, b).copy_(src)
+
+    def step(self, D, stream=None) -> None:
+        e, p = self.engine, self.plan
+        e.load(D, stream)
+        e.focus(*p.focus_tiles, stream=stream)
+        self.exchange_focus()
+        e.cohesion(*p.cohesion_rows, stream=stream)
+        self.gather_cohesion()
