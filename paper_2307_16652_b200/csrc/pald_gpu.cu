@@ -241,6 +241,8 @@ struct pald_gpu_plan {
   CUtensorMap tm_d, tm_dnu, tm_w;
   bool loaded = false;
   bool exact = false;
+  bool focus_dirty = false;
+  int sms = 148;
   uint64_t launches = 0;
 
   ~pald_gpu_plan() {
@@ -339,6 +341,7 @@ int plan_load_impl(pald_gpu_plan* p, const float* dD, uint64_t ldd, cudaStream_t
   PALD_CUDA(cudaMemsetAsync(p->u, 0, p->n * p->ld * 4, s));
   PALD_CUDA(cudaMemsetAsync(p->w, 0, p->n * p->ld * 4, s));
   p->loaded = true;
+  p->focus_dirty = false;
   return PALD_GPU_OK;
 }
 
@@ -346,20 +349,31 @@ int plan_focus_impl(pald_gpu_plan* p, uint64_t tr0, uint64_t tr1, cudaStream_t s
   if (!p->loaded) return set_error(PALD_GPU_ERR_VALIDATION, "plan has no distances loaded");
   tr1 = std::min(tr1, p->nb);
   if (tr0 >= tr1) return PALD_GPU_OK;
-  uint64_t tiles = 0;
-  for (uint64_t t = tr0; t < tr1; ++t) tiles += p->nb - t;
-  KernelArgs a{p->ds, p->u, p->w, p->c, (int)p->n, (int)p->ld, (int)p->nb, (int)tr0, (int)tr1};
+  if (p->focus_dirty) {  // counts accumulate into W: start from zero again
+    PALD_CUDA(cudaMemsetAsync(p->u, 0, p->n * p->ld * 4, s));
+    PALD_CUDA(cudaMemsetAsync(p->w, 0, p->n * p->ld * 4, s));
+  }
+  p->focus_dirty = true;
+  long long tiles = 0;
+  for (uint64_t t = tr0; t < tr1; ++t) tiles += (long long)(p->nb - t);
+  KernelArgs a{p->ds, p->u, p->w, p->c, (int)p->n, (int)p->ld, (int)p->nb, (int)tr0, (int)tr1, tiles};
+  const long long units = tiles * (long long)((p->n + kBK - 1) / kBK);
+  const int grid = (int)std::min<long long>(units, p->sms);
   int rc;
   const bool tri = p->algorithm == PALD_GPU_TRIPLET;
   if (!p->exact) {
-    rc = tri ? launch_tile<0, true, true, true, false, true>(p->tm_d, p->tm_dnu, p->tm_w, a, (int)tiles, s)
-             : launch_tile<0, false, false, false, false, true>(p->tm_d, p->tm_dnu, p->tm_w, a, (int)tiles, s);
+    rc = tri ? launch_tile<0, true, true, true, false, true>(p->tm_d, p->tm_dnu, p->tm_w, a, grid, s)
+             : launch_tile<0, false, false, false, false, true>(p->tm_d, p->tm_dnu, p->tm_w, a, grid, s);
   } else {
-    rc = tri ? launch_tile<0, true, true, true, false, false>(p->tm_d, p->tm_dnu, p->tm_w, a, (int)tiles, s)
-             : launch_tile<0, false, false, false, false, false>(p->tm_d, p->tm_dnu, p->tm_w, a, (int)tiles, s);
+    rc = tri ? launch_tile<0, true, true, true, false, false>(p->tm_d, p->tm_dnu, p->tm_w, a, grid, s)
+             : launch_tile<0, false, false, false, false, false>(p->tm_d, p->tm_dnu, p->tm_w, a, grid, s);
   }
-  if (rc == PALD_GPU_OK) ++p->launches;
-  return rc;
+  if (rc) return rc;
+  ++p->launches;
+  focus_finish_kernel<<<(unsigned)(tiles * 4), 256, 0, s>>>(p->u, p->w, (int)p->n, (int)p->ld, (int)p->nb, (int)tr0);
+  PALD_CUDA(cudaGetLastError());
+  ++p->launches;
+  return PALD_GPU_OK;
 }
 
 int plan_cohesion_impl(pald_gpu_plan* p, uint64_t row0, uint64_t row1, cudaStream_t s) {
@@ -369,16 +383,17 @@ int plan_cohesion_impl(pald_gpu_plan* p, uint64_t row0, uint64_t row1, cudaStrea
   if (row0 % kTile != 0 || (row1 % kTile != 0 && row1 != p->n))
     return set_error(PALD_GPU_ERR_VALIDATION, "cohesion row range must be aligned to %d", kTile);
   const uint64_t tr0 = row0 / kTile, tr1 = (row1 + kTile - 1) / kTile;
-  const uint64_t tiles = (tr1 - tr0) * p->nb;
-  KernelArgs a{p->ds, p->u, p->w, p->c, (int)p->n, (int)p->ld, (int)p->nb, (int)tr0, (int)tr1};
+  const long long tiles = (long long)((tr1 - tr0) * p->nb);
+  KernelArgs a{p->ds, p->u, p->w, p->c, (int)p->n, (int)p->ld, (int)p->nb, (int)tr0, (int)tr1, tiles};
+  const int grid = (int)std::min<long long>(tiles, p->sms);
   int rc;
   const bool tri = p->algorithm == PALD_GPU_TRIPLET;
   if (!p->exact) {
-    rc = tri ? launch_tile<1, true, true, false, true, true>(p->tm_d, p->tm_dnu, p->tm_w, a, (int)tiles, s)
-             : launch_tile<1, false, true, false, false, true>(p->tm_d, p->tm_dnu, p->tm_w, a, (int)tiles, s);
+    rc = tri ? launch_tile<1, true, true, false, true, true>(p->tm_d, p->tm_dnu, p->tm_w, a, grid, s)
+             : launch_tile<1, false, true, false, false, true>(p->tm_d, p->tm_dnu, p->tm_w, a, grid, s);
   } else {
-    rc = tri ? launch_tile<1, true, true, false, true, false>(p->tm_d, p->tm_dnu, p->tm_w, a, (int)tiles, s)
-             : launch_tile<1, false, true, false, false, false>(p->tm_d, p->tm_dnu, p->tm_w, a, (int)tiles, s);
+    rc = tri ? launch_tile<1, true, true, false, true, false>(p->tm_d, p->tm_dnu, p->tm_w, a, grid, s)
+             : launch_tile<1, false, true, false, false, false>(p->tm_d, p->tm_dnu, p->tm_w, a, grid, s);
   }
   if (rc == PALD_GPU_OK) ++p->launches;
   return rc;
@@ -455,6 +470,7 @@ int pald_gpu_plan_create(uint64_t n, const pald_gpu_opts* o, pald_gpu_plan** out
   p->nb = (n + kTile - 1) / kTile;
   p->algorithm = o->algorithm;
   p->flags = o->flags;
+  PALD_CUDA(cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, dev));
   if ((rc = plan_alloc(p.get()))) return rc;
   *out = p.release();
   return PALD_GPU_OK;

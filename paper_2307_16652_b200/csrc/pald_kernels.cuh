@@ -65,6 +65,7 @@ struct KernelArgs {
   int nb;                // tiles per dimension
   int tile_row_begin;    // first tile row of this launch
   int tile_row_end;
+  long long total_tiles; // tiles covered by this launch
 };
 
 // ---------------------------------------------------------------------------
@@ -104,60 +105,192 @@ __device__ __forceinline__ uint32_t nu_bits(uint32_t v) { return v + 1u; }
 __device__ __forceinline__ float nu_f(float v) { return __uint_as_float(__float_as_uint(v) + 1u); }
 
 // ---------------------------------------------------------------------------
-// The tile kernel. One CTA computes one 128 x 128 output tile over all n
-// third points; TMA streams 32-row chunks of the A/B(/W) panels through a
-// 4-stage mbarrier pipeline. Thread (ty, tx) owns rows {ty*4+i, 64+ty*4+i}
-// and columns {tx*4+j, 64+tx*4+j}; pairs of adjacent columns share one
-// packed FADD2/FFMA2 accumulate.
-//
-// PASS 0 = focus, 1 = cohesion. A_NU / B_NU / T_NU select the nu()
-// transforms above; ZERO_DIAG zeroes the cohesion diagonal (triplet).
+// Thread layout: 8 warps as a 4 x 2 grid of 4 x 8-thread warp tiles; thread
+// (ty, tx) in 16 x 16 owns rows {ty*4+i, 64+ty*4+i} and columns
+// {tx*4+j, 64+tx*4+j} (i, j < 4) of the 128 x 128 tile. A-panel LDS.128 of a
+// warp touch 4 distinct 16-byte words (broadcast), B-panel loads 8
+// consecutive words: one wavefront each.
+__device__ __forceinline__ int row_off(int ty, int i) { return i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4); }
+
+// One k step of the uniform (no per-element transform) fast path.
+template <int PASS, bool FAST>
+__device__ __forceinline__ void k_step(const float* __restrict__ sa, const float* __restrict__ sb,
+                                       const float* __restrict__ sw, int kk, int ty, int tx,
+                                       const float2 (&thr)[8][4], float2 (&acc)[8][4]) {
+  const float4 a0 = reinterpret_cast<const float4*>(sa + kk * kTile)[ty];
+  const float4 a1 = reinterpret_cast<const float4*>(sa + kk * kTile)[16 + ty];
+  const float4 b0 = reinterpret_cast<const float4*>(sb + kk * kTile)[tx];
+  const float4 b1 = reinterpret_cast<const float4*>(sb + kk * kTile)[16 + tx];
+  const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+  const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+  float w[8];
+  if (PASS == 1) {
+    const float4 w0 = reinterpret_cast<const float4*>(sw + kk * kTile)[ty];
+    const float4 w1 = reinterpret_cast<const float4*>(sw + kk * kTile)[16 + ty];
+    w[0] = w0.x; w[1] = w0.y; w[2] = w0.z; w[3] = w0.w;
+    w[4] = w1.x; w[5] = w1.y; w[6] = w1.z; w[7] = w1.w;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+#pragma unroll
+    for (int jp = 0; jp < 4; ++jp) {
+      if (FAST) {
+        const float m0 = fminf(a[i], b[2 * jp]);
+        const float m1 = fminf(a[i], b[2 * jp + 1]);
+        if (PASS == 0) {
+          const float k0f = __saturatef(__fmaf_rn(m0, -kCmpScale, thr[i][jp].x));
+          const float k1f = __saturatef(__fmaf_rn(m1, -kCmpScale, thr[i][jp].y));
+          acc[i][jp] = __fadd2_rn(acc[i][jp], make_float2(k0f, k1f));
+        } else {
+          const float k0f = __saturatef(__fmaf_rn(m0, kCmpScale, thr[i][jp].x));
+          const float k1f = __saturatef(__fmaf_rn(m1, kCmpScale, thr[i][jp].y));
+          acc[i][jp] = __ffma2_rn(make_float2(k0f, k1f), make_float2(w[i], w[i]), acc[i][jp]);
+        }
+      } else {
+        const uint32_t ai = __float_as_uint(a[i]);
+        const uint32_t m0 = min(ai, __float_as_uint(b[2 * jp]));
+        const uint32_t m1 = min(ai, __float_as_uint(b[2 * jp + 1]));
+        const uint32_t t0 = __float_as_uint(thr[i][jp].x), t1 = __float_as_uint(thr[i][jp].y);
+        if (PASS == 0) {
+          acc[i][jp].x += (m0 < t0) ? 1.f : 0.f;
+          acc[i][jp].y += (m1 < t1) ? 1.f : 0.f;
+        } else {
+          acc[i][jp].x = __fadd_rn(acc[i][jp].x, (t0 < m0) ? w[i] : 0.f);
+          acc[i][jp].y = __fadd_rn(acc[i][jp].y, (t1 < m1) ? w[i] : 0.f);
+        }
+      }
+    }
+  }
+}
+
+// One k step with per-element transforms (chunks that cross the row or
+// column tile, and the ragged last chunk).
+template <int PASS, bool FAST>
+__device__ __forceinline__ void k_step_sel(const float* __restrict__ sa, const float* __restrict__ sb,
+                                           const float* __restrict__ sw, int kk, int kg, int ty,
+                                           int tx, int r0, int c0, bool a_in, bool b_in,
+                                           const float2 (&thr)[8][4], float2 (&acc)[8][4]) {
+  float a[8], b[8], w[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    a[i] = sa[kk * kTile + row_off(ty, i)];
+    if (PASS == 1) w[i] = sw[kk * kTile + row_off(ty, i)];
+    b[i] = sb[kk * kTile + row_off(tx, i)];
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+#pragma unroll
+    for (int jp = 0; jp < 4; ++jp) {
+      float kv[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = 2 * jp + h;
+        const bool nua = a_in && (kg < c0 + row_off(tx, j));
+        const bool nub = b_in && (kg < r0 + row_off(ty, i));
+        const uint32_t av = nua ? nu_bits(__float_as_uint(a[i])) : __float_as_uint(a[i]);
+        const uint32_t bv = nub ? nu_bits(__float_as_uint(b[j])) : __float_as_uint(b[j]);
+        const float t = (h == 0) ? thr[i][jp].x : thr[i][jp].y;
+        if (FAST) {
+          const float m = fminf(__uint_as_float(av), __uint_as_float(bv));
+          kv[h] = (PASS == 0) ? __saturatef(__fmaf_rn(m, -kCmpScale, t))
+                              : __saturatef(__fmaf_rn(m, kCmpScale, t));
+        } else {
+          const uint32_t m = min(av, bv), tu = __float_as_uint(t);
+          kv[h] = (PASS == 0) ? ((m < tu) ? 1.f : 0.f) : ((tu < m) ? 1.f : 0.f);
+        }
+      }
+      if (PASS == 0) {
+        acc[i][jp] = __fadd2_rn(acc[i][jp], make_float2(kv[0], kv[1]));
+      } else {
+        acc[i][jp] = __ffma2_rn(make_float2(kv[0], kv[1]), make_float2(w[i], w[i]), acc[i][jp]);
+      }
+    }
+  }
+}
+
+// Tile index -> (tile row, tile col). Focus: upper-triangular tiles of tile
+// rows [tr_begin, tr_end) in row-major order; cohesion: all tiles of those
+// rows.
+template <int PASS>
+__device__ __forceinline__ void tile_coords(int t, int tr_begin, int nb, int& tr, int& tc) {
+  if (PASS == 0) {
+    // rows start at S(r) = r*nb - r*(r-1)/2 (relative to row 0); solve for r.
+    const long long base = (long long)tr_begin * nb - (long long)tr_begin * (tr_begin - 1) / 2;
+    const long long g = base + t;
+    const double bb = 2.0 * nb + 1.0;
+    int r = (int)((bb - sqrt(bb * bb - 8.0 * (double)g)) * 0.5);
+    r = max(0, min(r, nb - 1));
+    auto S = [&](long long rr) { return rr * nb - rr * (rr - 1) / 2; };
+    while (r > 0 && S(r) > g) --r;
+    while (r + 1 < nb && S(r + 1) <= g) ++r;
+    tr = r;
+    tc = r + (int)(g - S(r));
+  } else {
+    tr = tr_begin + t / nb;
+    tc = t % nb;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// The persistent tile kernel. Each CTA (one per SM) owns a contiguous range
+// of work units u = tile * nchunks + chunk:
+//   focus    (PASS 0): an equal share of all units ("stream-K"); partial
+//            tiles are combined exactly with red.global.add.f32 of integer
+//            counts (< 2^24) into the count buffer, converted to U and
+//            W = 1/U by focus_finish_kernel;
+//   cohesion (PASS 1): whole tiles only, so every C entry is one in-order
+//            fp32 sum (bit-identical to the reference).
+// TMA streams 32-row chunks of the A/B(/W) panels through a 4-stage
+// mbarrier pipeline that runs across tile boundaries. A stage is refilled by
+// the last warp to finish with it (shared-memory arrival counter), so no
+// block-wide barrier sits in the main loop.
 template <int PASS, bool A_NU, bool B_NU, bool T_NU, bool ZERO_DIAG, bool FAST>
 __global__ void __launch_bounds__(kThreads, 1)
     pald_tile_kernel(const __grid_constant__ CUtensorMap tm_d,
                      const __grid_constant__ CUtensorMap tm_dnu,
                      const __grid_constant__ CUtensorMap tm_w, const KernelArgs args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // Align the pipeline buffers to 1 KB with an offset into the same array,
+  // so the compiler keeps the shared address space (LDS, not generic LD).
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t full_bar[kStages];
-  __shared__ int s_tile[2];
+  __shared__ uint32_t done_cnt[kStages];
 
   const int tid = threadIdx.x;
   const int n = args.n, ld = args.ld, nb = args.nb;
+  const int nchunks = (n + kBK - 1) / kBK;
+  const int total_tiles = (int)args.total_tiles;
+  const int G = gridDim.x, g = blockIdx.x;
+  // Work units u = tile * nchunks + chunk (< 2^31 for n <= 2^17).
+  int u0, u1;
+  if (PASS == 0) {
+    const long long U = (long long)total_tiles * nchunks;
+    u0 = (int)(U * g / G);
+    u1 = (int)(U * (g + 1) / G);
+  } else {
+    u0 = (int)((long long)total_tiles * g / G) * nchunks;
+    u1 = (int)((long long)total_tiles * (g + 1) / G) * nchunks;
+  }
+  const int P = u1 - u0;
+  if (P <= 0) return;
 
-  // ---- tile coordinates -------------------------------------------------
   if (tid == 0) {
-    int b = blockIdx.x, tr = args.tile_row_begin, tc;
-    if (PASS == 0) {  // upper-triangular tiles of rows [begin, end)
-      while (b >= nb - tr) { b -= nb - tr; ++tr; }
-      tc = tr + b;
-    } else {          // all tiles of rows [begin, end)
-      tr += b / nb;
-      tc = b % nb;
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      done_cnt[s] = 0;
     }
-    s_tile[0] = tr;
-    s_tile[1] = tc;
-    for (int s = 0; s < kStages; ++s) mbar_init(&full_bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const int r0 = s_tile[0] * kTile, c0 = s_tile[1] * kTile;
 
-  const int warp = tid >> 5, lane = tid & 31;
-  const int ty = (warp >> 1) * 4 + (lane >> 3);  // 0..15
-  const int tx = (warp & 1) * 8 + (lane & 7);    // 0..15
-  int rows[8], cols[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    rows[i] = r0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
-    cols[i] = c0 + (i < 4 ? tx * 4 + i : 64 + tx * 4 + (i - 4));
-  }
-
-  const int nchunks = (n + kBK - 1) / kBK;
   constexpr int SB = stage_bytes(PASS);
-  auto issue = [&](int ch) {
-    const int s = ch % kStages;
+  auto issue = [&](int p) {
+    const int u = u0 + p;
+    const int t = u / nchunks, ch = u - t * nchunks;
+    int tr, tc;
+    tile_coords<PASS>(t, args.tile_row_begin, nb, tr, tc);
+    const int r0 = tr * kTile, c0 = tc * kTile;
+    const int s = p % kStages;
     const int k0 = ch * kBK, k1 = min(k0 + kBK, n);
     // Uniform per-chunk transform choice: the whole chunk lies below the
     // column (A) / row (B) tile => every element takes nu().
@@ -170,210 +303,162 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (PASS == 1) tma_load_2d(st + 2 * kBoxBytes, &tm_w, r0, k0, &full_bar[s]);
   };
   if (tid == 0) {
-    for (int ch = 0; ch < kStages && ch < nchunks; ++ch) issue(ch);
+    for (int p = 0; p < kStages && p < P; ++p) issue(p);
   }
 
-  // ---- per-output thresholds (hoisted out of the k loop) -----------------
-  // thr[i][jp] holds columns (2jp, 2jp+1) of row i.
-  float2 thr[8][4];
-  float2 acc[8][4];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-#pragma unroll
-    for (int jp = 0; jp < 4; ++jp) {
-      uint32_t t2[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int r = rows[i], c = cols[2 * jp + h];
-        uint32_t t = (r < n && c < n) ? __ldg(args.d + (size_t)r * ld + c) : 0u;
-        if (T_NU) t = nu_bits(t);
-        t2[h] = t;
-      }
-      if (FAST) {
-        const float s = (PASS == 0) ? kCmpScale : -kCmpScale;
-        thr[i][jp] = make_float2(__uint_as_float(t2[0]) * s, __uint_as_float(t2[1]) * s);
-      } else {
-        thr[i][jp] = make_float2(__uint_as_float(t2[0]), __uint_as_float(t2[1]));
-      }
-      acc[i][jp] = make_float2(0.f, 0.f);
-    }
-  }
+  const int warp = tid >> 5, lane = tid & 31;
+  const int ty = (warp >> 1) * 4 + (lane >> 3);  // 0..15
+  const int tx = (warp & 1) * 8 + (lane & 7);    // 0..15
 
-  // ---- main loop ----------------------------------------------------------
-  for (int ch = 0; ch < nchunks; ++ch) {
-    const int s = ch % kStages;
-    mbar_wait(&full_bar[s], (ch / kStages) & 1);
-    const uint8_t* st = smem + s * SB;
-    const float* sa = reinterpret_cast<const float*>(st);
-    const float* sb = reinterpret_cast<const float*>(st + kBoxBytes);
-    const float* sw = reinterpret_cast<const float*>(st + 2 * kBoxBytes);
-    const int k0 = ch * kBK;
-    const bool a_in = A_NU && (k0 >= c0) && (k0 < c0 + kTile);
-    const bool b_in = B_NU && (k0 >= r0) && (k0 < r0 + kTile);
-    const int kmax = min(kBK, n - k0);
-
-    if (!a_in && !b_in && kmax == kBK) {
-      // Fast, uniform chunk.
-#pragma unroll 2
-      for (int kk = 0; kk < kBK; ++kk) {
-        const float4 a0 = reinterpret_cast<const float4*>(sa + kk * kTile)[ty];
-        const float4 a1 = reinterpret_cast<const float4*>(sa + kk * kTile)[16 + ty];
-        const float4 b0 = reinterpret_cast<const float4*>(sb + kk * kTile)[tx];
-        const float4 b1 = reinterpret_cast<const float4*>(sb + kk * kTile)[16 + tx];
-        const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-        const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-        float w[8];
-        if (PASS == 1) {
-          const float4 w0 = reinterpret_cast<const float4*>(sw + kk * kTile)[ty];
-          const float4 w1 = reinterpret_cast<const float4*>(sw + kk * kTile)[16 + ty];
-          w[0] = w0.x; w[1] = w0.y; w[2] = w0.z; w[3] = w0.w;
-          w[4] = w1.x; w[5] = w1.y; w[6] = w1.z; w[7] = w1.w;
+  int p = 0;
+  int t = u0 / nchunks;
+  int ch_begin = u0 - t * nchunks;
+  while (p < P) {
+    // ---- one tile (possibly partial for the focus stream-K split) ---------
+    const int ch_end = min(nchunks, ch_begin + (P - p));
+    int tr, tc;
+    tile_coords<PASS>(t, args.tile_row_begin, nb, tr, tc);
+    const int r0 = tr * kTile, c0 = tc * kTile;
+    float2 thr[8][4];
+    float2 acc[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+#pragma unroll
+      for (int jp = 0; jp < 4; ++jp) {
+        uint32_t t2[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = r0 + row_off(ty, i), c = c0 + row_off(tx, 2 * jp + h);
+          uint32_t tv = (r < n && c < n) ? __ldg(args.d + (size_t)r * ld + c) : 0u;
+          if (T_NU) tv = nu_bits(tv);
+          t2[h] = tv;
         }
+        if (FAST) {
+          const float sc = (PASS == 0) ? kCmpScale : -kCmpScale;
+          thr[i][jp] = make_float2(__uint_as_float(t2[0]) * sc, __uint_as_float(t2[1]) * sc);
+        } else {
+          thr[i][jp] = make_float2(__uint_as_float(t2[0]), __uint_as_float(t2[1]));
+        }
+        acc[i][jp] = make_float2(0.f, 0.f);
+      }
+    }
+
+    for (int ch = ch_begin; ch < ch_end; ++ch, ++p) {
+      const int s = p % kStages;
+      mbar_wait(&full_bar[s], (p / kStages) & 1);
+      const uint8_t* st = smem + s * SB;
+      const float* sa = reinterpret_cast<const float*>(st);
+      const float* sb = reinterpret_cast<const float*>(st + kBoxBytes);
+      const float* sw = reinterpret_cast<const float*>(st + 2 * kBoxBytes);
+      const int k0 = ch * kBK;
+      const bool a_in = A_NU && (k0 >= c0) && (k0 < c0 + kTile);
+      const bool b_in = B_NU && (k0 >= r0) && (k0 < r0 + kTile);
+      const int kmax = min(kBK, n - k0);
+      if (!a_in && !b_in && kmax == kBK) {
+#pragma unroll 2
+        for (int kk = 0; kk < kBK; ++kk) k_step<PASS, FAST>(sa, sb, sw, kk, ty, tx, thr, acc);
+      } else {
+        for (int kk = 0; kk < kmax; ++kk)
+          k_step_sel<PASS, FAST>(sa, sb, sw, kk, k0 + kk, ty, tx, r0, c0, a_in, b_in, thr, acc);
+      }
+      // Release the stage: the last warp to arrive refills it.
+      __syncwarp();
+      if (lane == 0) {
+        const uint32_t old = atomicAdd(&done_cnt[s], 1u);
+        if (old == (uint32_t)(p / kStages + 1) * (kThreads / 32) - 1u && p + kStages < P)
+          issue(p + kStages);
+      }
+    }
+
+    // ---- flush ------------------------------------------------------------
+    if (PASS == 0) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < 8; ++i) {
+        const int r = r0 + row_off(ty, i);
+        if (r >= n) continue;
 #pragma unroll
-          for (int jp = 0; jp < 4; ++jp) {
-            if (FAST) {
-              const float m0 = fminf(a[i], b[2 * jp]);
-              const float m1 = fminf(a[i], b[2 * jp + 1]);
-              if (PASS == 0) {
-                const float k0f = __saturatef(__fmaf_rn(m0, -kCmpScale, thr[i][jp].x));
-                const float k1f = __saturatef(__fmaf_rn(m1, -kCmpScale, thr[i][jp].y));
-                acc[i][jp] = __fadd2_rn(acc[i][jp], make_float2(k0f, k1f));
-              } else {
-                const float k0f = __saturatef(__fmaf_rn(m0, kCmpScale, thr[i][jp].x));
-                const float k1f = __saturatef(__fmaf_rn(m1, kCmpScale, thr[i][jp].y));
-                acc[i][jp] = __ffma2_rn(make_float2(k0f, k1f), make_float2(w[i], w[i]), acc[i][jp]);
-              }
-            } else {
-              const uint32_t ai = __float_as_uint(a[i]);
-              const uint32_t m0 = min(ai, __float_as_uint(b[2 * jp]));
-              const uint32_t m1 = min(ai, __float_as_uint(b[2 * jp + 1]));
-              const uint32_t t0 = __float_as_uint(thr[i][jp].x), t1 = __float_as_uint(thr[i][jp].y);
-              if (PASS == 0) {
-                acc[i][jp].x += (m0 < t0) ? 1.f : 0.f;
-                acc[i][jp].y += (m1 < t1) ? 1.f : 0.f;
-              } else {
-                acc[i][jp].x = __fadd_rn(acc[i][jp].x, (t0 < m0) ? w[i] : 0.f);
-                acc[i][jp].y = __fadd_rn(acc[i][jp].y, (t1 < m1) ? w[i] : 0.f);
-              }
-            }
-          }
+        for (int j = 0; j < 8; ++j) {
+          const int c = c0 + row_off(tx, j);
+          const float v = (j & 1) ? acc[i][j >> 1].y : acc[i][j >> 1].x;
+          if (c < n) atomicAdd(args.w + (size_t)r * ld + c, v);  // RED.ADD.F32, exact
         }
       }
     } else {
-      // Chunk that crosses the row/column tile (per-element nu choice) or
-      // the ragged last chunk.
-      for (int kk = 0; kk < kmax; ++kk) {
-        const int kg = k0 + kk;
-        float a[8], b[8], w[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int off = (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
-          a[i] = sa[kk * kTile + off];
-          if (PASS == 1) w[i] = sw[kk * kTile + off];
-          const int offc = (i < 4 ? tx * 4 + i : 64 + tx * 4 + (i - 4));
-          b[i] = sb[kk * kTile + offc];
+      for (int i = 0; i < 8; ++i) {
+        const int r = r0 + row_off(ty, i);
+        if (r >= n) continue;
+        float v[8];
+#pragma unroll
+        for (int jp = 0; jp < 4; ++jp) {
+          v[2 * jp] = acc[i][jp].x;
+          v[2 * jp + 1] = acc[i][jp].y;
         }
+        if (ZERO_DIAG) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-#pragma unroll
-          for (int jp = 0; jp < 4; ++jp) {
-            float kv[2];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int j = 2 * jp + h;
-              const bool nua = a_in && (kg < cols[j]);
-              const bool nub = b_in && (kg < rows[i]);
-              const uint32_t av = nua ? nu_bits(__float_as_uint(a[i])) : __float_as_uint(a[i]);
-              const uint32_t bv = nub ? nu_bits(__float_as_uint(b[j])) : __float_as_uint(b[j]);
-              const float t = (h == 0) ? thr[i][jp].x : thr[i][jp].y;
-              if (FAST) {
-                const float m = fminf(__uint_as_float(av), __uint_as_float(bv));
-                kv[h] = (PASS == 0) ? __saturatef(__fmaf_rn(m, -kCmpScale, t))
-                                    : __saturatef(__fmaf_rn(m, kCmpScale, t));
-              } else {
-                const uint32_t m = min(av, bv), tu = __float_as_uint(t);
-                kv[h] = (PASS == 0) ? ((m < tu) ? 1.f : 0.f) : ((tu < m) ? 1.f : 0.f);
-              }
-            }
-            if (PASS == 0) {
-              acc[i][jp] = __fadd2_rn(acc[i][jp], make_float2(kv[0], kv[1]));
-            } else {
-              acc[i][jp] = __ffma2_rn(make_float2(kv[0], kv[1]), make_float2(w[i], w[i]), acc[i][jp]);
-            }
-          }
+          for (int j = 0; j < 8; ++j)
+            if (c0 + row_off(tx, j) == r) v[j] = 0.f;
         }
+        float* crow = args.c + (size_t)r * ld;
+        // Columns past n land in the row padding (ld >= round_up(n, 32)).
+        const int ca = c0 + tx * 4, cb = c0 + 64 + tx * 4;
+        if (ca < n) *reinterpret_cast<float4*>(crow + ca) = make_float4(v[0], v[1], v[2], v[3]);
+        if (cb < n) *reinterpret_cast<float4*>(crow + cb) = make_float4(v[4], v[5], v[6], v[7]);
       }
     }
-    __syncthreads();  // every warp is done with stage s
-    if (tid == 0 && ch + kStages < nchunks) issue(ch + kStages);
+    ++t;
+    ch_begin = 0;
   }
+}
 
-  // ---- epilogue -----------------------------------------------------------
-  if (PASS == 0) {
-    // Stage the count tile in shared memory, then write U and W = 1/U for
-    // the tile (coalesced rows) and its mirror image (coalesced columns).
-    float* tile = reinterpret_cast<float*>(smem);
-    constexpr int TS = kTile + 1;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int rl = rows[i] - r0;
-#pragma unroll
-      for (int jp = 0; jp < 4; ++jp) {
-        tile[rl * TS + (cols[2 * jp] - c0)] = acc[i][jp].x;
-        tile[rl * TS + (cols[2 * jp + 1] - c0)] = acc[i][jp].y;
-      }
-    }
-    __syncthreads();
-    const bool diag = (r0 == c0);
-    for (int idx = tid; idx < kTile * kTile; idx += kThreads) {
-      {  // direct: (r, c) with r < c (r == c -> 0)
-        const int rl = idx / kTile, cl = idx % kTile;
-        const int r = r0 + rl, c = c0 + cl;
-        if (r < n && c < n && (!diag || rl <= cl)) {
-          const float v = tile[rl * TS + cl];
-          const size_t o = (size_t)r * ld + c;
-          if (r == c) {
-            args.u[o] = 0;
-            args.w[o] = 0.f;
-          } else {
-            args.u[o] = static_cast<int32_t>(v);
-            args.w[o] = 1.0f / v;  // IEEE division: Real(1)/Real(cnt), blocked.hpp:401
-          }
-        }
-      }
-      {  // mirror: (c, r) for r < c
-        const int rl = idx % kTile, cl = idx / kTile;
-        const int r = r0 + rl, c = c0 + cl;
-        if (r < n && c < n && r < c) {
-          const float v = tile[rl * TS + cl];
-          const size_t o = (size_t)c * ld + r;
-          args.u[o] = static_cast<int32_t>(v);
-          args.w[o] = 1.0f / v;
+// Focus epilogue: counts (accumulated in the W buffer, upper-triangular
+// tiles of tile rows [tr_begin, tr_end)) -> U[r][c] = U[c][r] = count and
+// W[r][c] = W[c][r] = 1/count (IEEE division, Real(1)/Real(cnt),
+// blocked.hpp:401); diagonal 0. One CTA per 64 x 64 quadrant of a tile; the
+// quadrant is staged in shared memory so that both the direct and the
+// mirrored writes coalesce.
+__global__ void __launch_bounds__(256)
+    focus_finish_kernel(int32_t* __restrict__ u, float* __restrict__ w, int n, int ld, int nb,
+                        int tr_begin) {
+  constexpr int Q = kTile / 2;
+  __shared__ float tile[Q][Q + 1];
+  int tr, tc;
+  tile_coords<0>(blockIdx.x >> 2, tr_begin, nb, tr, tc);
+  const int qr = (blockIdx.x >> 1) & 1, qc = blockIdx.x & 1;
+  if (tr == tc && qr > qc) return;  // below the diagonal: the mirror of (0,1)
+  const int r0 = tr * kTile + qr * Q, c0 = tc * kTile + qc * Q;
+  const bool diag = (r0 == c0);
+  for (int idx = threadIdx.x; idx < Q * Q; idx += 256) {
+    const int rl = idx / Q, cl = idx % Q;
+    const int r = r0 + rl, c = c0 + cl;
+    tile[rl][cl] = (r < n && c < n) ? w[(size_t)r * ld + c] : 0.f;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < Q * Q; idx += 256) {
+    {  // direct (r, c), r <= c
+      const int rl = idx / Q, cl = idx % Q;
+      const int r = r0 + rl, c = c0 + cl;
+      if (r < n && c < n && (!diag || rl <= cl)) {
+        const size_t o = (size_t)r * ld + c;
+        if (r == c) {
+          u[o] = 0;
+          w[o] = 0.f;
+        } else {
+          const float v = tile[rl][cl];
+          u[o] = static_cast<int32_t>(v);
+          w[o] = 1.0f / v;
         }
       }
     }
-  } else {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int r = rows[i];
-      if (r >= n) continue;
-      float v[8];
-#pragma unroll
-      for (int jp = 0; jp < 4; ++jp) {
-        v[2 * jp] = acc[i][jp].x;
-        v[2 * jp + 1] = acc[i][jp].y;
+    {  // mirror (c, r), r < c
+      const int rl = idx % Q, cl = idx / Q;
+      const int r = r0 + rl, c = c0 + cl;
+      if (r < n && c < n && r < c) {
+        const float v = tile[rl][cl];
+        const size_t o = (size_t)c * ld + r;
+        u[o] = static_cast<int32_t>(v);
+        w[o] = 1.0f / v;
       }
-      if (ZERO_DIAG) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (cols[j] == r) v[j] = 0.f;
-      }
-      float* crow = args.c + (size_t)r * ld;
-      // Columns past n land in the row padding (ld >= round_up(n, 32)).
-      if (cols[0] < n) *reinterpret_cast<float4*>(crow + cols[0]) = make_float4(v[0], v[1], v[2], v[3]);
-      if (cols[4] < n) *reinterpret_cast<float4*>(crow + cols[4]) = make_float4(v[4], v[5], v[6], v[7]);
     }
   }
 }
