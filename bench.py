@@ -254,7 +254,7 @@ def time_engine_steps(engine, runner, D, steps: int, warmup: int, dist_on: bool)
         e[0].record(stream)
         engine.load(D)
         e[1].record(stream)
-        engine.focus(*p.focus_tiles)
+        engine.focus_counts(*p.focus_share)
         e[2].record(stream)
         runner.exchange_focus()
         e[3].record(stream)
@@ -404,10 +404,8 @@ def main() -> None:
     coh_ops = 2.0 * (r1 - r0) * n * n  # 3 cmp + 1 FMA per (x<y, z) = 2 per ordered (x, y, z)
     coh_s = phases["cohesion"] / 1e3
     achieved = coh_ops / coh_s
-    f0, f1 = runner.plan.focus_tiles
-    nb = engine.tiles_per_dim
-    pair_tiles = sum(nb - t for t in range(f0, f1))
-    focus_ops = 2.0 * pair_tiles * (engine.tile ** 2) / 2 * n  # 2 cmp per (x<y, z)
+    part, parts = runner.plan.focus_share
+    focus_ops = 2.0 * (n * (n - 1) / 2) * n / parts  # 2 cmp per (x<y, z), this rank's share
 
     line = {
         "metric": "pald_cohesion_triplets_per_s",

@@ -120,17 +120,21 @@ int pald_gpu_cohesion_f32_device(const float* dD, uint64_t ldd, uint64_t n,
                                  float* dC, uint64_t ldc, void* stream);
 
 /* ---- Staged plan: the building blocks of the multi-GPU drivers --------
- * A plan owns the device workspace for one n on one device. Pass 1
- * (focus) covers the upper-triangular 128x128 pair tiles whose tile row is
- * in [tile_row_begin, tile_row_end), writing U and W = 1/U for those tiles
- * and their mirror images; pass 2 (cohesion) writes C rows
- * [row_begin, row_end). Between the passes a multi-GPU driver sums U and W
- * over ranks (each entry is written by exactly one rank; the rest are 0). */
+ * A plan owns the device workspace for one n on one device.
+ * Pass 1 (focus) is split into work units (a 128 x 128 upper-triangular
+ * pair tile x a 32-point chunk of third points). focus_counts(part, parts)
+ * accumulates the integer focus counts of share `part` of `parts` equal
+ * shares of the units into the W buffer; focus_finish turns the counts
+ * into U and W = 1/U (both triangles). A multi-GPU driver gives each rank
+ * one share and SUMs the W buffers over ranks between the two calls
+ * (integer counts < 2^24 in fp32: exact, order-independent).
+ * Pass 2 (cohesion) writes C rows [row_begin, row_end) (tile aligned);
+ * each row is one in-order sum, so row bands need no reduction. */
 typedef struct pald_gpu_plan pald_gpu_plan;
 
 typedef struct pald_gpu_buffers {
   int32_t* U;        /* device, n x ld, focus sizes */
-  float* W;          /* device, n x ld, 1/U (diagonal 0) */
+  float* W;          /* device, n x ld, focus counts (after focus_counts) or 1/U (after finish) */
   float* C;          /* device, n x ld, unnormalized cohesion */
   uint64_t ld;       /* leading dimension (elements) of U, W, C */
   uint64_t n;
@@ -148,17 +152,18 @@ int pald_gpu_plan_destroy(pald_gpu_plan* plan);
 int pald_gpu_plan_load(pald_gpu_plan* plan, const float* dD, uint64_t ldd, void* stream);
 /* Same, from a host pointer (dense, ld = n). */
 int pald_gpu_plan_load_host(pald_gpu_plan* plan, const float* D, void* stream);
-int pald_gpu_plan_focus(pald_gpu_plan* plan, uint64_t tile_row_begin, uint64_t tile_row_end,
-                        void* stream);
+/* focus_counts(0, 1) + focus_finish */
+int pald_gpu_plan_focus(pald_gpu_plan* plan, void* stream);
+int pald_gpu_plan_focus_counts(pald_gpu_plan* plan, uint64_t part, uint64_t parts, void* stream);
+int pald_gpu_plan_focus_finish(pald_gpu_plan* plan, void* stream);
 int pald_gpu_plan_cohesion(pald_gpu_plan* plan, uint64_t row_begin, uint64_t row_end,
                            void* stream);
 int pald_gpu_plan_buffers(const pald_gpu_plan* plan, pald_gpu_buffers* out);
 /* Kernel launches issued by this plan so far (evidence counter). */
 uint64_t pald_gpu_plan_launches(const pald_gpu_plan* plan);
 
-/* Fraction of pass-1 work in tile rows [0, r) -- used to split the
- * triangular tile grid across ranks with equal work. */
-double pald_gpu_focus_work_prefix(uint64_t n, uint64_t tile_rows);
+/* Number of pass-1 work units of the plan. */
+uint64_t pald_gpu_focus_units(const pald_gpu_plan* plan);
 
 /* ---- Epilogue and input helpers ---------------------- */
 /* fill_diagonal, reference.hpp:213-220: c_xx = sum_{y != x} 1/u_xy,

@@ -29,10 +29,12 @@ EXPORTED_SYMBOLS = (
     "pald_gpu_plan_load",
     "pald_gpu_plan_load_host",
     "pald_gpu_plan_focus",
+    "pald_gpu_plan_focus_counts",
+    "pald_gpu_plan_focus_finish",
     "pald_gpu_plan_cohesion",
     "pald_gpu_plan_buffers",
     "pald_gpu_plan_launches",
-    "pald_gpu_focus_work_prefix",
+    "pald_gpu_focus_units",
     "pald_gpu_fill_diagonal",
     "pald_gpu_points_to_distances",
 )
@@ -105,11 +107,13 @@ def load(path: Path | None = None) -> C.CDLL:
         "pald_gpu_plan_destroy": (i32, [vp]),
         "pald_gpu_plan_load": (i32, [vp, vp, u64, vp]),
         "pald_gpu_plan_load_host": (i32, [vp, vp, vp]),
-        "pald_gpu_plan_focus": (i32, [vp, u64, u64, vp]),
+        "pald_gpu_plan_focus": (i32, [vp, vp]),
+        "pald_gpu_plan_focus_counts": (i32, [vp, u64, u64, vp]),
+        "pald_gpu_plan_focus_finish": (i32, [vp, vp]),
         "pald_gpu_plan_cohesion": (i32, [vp, u64, u64, vp]),
         "pald_gpu_plan_buffers": (i32, [vp, C.POINTER(Buffers)]),
         "pald_gpu_plan_launches": (u64, [vp]),
-        "pald_gpu_focus_work_prefix": (C.c_double, [u64, u64]),
+        "pald_gpu_focus_units": (u64, [vp]),
         "pald_gpu_fill_diagonal": (i32, [vp, u64, u64, vp, vp]),
         "pald_gpu_points_to_distances": (i32, [vp, u64, u64, vp, u64, vp]),
     }

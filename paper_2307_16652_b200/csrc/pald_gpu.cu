@@ -345,20 +345,27 @@ int plan_load_impl(pald_gpu_plan* p, const float* dD, uint64_t ldd, cudaStream_t
   return PALD_GPU_OK;
 }
 
-int plan_focus_impl(pald_gpu_plan* p, uint64_t tr0, uint64_t tr1, cudaStream_t s) {
+uint64_t focus_units(const pald_gpu_plan* p) {
+  return p->nb * (p->nb + 1) / 2 * ((p->n + kBK - 1) / kBK);
+}
+
+// Pass 1, share `part` of `parts` equal shares of the work units: integer
+// focus counts accumulated into the W buffer.
+int plan_focus_counts_impl(pald_gpu_plan* p, uint64_t part, uint64_t parts, cudaStream_t s) {
   if (!p->loaded) return set_error(PALD_GPU_ERR_VALIDATION, "plan has no distances loaded");
-  tr1 = std::min(tr1, p->nb);
-  if (tr0 >= tr1) return PALD_GPU_OK;
+  if (parts < 1 || part >= parts) return set_error(PALD_GPU_ERR_VALIDATION, "invalid share %llu of %llu",
+                                                   (unsigned long long)part, (unsigned long long)parts);
   if (p->focus_dirty) {  // counts accumulate into W: start from zero again
     PALD_CUDA(cudaMemsetAsync(p->u, 0, p->n * p->ld * 4, s));
     PALD_CUDA(cudaMemsetAsync(p->w, 0, p->n * p->ld * 4, s));
   }
   p->focus_dirty = true;
-  long long tiles = 0;
-  for (uint64_t t = tr0; t < tr1; ++t) tiles += (long long)(p->nb - t);
-  KernelArgs a{p->ds, p->u, p->w, p->c, (int)p->n, (int)p->ld, (int)p->nb, (int)tr0, (int)tr1, tiles};
-  const long long units = tiles * (long long)((p->n + kBK - 1) / kBK);
-  const int grid = (int)std::min<long long>(units, p->sms);
+  const uint64_t units = focus_units(p);
+  const long long ub = (long long)(units * part / parts), ue = (long long)(units * (part + 1) / parts);
+  if (ue <= ub) return PALD_GPU_OK;
+  const long long tiles = (long long)(p->nb * (p->nb + 1) / 2);
+  KernelArgs a{p->ds, p->u, p->w, p->c, (int)p->n, (int)p->ld, (int)p->nb, 0, (int)p->nb, tiles, ub, ue};
+  const int grid = (int)std::min<long long>(ue - ub, p->sms);
   int rc;
   const bool tri = p->algorithm == PALD_GPU_TRIPLET;
   if (!p->exact) {
@@ -370,10 +377,23 @@ int plan_focus_impl(pald_gpu_plan* p, uint64_t tr0, uint64_t tr1, cudaStream_t s
   }
   if (rc) return rc;
   ++p->launches;
-  focus_finish_kernel<<<(unsigned)(tiles * 4), 256, 0, s>>>(p->u, p->w, (int)p->n, (int)p->ld, (int)p->nb, (int)tr0);
+  return PALD_GPU_OK;
+}
+
+// Counts -> U and W = 1/U over the whole matrix.
+int plan_focus_finish_impl(pald_gpu_plan* p, cudaStream_t s) {
+  if (!p->loaded) return set_error(PALD_GPU_ERR_VALIDATION, "plan has no distances loaded");
+  const uint64_t tiles = p->nb * (p->nb + 1) / 2;
+  focus_finish_kernel<<<(unsigned)(tiles * 4), 256, 0, s>>>(p->u, p->w, (int)p->n, (int)p->ld, (int)p->nb, 0);
   PALD_CUDA(cudaGetLastError());
   ++p->launches;
   return PALD_GPU_OK;
+}
+
+int plan_focus_impl(pald_gpu_plan* p, cudaStream_t s) {
+  int rc = plan_focus_counts_impl(p, 0, 1, s);
+  if (rc) return rc;
+  return plan_focus_finish_impl(p, s);
 }
 
 int plan_cohesion_impl(pald_gpu_plan* p, uint64_t row0, uint64_t row1, cudaStream_t s) {
@@ -384,7 +404,7 @@ int plan_cohesion_impl(pald_gpu_plan* p, uint64_t row0, uint64_t row1, cudaStrea
     return set_error(PALD_GPU_ERR_VALIDATION, "cohesion row range must be aligned to %d", kTile);
   const uint64_t tr0 = row0 / kTile, tr1 = (row1 + kTile - 1) / kTile;
   const long long tiles = (long long)((tr1 - tr0) * p->nb);
-  KernelArgs a{p->ds, p->u, p->w, p->c, (int)p->n, (int)p->ld, (int)p->nb, (int)tr0, (int)tr1, tiles};
+  KernelArgs a{p->ds, p->u, p->w, p->c, (int)p->n, (int)p->ld, (int)p->nb, (int)tr0, (int)tr1, tiles, 0, 0};
   const int grid = (int)std::min<long long>(tiles, p->sms);
   int rc;
   const bool tri = p->algorithm == PALD_GPU_TRIPLET;
@@ -443,13 +463,7 @@ const char* pald_gpu_last_error(void) { return g_last_error.c_str(); }
 
 int pald_gpu_abi_version(void) { return PALD_GPU_ABI_VERSION; }
 
-double pald_gpu_focus_work_prefix(uint64_t n, uint64_t tile_rows) {
-  const uint64_t nb = (n + kTile - 1) / kTile;
-  const double total = (double)nb * (nb + 1) / 2.0;
-  double pre = 0;
-  for (uint64_t t = 0; t < std::min(tile_rows, nb); ++t) pre += (double)(nb - t);
-  return pre / total;
-}
+uint64_t pald_gpu_focus_units(const pald_gpu_plan* p) { return p ? focus_units(p) : 0; }
 
 int pald_gpu_plan_create(uint64_t n, const pald_gpu_opts* o, pald_gpu_plan** out) {
   int rc = check_opts(o);
@@ -497,10 +511,22 @@ int pald_gpu_plan_load_host(pald_gpu_plan* p, const float* D, void* stream) {
   return plan_load_impl(p, p->c, p->ld, s);
 }
 
-int pald_gpu_plan_focus(pald_gpu_plan* p, uint64_t tr0, uint64_t tr1, void* stream) {
+int pald_gpu_plan_focus(pald_gpu_plan* p, void* stream) {
   if (!p) return set_error(PALD_GPU_ERR_VALIDATION, "null plan");
   DeviceGuard g(p->device);
-  return plan_focus_impl(p, tr0, tr1, static_cast<cudaStream_t>(stream));
+  return plan_focus_impl(p, static_cast<cudaStream_t>(stream));
+}
+
+int pald_gpu_plan_focus_counts(pald_gpu_plan* p, uint64_t part, uint64_t parts, void* stream) {
+  if (!p) return set_error(PALD_GPU_ERR_VALIDATION, "null plan");
+  DeviceGuard g(p->device);
+  return plan_focus_counts_impl(p, part, parts, static_cast<cudaStream_t>(stream));
+}
+
+int pald_gpu_plan_focus_finish(pald_gpu_plan* p, void* stream) {
+  if (!p) return set_error(PALD_GPU_ERR_VALIDATION, "null plan");
+  DeviceGuard g(p->device);
+  return plan_focus_finish_impl(p, static_cast<cudaStream_t>(stream));
 }
 
 int pald_gpu_plan_cohesion(pald_gpu_plan* p, uint64_t r0, uint64_t r1, void* stream) {
@@ -540,7 +566,7 @@ int pald_gpu_cohesion_f32_device(const float* dD, uint64_t ldd, uint64_t n,
   if ((rc = get_cached_plan(dev, n, o, &p))) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if ((rc = plan_load_impl(p, dD, ldd, s))) return rc;
-  if ((rc = plan_focus_impl(p, 0, p->nb, s))) return rc;
+  if ((rc = plan_focus_impl(p, s))) return rc;
   if ((rc = plan_cohesion_impl(p, 0, n, s))) return rc;
   if (dU) PALD_CUDA(cudaMemcpy2DAsync(dU, ldu * 4, p->u, p->ld * 4, n * 4, n, cudaMemcpyDeviceToDevice, s));
   PALD_CUDA(cudaMemcpy2DAsync(dC, ldc * 4, p->c, p->ld * 4, n * 4, n, cudaMemcpyDeviceToDevice, s));
@@ -577,7 +603,7 @@ int pald_gpu_cohesion_f32(const float* D, uint64_t n, const pald_gpu_opts* o, in
   PALD_CUDA(cudaEventRecord(ev[0], s));
   if ((rc = pald_gpu_plan_load_host(p, D, s))) return rc;
   PALD_CUDA(cudaEventRecord(ev[1], s));
-  if ((rc = plan_focus_impl(p, 0, p->nb, s))) return rc;
+  if ((rc = plan_focus_impl(p, s))) return rc;
   PALD_CUDA(cudaEventRecord(ev[2], s));
   if ((rc = plan_cohesion_impl(p, 0, n, s))) return rc;
   PALD_CUDA(cudaEventRecord(ev[3], s));

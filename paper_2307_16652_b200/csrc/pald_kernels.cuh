@@ -63,9 +63,11 @@ struct KernelArgs {
   int n;
   int ld;
   int nb;                // tiles per dimension
-  int tile_row_begin;    // first tile row of this launch
+  int tile_row_begin;    // cohesion: first tile row of this launch
   int tile_row_end;
-  long long total_tiles; // tiles covered by this launch
+  long long total_tiles; // cohesion: tiles covered by this launch
+  long long unit_begin;  // focus: work units [unit_begin, unit_end) of the
+  long long unit_end;    //        whole upper triangle (u = tile*nchunks + chunk)
 };
 
 // ---------------------------------------------------------------------------
@@ -234,10 +236,12 @@ __device__ __forceinline__ void tile_coords(int t, int tr_begin, int nb, int& tr
 // ---------------------------------------------------------------------------
 // The persistent tile kernel. Each CTA (one per SM) owns a contiguous range
 // of work units u = tile * nchunks + chunk:
-//   focus    (PASS 0): an equal share of all units ("stream-K"); partial
-//            tiles are combined exactly with red.global.add.f32 of integer
-//            counts (< 2^24) into the count buffer, converted to U and
-//            W = 1/U by focus_finish_kernel;
+//   focus    (PASS 0): an equal share of the launch's unit range
+//            ("stream-K"); partial tiles are combined exactly with
+//            red.global.add.f32 of integer counts (< 2^24) into the count
+//            buffer (W), converted to U and W = 1/U by focus_finish_kernel.
+//            Ranks of a multi-GPU run take equal unit ranges and SUM the
+//            count buffers before the finish;
 //   cohesion (PASS 1): whole tiles only, so every C entry is one in-order
 //            fp32 sum (bit-identical to the reference).
 // TMA streams 32-row chunks of the A/B(/W) panels through a 4-stage
@@ -264,9 +268,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   // Work units u = tile * nchunks + chunk (< 2^31 for n <= 2^17).
   int u0, u1;
   if (PASS == 0) {
-    const long long U = (long long)total_tiles * nchunks;
-    u0 = (int)(U * g / G);
-    u1 = (int)(U * (g + 1) / G);
+    // focus: an equal share of this launch's unit range ("stream-K"), over
+    // the linear upper-triangular tile order of the whole matrix
+    const long long U = args.unit_end - args.unit_begin;
+    u0 = (int)(args.unit_begin + U * g / G);
+    u1 = (int)(args.unit_begin + U * (g + 1) / G);
   } else {
     u0 = (int)((long long)total_tiles * g / G) * nchunks;
     u1 = (int)((long long)total_tiles * (g + 1) / G) * nchunks;
@@ -288,7 +294,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int u = u0 + p;
     const int t = u / nchunks, ch = u - t * nchunks;
     int tr, tc;
-    tile_coords<PASS>(t, args.tile_row_begin, nb, tr, tc);
+    tile_coords<PASS>(t, PASS == 0 ? 0 : args.tile_row_begin, nb, tr, tc);
     const int r0 = tr * kTile, c0 = tc * kTile;
     const int s = p % kStages;
     const int k0 = ch * kBK, k1 = min(k0 + kBK, n);
@@ -317,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---- one tile (possibly partial for the focus stream-K split) ---------
     const int ch_end = min(nchunks, ch_begin + (P - p));
     int tr, tc;
-    tile_coords<PASS>(t, args.tile_row_begin, nb, tr, tc);
+    tile_coords<PASS>(t, PASS == 0 ? 0 : args.tile_row_begin, nb, tr, tc);
     const int r0 = tr * kTile, c0 = tc * kTile;
     float2 thr[8][4];
     float2 acc[8][4];

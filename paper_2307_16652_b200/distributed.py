@@ -2,12 +2,13 @@
 
 Work decomposition:
   * D is replicated (every rank lays out the same fp32 matrix).
-  * Pass 1 (focus): the upper-triangular 128x128 pair-tile grid is split
-    into contiguous tile-row ranges of equal work (row t holds nb - t tiles;
-    the reference's analogue is the z-split of parallel.hpp:185-204). Each
-    rank writes U and W = 1/U for its tiles and their mirror images; every
-    entry is written by exactly one rank and is 0 elsewhere, so a SUM
-    all-reduce assembles both matrices exactly (integer / single nonzero).
+  * Pass 1 (focus): the work units (upper-triangular 128x128 pair tile x
+    32-point chunk of third points) are split into equal contiguous shares,
+    one per rank (exact balance; the reference's analogue is the z-split of
+    parallel.hpp:185-204 with private partial counts summed). Each rank
+    accumulates integer focus counts; one SUM all-reduce of the count
+    buffer (exact: integers < 2^24 in fp32) and a local finish give every
+    rank the full U and W = 1/U.
   * Pass 2 (cohesion): C rows are split into equal bands of tile rows (each
     row costs the same n^2 work). No reduction is needed: each C row is a
     complete in-order sum on one rank (bit-identical to 1 GPU), and the
@@ -21,22 +22,6 @@ from dataclasses import dataclass
 
 import torch
 import torch.distributed as dist
-
-
-def focus_tile_split(nb: int, world: int) -> list[tuple[int, int]]:
-    """Contiguous tile-row ranges [t0, t1) of ~equal pass-1 work."""
-    total = nb * (nb + 1) // 2
-    bounds = [0]
-    acc = 0
-    t = 0
-    for k in range(1, world):
-        target = total * k / world
-        while t < nb and acc + (nb - t) / 2 <= target:
-            acc += nb - t
-            t += 1
-        bounds.append(t)
-    bounds.append(nb)
-    return [(bounds[i], bounds[i + 1]) for i in range(world)]
 
 
 def cohesion_row_split(n: int, tile: int, world: int) -> list[tuple[int, int]]:
@@ -54,17 +39,15 @@ def cohesion_row_split(n: int, tile: int, world: int) -> list[tuple[int, int]]:
 class ShardPlan:
     rank: int
     world: int
-    focus_tiles: tuple[int, int]
+    focus_share: tuple[int, int]      # (part, parts) of the pass-1 work units
     cohesion_rows: tuple[int, int]
     band_rows: int  # padded rows per rank for the C all-gather
 
 
 def make_shard_plan(n: int, tile: int, rank: int, world: int) -> ShardPlan:
-    nb = (n + tile - 1) // tile
-    f = focus_tile_split(nb, world)
     c = cohesion_row_split(n, tile, world)
     band = max(r1 - r0 for r0, r1 in c)
-    return ShardPlan(rank, world, f[rank], c[rank], band)
+    return ShardPlan(rank, world, (rank, world), c[rank], band)
 
 
 class ShardedRunner:
@@ -75,13 +58,12 @@ class ShardedRunner:
     interface -- the CPU tests use a gloo-backed stand-in).
     """
 
-    def __init__(self, engine, group=None, gather_u: bool = True):
+    def __init__(self, engine, group=None):
         self.engine = engine
         self.group = group
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.plan = make_shard_plan(engine.n, engine.tile, self.rank, self.world)
-        self.gather_u = gather_u
         ld = engine.ld
         self._even = all(r1 - r0 == self.plan.band_rows
                          for r0, r1 in cohesion_row_split(engine.n, engine.tile, self.world))
@@ -92,11 +74,10 @@ class ShardedRunner:
             self._recv = torch.empty(self.world * self.plan.band_rows * ld, dtype=torch.float32, device=dev)
 
     def exchange_focus(self) -> None:
-        if self.world == 1:
-            return
-        dist.all_reduce(self.engine.full_W(), op=dist.ReduceOp.SUM, group=self.group)
-        if self.gather_u:
-            dist.all_reduce(self.engine.full_U(), op=dist.ReduceOp.SUM, group=self.group)
+        """SUM the integer focus counts over ranks, then finish locally."""
+        if self.world > 1:
+            dist.all_reduce(self.engine.full_W(), op=dist.ReduceOp.SUM, group=self.group)
+        self.engine.focus_finish()
 
     def gather_cohesion(self) -> None:
         if self.world == 1:
@@ -120,7 +101,7 @@ class ShardedRunner:
     def step(self, D, stream=None) -> None:
         e, p = self.engine, self.plan
         e.load(D, stream)
-        e.focus(*p.focus_tiles, stream=stream)
+        e.focus_counts(*p.focus_share, stream=stream)
         self.exchange_focus()
         e.cohesion(*p.cohesion_rows, stream=stream)
         self.gather_cohesion()

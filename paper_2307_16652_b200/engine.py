@@ -35,7 +35,8 @@ class Engine:
 
     Steps (each asynchronous on ``stream`` unless noted):
       load(D)                 validate + range check (one small sync) + layout
-      focus(tr0, tr1)         pass 1 over pair-tile rows [tr0, tr1)
+      focus()                 pass 1: U and W = 1/U
+        = focus_counts(part, parts) + focus_finish()   (multi-GPU split)
       cohesion(r0, r1)        pass 2 over C rows [r0, r1)
     Views: ``U``, ``W``, ``C`` (n x n, strided by ld).
     """
@@ -118,11 +119,21 @@ class Engine:
         ptr = D.data_ptr() if isinstance(D, torch.Tensor) else D.ctypes.data
         _raise_for(self.lib.pald_gpu_plan_load_host(self._plan, ptr, self._stream(stream)))
 
-    def focus(self, tile_row_begin: int = 0, tile_row_end: int | None = None, stream=None) -> None:
-        if tile_row_end is None:
-            tile_row_end = self.tiles_per_dim
-        _raise_for(self.lib.pald_gpu_plan_focus(self._plan, tile_row_begin, tile_row_end,
-                                                self._stream(stream)))
+    def focus(self, stream=None) -> None:
+        """Pass 1 over all pairs: U and W = 1/U."""
+        _raise_for(self.lib.pald_gpu_plan_focus(self._plan, self._stream(stream)))
+
+    def focus_counts(self, part: int = 0, parts: int = 1, stream=None) -> None:
+        """Pass 1, share `part` of `parts` equal shares: counts into W."""
+        _raise_for(self.lib.pald_gpu_plan_focus_counts(self._plan, part, parts, self._stream(stream)))
+
+    def focus_finish(self, stream=None) -> None:
+        """Counts (W buffer, summed over ranks) -> U and W = 1/U."""
+        _raise_for(self.lib.pald_gpu_plan_focus_finish(self._plan, self._stream(stream)))
+
+    @property
+    def focus_units(self) -> int:
+        return int(self.lib.pald_gpu_focus_units(self._plan))
 
     def cohesion(self, row_begin: int = 0, row_end: int | None = None, stream=None) -> None:
         if row_end is None:
@@ -160,6 +171,3 @@ def points_to_distances(points: torch.Tensor, out: torch.Tensor | None = None, s
                                                 out.stride(0), s))
     return out
 
-
-def work_prefix(n: int, tile_rows: int) -> float:
-    return float(_lib.load().pald_gpu_focus_work_prefix(n, tile_rows))
