@@ -279,3 +279,50 @@ void pald_oracle_row_sums_f32(const float* c, uint64_t n, double* out) {
     out[x] = s;
   }
 }
+
+/* ---- sampled-row triplet restatement ----------------------------------- */
+
+/* 1 iff {p, q} is the pair the triplet algorithm credits for the triple
+ * {p, q, o} (p, q, o distinct): sort to a < b < c and apply the branch
+ * structure of triplet_entrywise, reference.hpp:171-180 / 194-203
+ * (r: (a,b); else s: (a,c) if d_ac < d_bc; else t: (b,c)). */
+static int triplet_closest_is(const float* d, uint64_t n, uint64_t p, uint64_t q, uint64_t o) {
+  uint64_t a = p, b = q, c = o, t;
+  if (a > b) { t = a; a = b; b = t; }
+  if (b > c) { t = b; b = c; c = t; }
+  if (a > b) { t = a; a = b; b = t; }
+  const float dab = d[a * n + b], dac = d[a * n + c], dbc = d[b * n + c];
+  uint64_t u, v;
+  if (dab < dac && dab < dbc) { u = a; v = b; }
+  else if (dac < dbc) { u = a; v = c; }
+  else { u = b; v = c; }
+  return (u == p && v == q) || (u == q && v == p);
+}
+
+/* Rows of the triplet result (U int32, C double before fill_diagonal),
+ * O(n^2) per row: u_pq = 2 + #{o : (p,q) is incremented} = n - #{o : (p,q)
+ * is the credited pair}; c_pq = sum_o 1/u_po over the o for which (p,q) is
+ * credited (the two cohesion updates of each case credit the pair's
+ * members with 1/u of their pairs with the third point). */
+void pald_oracle_triplet_rows_f64(const float* d, uint64_t n, const int64_t* rows, uint64_t nrows,
+                                  int32_t* u_rows, double* c_rows) {
+  for (uint64_t i = 0; i < nrows; ++i) {
+    const uint64_t p = (uint64_t)rows[i];
+    int32_t* ur = u_rows + i * n;
+    double* cr = c_rows + i * n;
+    for (uint64_t q = 0; q < n; ++q) {
+      if (q == p) { ur[q] = 0; continue; }
+      int32_t cnt = 0;
+      for (uint64_t o = 0; o < n; ++o)
+        if (o != p && o != q) cnt += triplet_closest_is(d, n, p, q, o);
+      ur[q] = (int32_t)n - cnt;
+    }
+    for (uint64_t q = 0; q < n; ++q) {
+      double s = 0.0;
+      if (q != p)
+        for (uint64_t o = 0; o < n; ++o)
+          if (o != p && o != q && triplet_closest_is(d, n, p, q, o)) s += 1.0 / ur[o];
+      cr[q] = s;
+    }
+  }
+}
