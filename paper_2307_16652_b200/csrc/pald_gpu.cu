@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -243,6 +244,7 @@ struct pald_gpu_plan {
   bool exact = false;
   bool focus_dirty = false;
   int sms = 148;
+  int2* focus_tiles = nullptr;  // grouped upper-triangular tile order
   uint64_t launches = 0;
 
   ~pald_gpu_plan() {
@@ -256,6 +258,7 @@ struct pald_gpu_plan {
     cudaFree(c);
     cudaFree(stats);
     cudaFreeHost(stats_host);
+    cudaFree(focus_tiles);
     cudaSetDevice(prev);
   }
 };
@@ -284,6 +287,19 @@ int plan_alloc(pald_gpu_plan* p) {
   PALD_CUDA(cudaMemset(p->dnu, 0, bytes));
   PALD_CUDA(cudaMemset(p->c, 0, bytes));
   PALD_CUDA(cudaMalloc(&p->stats, sizeof(Stats)));
+  {
+    // Focus tile order: groups of kGroupRows tile rows; inside a group,
+    // column by column, the group's rows r <= c. Concurrently resident CTAs
+    // then share few row and column panels in L2.
+    std::vector<int2> order;
+    const int nb = (int)p->nb;
+    order.reserve((size_t)nb * (nb + 1) / 2);
+    for (int g0 = 0; g0 < nb; g0 += kGroupRows)
+      for (int c = g0; c < nb; ++c)
+        for (int r = g0; r < std::min(nb, g0 + kGroupRows) && r <= c; ++r) order.push_back(make_int2(r, c));
+    PALD_CUDA(cudaMalloc(&p->focus_tiles, order.size() * sizeof(int2)));
+    PALD_CUDA(cudaMemcpy(p->focus_tiles, order.data(), order.size() * sizeof(int2), cudaMemcpyHostToDevice));
+  }
   PALD_CUDA(cudaMallocHost(&p->stats_host, sizeof(Stats)));
   int rc;
   if ((rc = make_map(&p->tm_d, p->ds, p->n, p->ld))) return rc;
@@ -364,7 +380,8 @@ int plan_focus_counts_impl(pald_gpu_plan* p, uint64_t part, uint64_t parts, cuda
   const long long ub = (long long)(units * part / parts), ue = (long long)(units * (part + 1) / parts);
   if (ue <= ub) return PALD_GPU_OK;
   const long long tiles = (long long)(p->nb * (p->nb + 1) / 2);
-  KernelArgs a{p->ds, p->u, p->w, p->c, (int)p->n, (int)p->ld, (int)p->nb, 0, (int)p->nb, tiles, ub, ue};
+  KernelArgs a{p->ds, p->u, p->w, p->c, (int)p->n, (int)p->ld, (int)p->nb, 0, (int)p->nb, tiles, ub, ue,
+               p->focus_tiles, kGroupRows};
   const int grid = (int)std::min<long long>(ue - ub, p->sms);
   int rc;
   const bool tri = p->algorithm == PALD_GPU_TRIPLET;
@@ -404,7 +421,13 @@ int plan_cohesion_impl(pald_gpu_plan* p, uint64_t row0, uint64_t row1, cudaStrea
     return set_error(PALD_GPU_ERR_VALIDATION, "cohesion row range must be aligned to %d", kTile);
   const uint64_t tr0 = row0 / kTile, tr1 = (row1 + kTile - 1) / kTile;
   const long long tiles = (long long)((tr1 - tr0) * p->nb);
-  KernelArgs a{p->ds, p->u, p->w, p->c, (int)p->n, (int)p->ld, (int)p->nb, (int)tr0, (int)tr1, tiles, 0, 0};
+  const long long nch = (long long)((p->n + kBK - 1) / kBK);
+  static const int group_rows = [] {
+    const char* e = getenv("PALD_GPU_GROUP_ROWS");  // tuning knob (default kGroupRows)
+    return e ? std::max(1, atoi(e)) : kGroupRows;
+  }();
+  KernelArgs a{p->ds, p->u, p->w, p->c, (int)p->n, (int)p->ld, (int)p->nb, (int)tr0, (int)tr1, tiles, 0,
+               tiles * nch, nullptr, group_rows};
   const int grid = (int)std::min<long long>(tiles, p->sms);
   int rc;
   const bool tri = p->algorithm == PALD_GPU_TRIPLET;

@@ -66,9 +66,13 @@ struct KernelArgs {
   int tile_row_begin;    // cohesion: first tile row of this launch
   int tile_row_end;
   long long total_tiles; // cohesion: tiles covered by this launch
-  long long unit_begin;  // focus: work units [unit_begin, unit_end) of the
-  long long unit_end;    //        whole upper triangle (u = tile*nchunks + chunk)
+  long long unit_begin;  // work units [unit_begin, unit_end), u = tile*nchunks + chunk, tile
+  long long unit_end;    // index in the launch's tile order (focus: the whole upper triangle)
+  const int2* focus_tiles;  // focus tile order: (tile row, tile col), grouped raster
+  int group_rows;           // cohesion raster group height (tile rows)
 };
+
+constexpr int kGroupRows = 16;  // tile rows per raster group (L2 reuse of the panels)
 
 // ---------------------------------------------------------------------------
 // mbarrier / TMA primitives (PTX).
@@ -210,27 +214,96 @@ __device__ __forceinline__ void k_step_sel(const float* __restrict__ sa, const f
   }
 }
 
-// Tile index -> (tile row, tile col). Focus: upper-triangular tiles of tile
-// rows [tr_begin, tr_end) in row-major order; cohesion: all tiles of those
-// rows.
+// Focus-finish tile index -> (tile row, tile col): upper-triangular tiles in
+// row-major order.
+__device__ __forceinline__ void tri_coords(int t, int nb, int& tr, int& tc) {
+  const double bb = 2.0 * nb + 1.0;
+  int r = (int)((bb - sqrt(bb * bb - 8.0 * (double)t)) * 0.5);
+  r = max(0, min(r, nb - 1));
+  auto S = [&](int rr) { return rr * nb - rr * (rr - 1) / 2; };
+  while (r > 0 && S(r) > t) --r;
+  while (r + 1 < nb && S(r + 1) <= t) ++r;
+  tr = r;
+  tc = r + (t - S(r));
+}
+
+// Launch tile index -> (tile row, tile col).
+//   focus:    the plan's grouped upper-triangular order (args.focus_tiles);
+//   cohesion: grouped raster over tile rows [tile_row_begin, tile_row_end) x
+//             all tile columns: groups of kGroupRows rows, column-major inside
+//             a group, so the ~148 concurrently resident tiles share a few
+//             row panels and column panels in L2.
 template <int PASS>
-__device__ __forceinline__ void tile_coords(int t, int tr_begin, int nb, int& tr, int& tc) {
+__device__ __forceinline__ void tile_coords(const KernelArgs& a, int t, int& tr, int& tc) {
   if (PASS == 0) {
-    // rows start at S(r) = r*nb - r*(r-1)/2 (relative to row 0); solve for r.
-    const long long base = (long long)tr_begin * nb - (long long)tr_begin * (tr_begin - 1) / 2;
-    const long long g = base + t;
-    const double bb = 2.0 * nb + 1.0;
-    int r = (int)((bb - sqrt(bb * bb - 8.0 * (double)g)) * 0.5);
-    r = max(0, min(r, nb - 1));
-    auto S = [&](long long rr) { return rr * nb - rr * (rr - 1) / 2; };
-    while (r > 0 && S(r) > g) --r;
-    while (r + 1 < nb && S(r + 1) <= g) ++r;
-    tr = r;
-    tc = r + (int)(g - S(r));
+    const int2 v = a.focus_tiles[t];
+    tr = v.x;
+    tc = v.y;
   } else {
-    tr = tr_begin + t / nb;
-    tc = t % nb;
+    const int nrows = a.tile_row_end - a.tile_row_begin, gr = a.group_rows;
+    const int grp = t / (gr * a.nb);
+    const int rows_in = min(gr, nrows - grp * gr);
+    const int local = t - grp * gr * a.nb;
+    tc = local / rows_in;
+    tr = a.tile_row_begin + grp * gr + (local - tc * rows_in);
   }
+}
+
+// Work split of a launch over its G CTAs (hybrid data-parallel + stream-K):
+// whole tiles in rounds of G (CTA g takes tiles t_a + j*G + g), then the
+// remainder -- the partial head tile, the leftover tiles and the partial
+// tail tile -- split into equal contiguous unit shares (focus) or one whole
+// leftover tile per CTA (cohesion, whose tiles are never split).
+struct WorkSplit {
+  int C;          // chunks per tile
+  int t_a;        // first whole tile
+  int full;       // rounds of whole tiles
+  int head_len;   // remainder part 1: units [ub, ub + head_len)
+  long long ub;
+  long long mid;  // remainder part 2 starts at unit `mid`
+  int rs, re;     // this CTA's remainder share [rs, re)
+  __device__ __forceinline__ long long rem_unit(int q) const {
+    return q < head_len ? ub + q : mid + (q - head_len);
+  }
+  __device__ __forceinline__ long long unit_of(int p, int g, int G) const {
+    if (p < full * C) {
+      const int j = p / C;
+      return (long long)(t_a + j * G + g) * C + (p - j * C);
+    }
+    return rem_unit(rs + (p - full * C));
+  }
+};
+
+template <int PASS>
+__device__ __forceinline__ WorkSplit make_split(const KernelArgs& a, int C, int g, int G) {
+  WorkSplit w;
+  w.C = C;
+  w.ub = a.unit_begin;
+  const long long ue = a.unit_end;
+  long long ta = (w.ub + C - 1) / C, tb = ue / C;
+  if (ta > tb) {  // the range lies inside one tile
+    ta = tb = w.ub / C;
+    w.t_a = (int)ta;
+    w.full = 0;
+    w.head_len = (int)(ue - w.ub);
+    w.mid = ue;
+  } else {
+    w.t_a = (int)ta;
+    const int M = (int)(tb - ta);
+    w.full = M / G;
+    w.head_len = (int)(ta * C - w.ub);
+    w.mid = (ta + (long long)w.full * G) * C;
+  }
+  const int rem = w.head_len + (int)(ue - w.mid);
+  if (PASS == 0) {
+    w.rs = (int)((long long)rem * g / G);
+    w.re = (int)((long long)rem * (g + 1) / G);
+  } else {  // whole leftover tiles, one per CTA
+    const int left = rem / C;
+    w.rs = g < left ? g * C : 0;
+    w.re = g < left ? (g + 1) * C : 0;
+  }
+  return w;
 }
 
 // ---------------------------------------------------------------------------
@@ -263,40 +336,47 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int tid = threadIdx.x;
   const int n = args.n, ld = args.ld, nb = args.nb;
   const int nchunks = (n + kBK - 1) / kBK;
-  const int total_tiles = (int)args.total_tiles;
   const int G = gridDim.x, g = blockIdx.x;
-  // Work units u = tile * nchunks + chunk (< 2^31 for n <= 2^17).
-  int u0, u1;
-  if (PASS == 0) {
-    // focus: an equal share of this launch's unit range ("stream-K"), over
-    // the linear upper-triangular tile order of the whole matrix
-    const long long U = args.unit_end - args.unit_begin;
-    u0 = (int)(args.unit_begin + U * g / G);
-    u1 = (int)(args.unit_begin + U * (g + 1) / G);
-  } else {
-    u0 = (int)((long long)total_tiles * g / G) * nchunks;
-    u1 = (int)((long long)total_tiles * (g + 1) / G) * nchunks;
-  }
-  const int P = u1 - u0;
+  const WorkSplit ws = make_split<PASS>(args, nchunks, g, G);
+  const int P = ws.full * nchunks + (ws.re - ws.rs);
   if (P <= 0) return;
 
+  // Run table: run ri < full is whole tile t_a + ri*G + g; the (at most
+  // kMaxRem) remainder runs are built once by thread 0.
+  constexpr int kMaxRem = 6;
+  __shared__ int s_rem[kMaxRem][3];
+  __shared__ int s_nrem;
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full_bar[s], 1);
       done_cnt[s] = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    int nr = 0;
+    for (int q = ws.rs; q < ws.re && nr < kMaxRem;) {
+      const long long u = ws.rem_unit(q);
+      const int t = (int)(u / nchunks), ch = (int)(u - (long long)t * nchunks);
+      int len = min(nchunks - ch, ws.re - q);
+      if (q < ws.head_len) len = min(len, ws.head_len - q);
+      s_rem[nr][0] = t;
+      s_rem[nr][1] = ch;
+      s_rem[nr][2] = ch + len;
+      ++nr;
+      q += len;
+    }
+    s_nrem = nr;
   }
   __syncthreads();
+  const int R = ws.full + s_nrem;
+  auto run_t = [&](int ri) { return ri < ws.full ? ws.t_a + ri * G + g : s_rem[ri - ws.full][0]; };
+  auto run_c0 = [&](int ri) { return ri < ws.full ? 0 : s_rem[ri - ws.full][1]; };
+  auto run_c1 = [&](int ri) { return ri < ws.full ? nchunks : s_rem[ri - ws.full][2]; };
 
   constexpr int SB = stage_bytes(PASS);
-  auto issue = [&](int p) {
-    const int u = u0 + p;
-    const int t = u / nchunks, ch = u - t * nchunks;
+  auto issue = [&](int t, int ch, int s) {
     int tr, tc;
-    tile_coords<PASS>(t, PASS == 0 ? 0 : args.tile_row_begin, nb, tr, tc);
+    tile_coords<PASS>(args, t, tr, tc);
     const int r0 = tr * kTile, c0 = tc * kTile;
-    const int s = p % kStages;
     const int k0 = ch * kBK, k1 = min(k0 + kBK, n);
     // Uniform per-chunk transform choice: the whole chunk lies below the
     // column (A) / row (B) tile => every element takes nu().
@@ -308,8 +388,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_load_2d(st + kBoxBytes, mb, c0, k0, &full_bar[s]);
     if (PASS == 1) tma_load_2d(st + 2 * kBoxBytes, &tm_w, r0, k0, &full_bar[s]);
   };
-  if (tid == 0) {
-    for (int p = 0; p < kStages && p < P; ++p) issue(p);
+  // Producer iterator (run index, chunk) of unit p + kStages, kept by every
+  // warp's lane 0 so that whichever warp releases a stage can refill it.
+  int pr_ri = 0, pr_ch = R > 0 ? run_c0(0) : 0;
+  auto pr_advance = [&]() {
+    if (++pr_ch >= run_c1(pr_ri)) {
+      ++pr_ri;
+      if (pr_ri < R) pr_ch = run_c0(pr_ri);
+    }
+  };
+  for (int p = 0; p < kStages && p < P; ++p) {
+    if (tid == 0) issue(run_t(pr_ri), pr_ch, p);
+    pr_advance();
   }
 
   const int warp = tid >> 5, lane = tid & 31;
@@ -317,13 +407,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int tx = (warp & 1) * 8 + (lane & 7);    // 0..15
 
   int p = 0;
-  int t = u0 / nchunks;
-  int ch_begin = u0 - t * nchunks;
-  while (p < P) {
-    // ---- one tile (possibly partial for the focus stream-K split) ---------
-    const int ch_end = min(nchunks, ch_begin + (P - p));
+  for (int ri = 0; ri < R; ++ri) {
+    const int t = run_t(ri), ch_begin = run_c0(ri), ch_end = run_c1(ri);
     int tr, tc;
-    tile_coords<PASS>(t, PASS == 0 ? 0 : args.tile_row_begin, nb, tr, tc);
+    tile_coords<PASS>(args, t, tr, tc);
     const int r0 = tr * kTile, c0 = tc * kTile;
     float2 thr[8][4];
     float2 acc[8][4];
@@ -372,7 +459,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) {
         const uint32_t old = atomicAdd(&done_cnt[s], 1u);
         if (old == (uint32_t)(p / kStages + 1) * (kThreads / 32) - 1u && p + kStages < P)
-          issue(p + kStages);
+          issue(run_t(pr_ri), pr_ch, s);
+        pr_advance();
       }
     }
 
@@ -412,8 +500,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (cb < n) *reinterpret_cast<float4*>(crow + cb) = make_float4(v[4], v[5], v[6], v[7]);
       }
     }
-    ++t;
-    ch_begin = 0;
   }
 }
 
@@ -429,7 +515,7 @@ __global__ void __launch_bounds__(256)
   constexpr int Q = kTile / 2;
   __shared__ float tile[Q][Q + 1];
   int tr, tc;
-  tile_coords<0>(blockIdx.x >> 2, tr_begin, nb, tr, tc);
+  tri_coords(blockIdx.x >> 2, nb, tr, tc);
   const int qr = (blockIdx.x >> 1) & 1, qc = blockIdx.x & 1;
   if (tr == tc && qr > qc) return;  // below the diagonal: the mirror of (0,1)
   const int r0 = tr * kTile + qr * Q, c0 = tc * kTile + qc * Q;
