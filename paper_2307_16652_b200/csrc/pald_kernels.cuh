@@ -46,14 +46,22 @@
 namespace pald_gpu {
 
 constexpr int kTile = 128;      // pair-tile edge (rows and columns)
-constexpr int kBK = 32;         // third-point chunk per pipeline stage
+#ifndef PALD_BK
+#define PALD_BK 64
+#endif
+constexpr int kBK = PALD_BK;    // third-point chunk per pipeline stage
 constexpr int kThreads = 256;   // 8 warps, 16 x 16 threads, 8 x 8 outputs each
-constexpr int kStages = 4;
+// Pipeline depth per pass so that stages x stage_bytes fits the 227 KB of
+// shared memory (focus: 2 boxes per stage, cohesion: 3).
+__host__ __device__ constexpr int stages_for(int pass) {
+  return (pass == 0 ? 2 : 3) * kBK * 128 * 4 * 4 <= 200 * 1024 ? 4
+         : (pass == 0 ? 2 : 3) * kBK * 128 * 4 * 3 <= 200 * 1024 ? 3 : 2;
+}
 constexpr int kBoxBytes = kBK * kTile * 4;  // one TMA box (16 KB)
 constexpr float kCmpScale = 0x1p125f;       // S of the FFMA.SAT compare
 
 __host__ __device__ constexpr int stage_bytes(int pass) { return (pass == 0 ? 2 : 3) * kBoxBytes; }
-__host__ __device__ constexpr int smem_bytes(int pass) { return kStages * stage_bytes(pass) + 1024; }
+__host__ __device__ constexpr int smem_bytes(int pass) { return stages_for(pass) * stage_bytes(pass) + 1024; }
 
 struct KernelArgs {
   const uint32_t* d;     // layout of D (scaled fp32 bits or integer keys), n x ld
@@ -330,6 +338,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // Align the pipeline buffers to 1 KB with an offset into the same array,
   // so the compiler keeps the shared address space (LDS, not generic LD).
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  constexpr int kStages = stages_for(PASS);
   __shared__ uint64_t full_bar[kStages];
   __shared__ uint32_t done_cnt[kStages];
 
