@@ -46,9 +46,11 @@ extern "C" {
  * parallel.hpp:257). */
 enum pald_gpu_algorithm { PALD_GPU_PAIRWISE = 0, PALD_GPU_TRIPLET = 1 };
 
-/* Policy, types.hpp:34. The GPU engine implements Strict; InclusiveSplit
- * returns PALD_GPU_ERR_UNSUPPORTED (the triplet reference does the same,
- * blocked.hpp:429-430). */
+/* Policy, types.hpp:34. Pairwise supports both (InclusiveSplit: `<=` focus
+ * membership, support split 0.5/0.5 on ties, blocked.hpp:117,150-158; C
+ * bit-identical to blocked_pairwise<float>(..., InclusiveSplit)); triplet is
+ * Strict only and returns PALD_GPU_ERR_UNSUPPORTED otherwise, as the
+ * reference throws UnsupportedPolicyError (blocked.hpp:429-430). */
 enum pald_gpu_policy { PALD_GPU_STRICT = 0, PALD_GPU_INCLUSIVE_SPLIT = 1 };
 
 enum pald_gpu_status {

@@ -21,8 +21,9 @@
 //     the fp32 result like detail::collect_result (blocked.hpp:352-359),
 //     normalized = false;
 //   * errors: ValidationError (block sizes < 1, workers < 1),
-//     UnsupportedPolicyError (triplet with InclusiveSplit; the GPU pairwise
-//     path implements Strict), std::runtime_error for CUDA failures.
+//     UnsupportedPolicyError (triplet with InclusiveSplit, as the
+//     reference), std::runtime_error for CUDA failures. Pairwise supports
+//     both policies.
 //   * Real: the engine computes in fp32 (the reference's performance
 //     instantiation); Real = double is rejected at compile time.
 #pragma once

@@ -50,6 +50,7 @@ class Oracle:
             "pald_oracle_normalize": (None, [_vp, _u64]),
             "pald_oracle_local_depths": (None, [_vp, _u64, _vp]),
             "pald_oracle_pairwise_f32": (None, [_vp, _u64, _vp, _vp]),
+            "pald_oracle_pairwise_policy_f32": (None, [_vp, _u64, _i32, _vp, _vp]),
             "pald_oracle_pairwise_rows_f32": (None, [_vp, _u64, _vp, _u64, _vp, _vp]),
             "pald_oracle_pairwise_f32in_f64": (None, [_vp, _u64, _vp, _vp]),
             "pald_oracle_triplet_f32in_f64": (None, [_vp, _u64, _vp, _vp]),
@@ -97,12 +98,12 @@ class Oracle:
         return out
 
     # fp32-input restatements
-    def pairwise_f32(self, d: np.ndarray):
+    def pairwise_f32(self, d: np.ndarray, policy: int = 0):
         d = np.ascontiguousarray(d, np.float32)
         n = d.shape[0]
         u = np.empty((n, n), np.int32)
         c = np.empty((n, n), np.float32)
-        self.lib.pald_oracle_pairwise_f32(_ptr(d), n, _ptr(u), _ptr(c))
+        self.lib.pald_oracle_pairwise_policy_f32(_ptr(d), n, policy, _ptr(u), _ptr(c))
         return u, c
 
     def pairwise_rows_f32(self, d: np.ndarray, rows) -> tuple[np.ndarray, np.ndarray]:

@@ -154,14 +154,18 @@ void pald_oracle_local_depths(const double* c, uint64_t n, double* depths) {
  * u_xy is pair_block_focus (blocked.hpp:101-122) summed over all z, and
  * 1/u is Real(1)/Real(cnt) (blocked.hpp:401). */
 static void pairwise_row_f32(const float* d, uint64_t n, uint64_t x, int32_t* urow, float* crow,
-                             float* wrow) {
+                             float* wrow, int policy) {
   const float* rx = d + x * n;
   for (uint64_t y = 0; y < n; ++y) {
     if (y == x) { urow[y] = 0; wrow[y] = 0.0f; continue; }
     const float* ry = d + y * n;
     const float dxy = rx[y];
     int32_t cnt = 0;
-    for (uint64_t z = 0; z < n; ++z) cnt += (rx[z] < dxy) | (ry[z] < dxy);
+    if (policy == ORACLE_STRICT) {
+      for (uint64_t z = 0; z < n; ++z) cnt += (rx[z] < dxy) | (ry[z] < dxy);
+    } else {
+      for (uint64_t z = 0; z < n; ++z) cnt += (rx[z] <= dxy) | (ry[z] <= dxy);
+    }
     urow[y] = cnt;
     wrow[y] = 1.0f / (float)cnt;
   }
@@ -170,21 +174,40 @@ static void pairwise_row_f32(const float* d, uint64_t n, uint64_t x, int32_t* ur
     if (y == x) continue;
     const float* ry = d + y * n;
     const float w = wrow[y];
-    if (y > x) {
-      const float dxy = rx[y];  /* pair (x, y): cx update */
-      for (uint64_t z = 0; z < n; ++z) {
-        const float dxz = rx[z], dyz = ry[z];
-        const int r = ((dxz < dyz ? dxz : dyz) < dxy);
-        const int s = (dxz < dyz);
-        if (r && s) crow[z] += w;
+    if (policy == ORACLE_STRICT) {
+      if (y > x) {
+        const float dxy = rx[y];  /* pair (x, y): cx update */
+        for (uint64_t z = 0; z < n; ++z) {
+          const float dxz = rx[z], dyz = ry[z];
+          const int r = ((dxz < dyz ? dxz : dyz) < dxy);
+          const int s = (dxz < dyz);
+          if (r && s) crow[z] += w;
+        }
+      } else {
+        const float dyx = ry[x];  /* pair (y, x): cy update, x is the second point */
+        for (uint64_t z = 0; z < n; ++z) {
+          const float dyz = ry[z], dxz = rx[z];
+          const int r = ((dyz < dxz ? dyz : dxz) < dyx);
+          const int s = (dyz < dxz);
+          if (r && !s) crow[z] += w;
+        }
       }
     } else {
-      const float dyx = ry[x];  /* pair (y, x): cy update, x is the second point */
+      /* InclusiveSplit, masked form blocked.hpp:150-158:
+       * r = min(d1z, d2z) <= d12, sx = [d1z < d2z] + 0.5 [d1z == d2z],
+       * first point += r*sx*w, second point += r*(1-sx)*w (one addition). */
+      const float dxy = rx[y];
       for (uint64_t z = 0; z < n; ++z) {
-        const float dyz = ry[z], dxz = rx[z];
-        const int r = ((dyz < dxz ? dyz : dxz) < dyx);
-        const int s = (dyz < dxz);
-        if (r && !s) crow[z] += w;
+        const float dxz = rx[z], dyz = ry[z];
+        const float r = ((dxz < dyz ? dxz : dyz) <= dxy) ? 1.0f : 0.0f;
+        float share;
+        if (y > x) {  /* x is the first point */
+          share = (dxz < dyz ? 1.0f : 0.0f) + 0.5f * (dxz == dyz ? 1.0f : 0.0f);
+        } else {      /* x is the second point of pair (y, x): 1 - s_y */
+          const float sy = (dyz < dxz ? 1.0f : 0.0f) + 0.5f * (dyz == dxz ? 1.0f : 0.0f);
+          share = 1.0f - sy;
+        }
+        if (r != 0.0f && share != 0.0f) crow[z] += r * share * w;
       }
     }
   }
@@ -193,7 +216,14 @@ static void pairwise_row_f32(const float* d, uint64_t n, uint64_t x, int32_t* ur
 /* Full pairwise fp32 result (U int32, C fp32) in reference order. O(n^3). */
 void pald_oracle_pairwise_f32(const float* d, uint64_t n, int32_t* u, float* c) {
   float* w = (float*)malloc(sizeof(float) * n);
-  for (uint64_t x = 0; x < n; ++x) pairwise_row_f32(d, n, x, u + x * n, c + x * n, w);
+  for (uint64_t x = 0; x < n; ++x) pairwise_row_f32(d, n, x, u + x * n, c + x * n, w, ORACLE_STRICT);
+  free(w);
+}
+
+/* Same, with a policy (0 Strict, 1 InclusiveSplit). */
+void pald_oracle_pairwise_policy_f32(const float* d, uint64_t n, int policy, int32_t* u, float* c) {
+  float* w = (float*)malloc(sizeof(float) * n);
+  for (uint64_t x = 0; x < n; ++x) pairwise_row_f32(d, n, x, u + x * n, c + x * n, w, policy);
   free(w);
 }
 
@@ -203,7 +233,7 @@ void pald_oracle_pairwise_rows_f32(const float* d, uint64_t n, const int64_t* ro
                                    uint64_t nrows, int32_t* u_rows, float* c_rows) {
   float* w = (float*)malloc(sizeof(float) * n);
   for (uint64_t i = 0; i < nrows; ++i)
-    pairwise_row_f32(d, n, (uint64_t)rows[i], u_rows + i * n, c_rows + i * n, w);
+    pairwise_row_f32(d, n, (uint64_t)rows[i], u_rows + i * n, c_rows + i * n, w, ORACLE_STRICT);
   free(w);
 }
 

@@ -182,10 +182,10 @@ int make_map(CUtensorMap* map, const void* base, uint64_t n, uint64_t ld) {
   return PALD_GPU_OK;
 }
 
-template <int PASS, bool A_NU, bool B_NU, bool T_NU, bool ZD, bool FAST>
+template <int PASS, bool A_NU, bool B_NU, bool T_NU, bool ZD, bool FAST, bool SPLIT = false>
 int launch_tile(const CUtensorMap& md, const CUtensorMap& mnu, const CUtensorMap& mw,
                 const KernelArgs& a, int grid, cudaStream_t s) {
-  auto k = pald_tile_kernel<PASS, A_NU, B_NU, T_NU, ZD, FAST>;
+  auto k = pald_tile_kernel<PASS, A_NU, B_NU, T_NU, ZD, FAST, SPLIT>;
   static bool attr_done[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -217,9 +217,6 @@ int check_opts(const pald_gpu_opts* o) {
       return set_error(PALD_GPU_ERR_VALIDATION, "triplet block sizes must be >= 1");
   } else {
     if (o->block < 1) return set_error(PALD_GPU_ERR_VALIDATION, "pairwise block size must be >= 1");
-    if (o->policy != PALD_GPU_STRICT)
-      return set_error(PALD_GPU_ERR_UNSUPPORTED,
-                       "the GPU engine implements the strict policy only (InclusiveSplit pending)");
   }
   return PALD_GPU_OK;
 }
@@ -231,6 +228,7 @@ struct pald_gpu_plan {
   int device = 0;
   uint64_t n = 0, ld = 0, nb = 0;
   int algorithm = 0;
+  int policy = 0;
   uint32_t flags = 0;
   uint32_t* ds = nullptr;
   uint32_t* dnu = nullptr;
@@ -385,12 +383,16 @@ int plan_focus_counts_impl(pald_gpu_plan* p, uint64_t part, uint64_t parts, cuda
   const int grid = (int)std::min<long long>(ue - ub, p->sms);
   int rc;
   const bool tri = p->algorithm == PALD_GPU_TRIPLET;
+  const bool split = p->policy == PALD_GPU_INCLUSIVE_SPLIT;
+  const CUtensorMap &md = p->tm_d, &mn = p->tm_dnu, &mw = p->tm_w;
   if (!p->exact) {
-    rc = tri ? launch_tile<0, true, true, true, false, true>(p->tm_d, p->tm_dnu, p->tm_w, a, grid, s)
-             : launch_tile<0, false, false, false, false, true>(p->tm_d, p->tm_dnu, p->tm_w, a, grid, s);
+    rc = tri     ? launch_tile<0, true, true, true, false, true>(md, mn, mw, a, grid, s)
+         : split ? launch_tile<0, false, false, true, false, true>(md, mn, mw, a, grid, s)  // <= : < nu(T)
+                 : launch_tile<0, false, false, false, false, true>(md, mn, mw, a, grid, s);
   } else {
-    rc = tri ? launch_tile<0, true, true, true, false, false>(p->tm_d, p->tm_dnu, p->tm_w, a, grid, s)
-             : launch_tile<0, false, false, false, false, false>(p->tm_d, p->tm_dnu, p->tm_w, a, grid, s);
+    rc = tri     ? launch_tile<0, true, true, true, false, false>(md, mn, mw, a, grid, s)
+         : split ? launch_tile<0, false, false, true, false, false>(md, mn, mw, a, grid, s)
+                 : launch_tile<0, false, false, false, false, false>(md, mn, mw, a, grid, s);
   }
   if (rc) return rc;
   ++p->launches;
@@ -431,12 +433,16 @@ int plan_cohesion_impl(pald_gpu_plan* p, uint64_t row0, uint64_t row1, cudaStrea
   const int grid = (int)std::min<long long>(tiles, p->sms);
   int rc;
   const bool tri = p->algorithm == PALD_GPU_TRIPLET;
+  const bool split = p->policy == PALD_GPU_INCLUSIVE_SPLIT;
+  const CUtensorMap &md = p->tm_d, &mn = p->tm_dnu, &mw = p->tm_w;
   if (!p->exact) {
-    rc = tri ? launch_tile<1, true, true, false, true, true>(p->tm_d, p->tm_dnu, p->tm_w, a, grid, s)
-             : launch_tile<1, false, true, false, false, true>(p->tm_d, p->tm_dnu, p->tm_w, a, grid, s);
+    rc = tri     ? launch_tile<1, true, true, false, true, true>(md, mn, mw, a, grid, s)
+         : split ? launch_tile<1, false, false, false, false, true, true>(md, mn, mw, a, grid, s)
+                 : launch_tile<1, false, true, false, false, true>(md, mn, mw, a, grid, s);
   } else {
-    rc = tri ? launch_tile<1, true, true, false, true, false>(p->tm_d, p->tm_dnu, p->tm_w, a, grid, s)
-             : launch_tile<1, false, true, false, false, false>(p->tm_d, p->tm_dnu, p->tm_w, a, grid, s);
+    rc = tri     ? launch_tile<1, true, true, false, true, false>(md, mn, mw, a, grid, s)
+         : split ? launch_tile<1, false, false, false, false, false, true>(md, mn, mw, a, grid, s)
+                 : launch_tile<1, false, true, false, false, false>(md, mn, mw, a, grid, s);
   }
   if (rc == PALD_GPU_OK) ++p->launches;
   return rc;
@@ -462,6 +468,7 @@ int get_cached_plan(int dev, uint64_t n, const pald_gpu_opts* o, pald_gpu_plan**
     slot.reset(p);
   }
   slot->algorithm = o->algorithm;
+  slot->policy = o->policy;
   slot->flags = o->flags;
   slot->loaded = false;
   *out = slot.get();
@@ -506,6 +513,7 @@ int pald_gpu_plan_create(uint64_t n, const pald_gpu_opts* o, pald_gpu_plan** out
   p->ld = round_up(n, 32);
   p->nb = (n + kTile - 1) / kTile;
   p->algorithm = o->algorithm;
+  p->policy = o->policy;
   p->flags = o->flags;
   PALD_CUDA(cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, dev));
   if ((rc = plan_alloc(p.get()))) return rc;

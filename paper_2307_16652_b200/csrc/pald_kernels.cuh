@@ -222,6 +222,49 @@ __device__ __forceinline__ void k_step_sel(const float* __restrict__ sa, const f
   }
 }
 
+// One k step of the InclusiveSplit cohesion pass (pairwise, blocked.hpp:
+// 150-158). With A' = nu(d_xy) (the A panel comes from nu(D)), B = d_yz and
+// T = d_xz, the reference's r*sx*w (r = [min(d_xz,d_yz) <= d_xy],
+// sx = [d_xz < d_yz] + 0.5 [d_xz == d_yz]) equals, for either order of the
+// pair, (w/2) * ([T < min(A', B)] + [T < min(A', nu(B))]); the sum of the
+// two indicators (0, 1, 2) times w/2 is one exact product, so each pair still
+// adds a single correctly rounded term, in ascending y.
+template <bool FAST>
+__device__ __forceinline__ void k_step_split(const float* __restrict__ sa, const float* __restrict__ sb,
+                                             const float* __restrict__ sw, int kk, int ty, int tx,
+                                             const float2 (&thr)[8][4], float2 (&acc)[8][4]) {
+  float a[8], b[8], bn[8], wh[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    a[i] = sa[kk * kTile + row_off(ty, i)];
+    wh[i] = 0.5f * sw[kk * kTile + row_off(ty, i)];
+    b[i] = sb[kk * kTile + row_off(tx, i)];
+    bn[i] = nu_f(b[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+#pragma unroll
+    for (int jp = 0; jp < 4; ++jp) {
+      float k1[2], k2[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = 2 * jp + h;
+        const float t = (h == 0) ? thr[i][jp].x : thr[i][jp].y;
+        if (FAST) {
+          k1[h] = __saturatef(__fmaf_rn(fminf(a[i], b[j]), kCmpScale, t));
+          k2[h] = __saturatef(__fmaf_rn(fminf(a[i], bn[j]), kCmpScale, t));
+        } else {
+          const uint32_t ai = __float_as_uint(a[i]), tu = __float_as_uint(t);
+          k1[h] = (tu < min(ai, __float_as_uint(b[j]))) ? 1.f : 0.f;
+          k2[h] = (tu < min(ai, __float_as_uint(bn[j]))) ? 1.f : 0.f;
+        }
+      }
+      const float2 kk2 = __fadd2_rn(make_float2(k1[0], k1[1]), make_float2(k2[0], k2[1]));
+      acc[i][jp] = __ffma2_rn(kk2, make_float2(wh[i], wh[i]), acc[i][jp]);
+    }
+  }
+}
+
 // Focus-finish tile index -> (tile row, tile col): upper-triangular tiles in
 // row-major order.
 __device__ __forceinline__ void tri_coords(int t, int nb, int& tr, int& tc) {
@@ -329,7 +372,7 @@ __device__ __forceinline__ WorkSplit make_split(const KernelArgs& a, int C, int 
 // mbarrier pipeline that runs across tile boundaries. A stage is refilled by
 // the last warp to finish with it (shared-memory arrival counter), so no
 // block-wide barrier sits in the main loop.
-template <int PASS, bool A_NU, bool B_NU, bool T_NU, bool ZERO_DIAG, bool FAST>
+template <int PASS, bool A_NU, bool B_NU, bool T_NU, bool ZERO_DIAG, bool FAST, bool SPLIT = false>
 __global__ void __launch_bounds__(kThreads, 1)
     pald_tile_kernel(const __grid_constant__ CUtensorMap tm_d,
                      const __grid_constant__ CUtensorMap tm_dnu,
@@ -389,7 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int k0 = ch * kBK, k1 = min(k0 + kBK, n);
     // Uniform per-chunk transform choice: the whole chunk lies below the
     // column (A) / row (B) tile => every element takes nu().
-    const CUtensorMap* ma = (A_NU && k1 <= c0) ? &tm_dnu : &tm_d;
+    const CUtensorMap* ma = ((PASS == 1 && SPLIT) || (A_NU && k1 <= c0)) ? &tm_dnu : &tm_d;
     const CUtensorMap* mb = (B_NU && k1 <= r0) ? &tm_dnu : &tm_d;
     uint8_t* st = smem + s * SB;
     mbar_expect_tx(&full_bar[s], SB);
@@ -456,7 +499,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool a_in = A_NU && (k0 >= c0) && (k0 < c0 + kTile);
       const bool b_in = B_NU && (k0 >= r0) && (k0 < r0 + kTile);
       const int kmax = min(kBK, n - k0);
-      if (!a_in && !b_in && kmax == kBK) {
+      if (PASS == 1 && SPLIT) {
+        for (int kk = 0; kk < kmax; ++kk) k_step_split<FAST>(sa, sb, sw, kk, ty, tx, thr, acc);
+      } else if (!a_in && !b_in && kmax == kBK) {
 #pragma unroll 2
         for (int kk = 0; kk < kBK; ++kk) k_step<PASS, FAST>(sa, sb, sw, kk, ty, tx, thr, acc);
       } else {

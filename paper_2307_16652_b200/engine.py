@@ -42,7 +42,7 @@ class Engine:
     """
 
     def __init__(self, n: int, algorithm: str = "pairwise", device: int | None = None,
-                 force_exact: bool = False, skip_validation: bool = False):
+                 force_exact: bool = False, skip_validation: bool = False, policy: str = "strict"):
         self.lib = _lib.load()
         if device is None:
             device = torch.cuda.current_device()
@@ -52,7 +52,8 @@ class Engine:
         alg = {"pairwise": _lib.PAIRWISE, "triplet": _lib.TRIPLET}[algorithm]
         flags = (_lib.FLAG_FORCE_EXACT if force_exact else 0) | (
             _lib.FLAG_SKIP_VALIDATION if skip_validation else 0)
-        opts = _lib.make_opts(algorithm=alg, device=self.device, flags=flags)
+        pol = {"strict": _lib.STRICT, "split": _lib.INCLUSIVE_SPLIT}[policy]
+        opts = _lib.make_opts(algorithm=alg, policy=pol, device=self.device, flags=flags)
         self._plan = C.c_void_p()
         _raise_for(self.lib.pald_gpu_plan_create(self.n, C.byref(opts), C.byref(self._plan)))
         b = _lib.Buffers()

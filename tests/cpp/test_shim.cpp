@@ -18,6 +18,7 @@
 #include "pald_gpu.hpp"
 
 extern "C" void pald_oracle_pairwise_f32(const float* d, uint64_t n, int32_t* u, float* c);
+extern "C" void pald_oracle_pairwise_policy_f32(const float* d, uint64_t n, int policy, int32_t* u, float* c);
 extern "C" void pald_oracle_triplet_f32in_f64(const float* d, uint64_t n, int32_t* u, double* c);
 
 static int failures = 0;
@@ -132,6 +133,16 @@ static void gpu_tests() {
         CHECK(g.focus.sizes == uo);
         bool same = true;
         for (std::size_t i = 0; i < n * n; ++i) same &= g.cohesion.values[i] == (double)co[i];
+        CHECK(same);
+      }
+      {  // InclusiveSplit (blocked.hpp:150-158), bit-exact as well
+        std::vector<int32_t> us(n * n);
+        std::vector<float> cs(n * n);
+        pald_oracle_pairwise_policy_f32(df.data(), n, 1, us.data(), cs.data());
+        const auto g = pald::gpu::blocked_pairwise<float>(d, 4, Policy::InclusiveSplit);
+        CHECK(g.focus.sizes == us);
+        bool same = true;
+        for (std::size_t i = 0; i < n * n; ++i) same &= g.cohesion.values[i] == (double)cs[i];
         CHECK(same);
       }
       pald::PhaseTimes pt;

@@ -11,6 +11,7 @@ Writes tests/golden/golden.npz. Contents (per case "<name>"):
   <name>.tr_U/C     triplet_entrywise(d)                    reference.hpp:154-208
   <name>.trf_C      blocked_triplet<float>(d, 8, 4) C       blocked.hpp:424-477
   <name>.split_U/C  pairwise_entrywise(d, InclusiveSplit)
+  <name>.splitf_C   blocked_pairwise<float>(d, b=5, InclusiveSplit) C
   <name>.fill_C     triplet C after fill_diagonal           reference.hpp:213-220
 """
 import sys
@@ -58,6 +59,8 @@ def main():
         out[f"{name}.trf_C"] = ctf
         us, cs = ref.pairwise_entrywise(d, 1)
         out[f"{name}.split_U"], out[f"{name}.split_C"] = us, cs
+        _, csf, _ = ref.blocked_pairwise(d, 5, 1, use_float=True)
+        out[f"{name}.splitf_C"] = csf
         cfill = ct.copy()
         ref.fill_diagonal(ut, cfill)
         out[f"{name}.fill_C"] = cfill

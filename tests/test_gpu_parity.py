@@ -72,3 +72,25 @@ def test_triplet(oracle, n, kind, exact):
     rs_ref = c_ref.sum(1)
     rs = c.astype(np.float64).sum(1)
     assert np.max(np.abs(rs - rs_ref) / np.maximum(rs_ref, 1.0)) <= TOL
+
+
+@pytest.mark.parametrize("exact", [False, True])
+@pytest.mark.parametrize("n,kind", [(2, "rand"), (3, "t3"), (33, "ties"), (130, "ties"), (200, "rand"), (257, "ties3")])
+def test_pairwise_inclusive_split_bit_exact(oracle, n, kind, exact):
+    from paper_2307_16652_b200.engine import Engine
+    import torch
+
+    if kind == "t3":
+        d = np.ones((3, 3), np.float32) - np.eye(3, dtype=np.float32)
+    elif kind == "rand":
+        d = random_upper(n, 5 + n)
+    elif kind == "ties":
+        d = int_upper(n, 9 + n)
+    else:
+        d = int_upper(n, 9 + n, 1, 3)
+    u_ref, c_ref = oracle.pairwise_f32(d, policy=1)
+    e = Engine(d.shape[0], "pairwise", force_exact=exact, policy="split")
+    e.run(torch.from_numpy(d).cuda())
+    torch.cuda.synchronize()
+    assert np.array_equal(e.U.cpu().numpy(), u_ref)
+    assert np.array_equal(e.C.cpu().numpy().view(np.uint32), c_ref.view(np.uint32))

@@ -95,6 +95,9 @@ def test_oracle_matches_golden(oracle, case):
     u32, c32 = oracle.pairwise_f32(d.astype(np.float32))
     assert np.array_equal(u32, g("pw_U"))
     assert np.array_equal(c32.astype(np.float64), g("pwf_C"))
+    us32, cs32 = oracle.pairwise_f32(d.astype(np.float32), policy=1)
+    assert np.array_equal(us32, g("split_U"))
+    assert np.array_equal(cs32.astype(np.float64), g("splitf_C"))
     # fp64-on-fp32 oracles: U identical to the reference's, C within tolerance
     uf, cf = oracle.pairwise_f64(d.astype(np.float32))
     assert np.array_equal(uf, g("pw_U"))
