@@ -180,6 +180,25 @@ int pald_gpu_fill_diagonal(const int32_t* dU, uint64_t ldu, uint64_t n, double* 
 int pald_gpu_points_to_distances(const double* dP, uint64_t n, uint64_t dim, float* dD,
                                  uint64_t ldd, void* stream);
 
+/* Local depths (reference.hpp:231-241) of the normalized cohesion matrix
+ * (normalize, reference.hpp:223-228), straight from the fp32 C on the
+ * device: depth_x = sum_z double(c_xz) * (1/(n-1)), z ascending, in double --
+ * the reference's arithmetic and order, bit for bit. `diag` (device, n
+ * doubles, nullable) replaces c_xx first (the triplet's fill_diagonal). */
+int pald_gpu_local_depths(const float* dC, uint64_t ldc, uint64_t n, const double* diag,
+                          double* depths_out, void* stream);
+
+/* Strong ties (analyze.hpp:34-53) of the normalized C: edges x < y with
+ * min(c'_xy, c'_yx) >= threshold, row-major order. threshold_in (device,
+ * nullable) overrides the universal threshold 0.5 * mean(c'_xx), which is
+ * written to threshold_out (device). The edge count goes to count_out
+ * (device); up to `capacity` edges are written to xs, ys, strength
+ * (device arrays, nullable to only count). */
+int pald_gpu_strong_ties(const float* dC, uint64_t ldc, uint64_t n, const double* diag,
+                         const double* threshold_in, double* threshold_out, uint64_t capacity,
+                         uint32_t* xs, uint32_t* ys, double* strength, uint64_t* count_out,
+                         void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -17,8 +17,8 @@ LIB_DIR = PKG_DIR / "lib"
 LIB_PATH = LIB_DIR / "libpald_gpu.so"
 INCLUDE = PKG_DIR.parent / "include"
 
-SOURCES = [CSRC / "pald_gpu.cu"]
-DEPS = SOURCES + [CSRC / "pald_kernels.cuh", INCLUDE / "pald_gpu.h"]
+SOURCES = [CSRC / "pald_gpu.cu", CSRC / "pald_epilogue.cu"]
+DEPS = SOURCES + [CSRC / "pald_kernels.cuh", CSRC / "pald_internal.h", INCLUDE / "pald_gpu.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -37,6 +37,8 @@ EXPORTED_SYMBOLS = (
     "pald_gpu_focus_units",
     "pald_gpu_fill_diagonal",
     "pald_gpu_points_to_distances",
+    "pald_gpu_local_depths",
+    "pald_gpu_strong_ties",
 )
 
 
@@ -116,6 +118,8 @@ def load(path: Path | None = None) -> C.CDLL:
         "pald_gpu_focus_units": (u64, [vp]),
         "pald_gpu_fill_diagonal": (i32, [vp, u64, u64, vp, vp]),
         "pald_gpu_points_to_distances": (i32, [vp, u64, u64, vp, u64, vp]),
+        "pald_gpu_local_depths": (i32, [vp, u64, u64, vp, vp, vp]),
+        "pald_gpu_strong_ties": (i32, [vp, u64, u64, vp, vp, vp, u64, vp, vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "../../include/pald_gpu.h"
+#include "pald_internal.h"
 #include "pald_kernels.cuh"
 
 using namespace pald_gpu;
@@ -676,3 +677,8 @@ int pald_gpu_points_to_distances(const double* dP, uint64_t n, uint64_t dim, flo
 }
 
 }  // extern "C"
+
+int pald_gpu_set_error(int code, const char* message) {
+  g_last_error = message;
+  return code;
+}

@@ -147,6 +147,47 @@ class Engine:
         self.focus(stream=stream)
         self.cohesion(stream=stream)
 
+    # -- epilogue: fill_diagonal, depths, strong ties -----
+    def fill_diagonal(self, stream=None) -> torch.Tensor:
+        """reference.hpp:213-220 on the device: c_xx = sum_{y!=x} 1/u_xy (double)."""
+        out = torch.empty(self.n, dtype=torch.float64, device=f"cuda:{self.device}")
+        _raise_for(self.lib.pald_gpu_fill_diagonal(self._ptrs[0], self.ld, self.n, out.data_ptr(),
+                                                   self._stream(stream)))
+        return out
+
+    def local_depths(self, diag: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """Row sums of the normalized C (reference.hpp:223-241), double."""
+        out = torch.empty(self.n, dtype=torch.float64, device=f"cuda:{self.device}")
+        _raise_for(self.lib.pald_gpu_local_depths(self._ptrs[2], self.ld, self.n,
+                                                  diag.data_ptr() if diag is not None else None,
+                                                  out.data_ptr(), self._stream(stream)))
+        return out
+
+    def strong_ties(self, diag: torch.Tensor | None = None, threshold: float | None = None,
+                    stream=None):
+        """Strong-tie graph of the normalized C (analyze.hpp:34-53):
+        returns (threshold, xs, ys, strength) with edges in row-major order."""
+        dev = f"cuda:{self.device}"
+        thr_out = torch.empty(1, dtype=torch.float64, device=dev)
+        thr_in = (torch.tensor([threshold], dtype=torch.float64, device=dev)
+                  if threshold is not None else None)
+        cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+        st = self._stream(stream)
+        dptr = diag.data_ptr() if diag is not None else None
+        tptr = thr_in.data_ptr() if thr_in is not None else None
+        _raise_for(self.lib.pald_gpu_strong_ties(self._ptrs[2], self.ld, self.n, dptr, tptr,
+                                                 thr_out.data_ptr(), 0, None, None, None,
+                                                 cnt.data_ptr(), st))
+        m = int(cnt.item())
+        xs = torch.empty(m, dtype=torch.int32, device=dev)
+        ys = torch.empty(m, dtype=torch.int32, device=dev)
+        sv = torch.empty(m, dtype=torch.float64, device=dev)
+        if m:
+            _raise_for(self.lib.pald_gpu_strong_ties(self._ptrs[2], self.ld, self.n, dptr, tptr,
+                                                     thr_out.data_ptr(), m, xs.data_ptr(),
+                                                     ys.data_ptr(), sv.data_ptr(), cnt.data_ptr(), st))
+        return float(thr_out.item()), xs, ys, sv
+
     @property
     def exact_path(self) -> bool:
         b = _lib.Buffers()

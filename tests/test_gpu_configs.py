@@ -300,3 +300,35 @@ def test_python_api_mirror(oracle):
     assert max_rel_diff(t.cohesion.values, c_ref) < 1e-5  # distinct distances: tri+fill == pairwise
     pg.normalize(r.cohesion)
     assert abs(pg.local_depths(r.cohesion).depths.mean() - 0.5) < 1e-6
+
+
+@pytest.mark.parametrize("alg", ["pairwise", "triplet"])
+def test_epilogue_depths_and_strong_ties(oracle, alg):
+    """normalize + local_depths (reference.hpp:223-241) and strong ties
+    (analyze.hpp:34-53) on the device, against the reference arithmetic in
+    double (the C oracle for depths; a literal restatement for ties)."""
+    n = 300
+    d = int_upper(n, 21) if alg == "triplet" else random_upper(n, 22)
+    e = run(torch.from_numpy(d).cuda(), alg)
+    diag = e.fill_diagonal() if alg == "triplet" else None
+    depths = e.local_depths(diag).cpu().numpy()
+    thr, xs, ys, sv = e.strong_ties(diag)
+    c = e.C.cpu().numpy().astype(np.float64)
+    if diag is not None:
+        np.fill_diagonal(c, diag.cpu().numpy())
+    oracle.normalize(c)
+    ref_depths = oracle.local_depths(c)
+    assert np.array_equal(depths, ref_depths)
+    s = 0.0
+    for x in range(n):
+        s += c[x, x]
+    ref_thr = 0.5 * s / n
+    assert thr == ref_thr
+    edges = [(x, y, min(c[x, y], c[y, x])) for x in range(n) for y in range(x + 1, n)
+             if min(c[x, y], c[y, x]) >= ref_thr]
+    assert len(edges) == xs.numel() and len(edges) > 0
+    got = list(zip(xs.cpu().tolist(), ys.cpu().tolist(), sv.cpu().tolist()))
+    assert got == edges
+    # explicit threshold override
+    thr2, xs2, _, _ = e.strong_ties(diag, threshold=ref_thr * 2)
+    assert thr2 == ref_thr * 2 and xs2.numel() == sum(1 for t in edges if t[2] >= ref_thr * 2)
