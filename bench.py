@@ -307,6 +307,44 @@ def e2e_host(n: int, D_dev, steps: int, warmup: int):
     return n ** 3 / t, t, checksum
 
 
+def e2e_sharded(engine, runner, D_dev, steps: int, warmup: int, rank: int):
+    """N > 1: the public multi-GPU path (ShardedRunner over the staged C ABI)
+    with host buffers: every rank uploads D from pinned host memory, rank 0
+    downloads U and C; wall time, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    n = engine.n
+    d_h = torch.empty((n, n), dtype=torch.float32, pin_memory=True)
+    d_h.copy_(D_dev)
+    u_h = c_h = None
+    if rank == 0:
+        u_h = torch.empty((n, n), dtype=torch.int32, pin_memory=True)
+        c_h = torch.empty((n, n), dtype=torch.float32, pin_memory=True)
+    times = []
+    for i in range(warmup + steps):
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        engine.load_host(d_h)
+        p = runner.plan
+        engine.focus_counts(*p.focus_share)
+        runner.exchange_focus()
+        engine.cohesion(*p.cohesion_rows)
+        runner.gather_cohesion()
+        if rank == 0:
+            u_h.copy_(engine.U)
+            c_h.copy_(engine.C)
+        torch.cuda.synchronize()
+        t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        if i >= warmup:
+            times.append(float(t))
+    tm = statistics.mean(times)
+    del d_h, u_h, c_h
+    return n ** 3 / tm, tm
+
+
 def secondary_configs(steps: int) -> dict:
     """N=1: the other BASELINE.json configs (parity cases) timed device-resident."""
     import torch
@@ -465,8 +503,14 @@ def main() -> None:
             del engine, runner
             torch.cuda.empty_cache()
             line["secondary_configs"] = secondary_configs(3)
-    elif rank == 0:
-        line["e2e"] = {"value": None, "note": "host-buffer C-ABI path is single-GPU; see N=1 line"}
+    elif not args.no_e2e:
+        try:
+            ev, et = e2e_sharded(engine, runner, D, max(1, min(args.steps, 3)), 1, rank)
+            line["e2e"] = {"value": ev, "unit": "triplets/s", "seconds_per_step": et,
+                           "h2d_bytes_per_step": world * n * n * 4, "d2h_bytes_per_step": 2 * n * n * 4,
+                           "path": "ShardedRunner over the staged C ABI, pinned host D per rank, U/C to rank 0"}
+        except Exception as e:
+            line["e2e"] = {"value": None, "error": repr(e)}
 
     if rank == 0:
         print(json.dumps(line), flush=True)
