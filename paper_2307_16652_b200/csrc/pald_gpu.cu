@@ -168,12 +168,12 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-int make_map(CUtensorMap* map, const void* base, uint64_t n, uint64_t ld) {
+int make_map(CUtensorMap* map, const void* base, uint64_t n, uint64_t ld, int box_cols = kTile) {
   auto encode = get_encode();
   if (!encode) return set_error(PALD_GPU_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {n, n};
   cuuint64_t strides[1] = {ld * 4};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(kTile), static_cast<cuuint32_t>(kBK)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(kBK)};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims,
                       strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -183,18 +183,19 @@ int make_map(CUtensorMap* map, const void* base, uint64_t n, uint64_t ld) {
   return PALD_GPU_OK;
 }
 
-template <int PASS, bool A_NU, bool B_NU, bool T_NU, bool ZD, bool FAST, bool SPLIT = false>
+template <int PASS, bool A_NU, bool B_NU, bool T_NU, bool ZD, bool FAST, bool SPLIT = false,
+          int TILE = kTile>
 int launch_tile(const CUtensorMap& md, const CUtensorMap& mnu, const CUtensorMap& mw,
                 const KernelArgs& a, int grid, cudaStream_t s) {
-  auto k = pald_tile_kernel<PASS, A_NU, B_NU, T_NU, ZD, FAST, SPLIT>;
+  auto k = pald_tile_kernel<PASS, A_NU, B_NU, T_NU, ZD, FAST, SPLIT, TILE>;
   static bool attr_done[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (!attr_done[dev & 63]) {
-    PALD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes(PASS)));
+    PALD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes(PASS, TILE)));
     attr_done[dev & 63] = true;
   }
-  k<<<grid, kThreads, smem_bytes(PASS), s>>>(md, mnu, mw, a);
+  k<<<grid, kThreads, smem_bytes(PASS, TILE), s>>>(md, mnu, mw, a);
   PALD_CUDA(cudaGetLastError());
   return PALD_GPU_OK;
 }
@@ -238,7 +239,8 @@ struct pald_gpu_plan {
   float* c = nullptr;
   Stats* stats = nullptr;
   Stats* stats_host = nullptr;
-  CUtensorMap tm_d, tm_dnu, tm_w;
+  CUtensorMap tm_d, tm_dnu, tm_w;        // 128-wide boxes
+  CUtensorMap tm_d64, tm_dnu64, tm_w64;  // 64-wide boxes (small-n cohesion tiles)
   bool loaded = false;
   bool exact = false;
   bool focus_dirty = false;
@@ -304,6 +306,9 @@ int plan_alloc(pald_gpu_plan* p) {
   if ((rc = make_map(&p->tm_d, p->ds, p->n, p->ld))) return rc;
   if ((rc = make_map(&p->tm_dnu, p->dnu, p->n, p->ld))) return rc;
   if ((rc = make_map(&p->tm_w, p->w, p->n, p->ld))) return rc;
+  if ((rc = make_map(&p->tm_d64, p->ds, p->n, p->ld, 64))) return rc;
+  if ((rc = make_map(&p->tm_dnu64, p->dnu, p->n, p->ld, 64))) return rc;
+  if ((rc = make_map(&p->tm_w64, p->w, p->n, p->ld, 64))) return rc;
   // The memsets above run on the legacy default stream; callers may use
   // non-blocking streams, so finish them before the plan is handed out.
   PALD_CUDA(cudaDeviceSynchronize());
@@ -416,35 +421,50 @@ int plan_focus_impl(pald_gpu_plan* p, cudaStream_t s) {
   return plan_focus_finish_impl(p, s);
 }
 
+template <int TILE>
+int launch_cohesion(pald_gpu_plan* p, uint64_t row0, uint64_t row1, cudaStream_t s) {
+  const uint64_t nbt = (p->n + TILE - 1) / TILE;
+  const uint64_t tr0 = row0 / TILE, tr1 = (row1 + TILE - 1) / TILE;
+  const long long tiles = (long long)((tr1 - tr0) * nbt);
+  const long long nch = (long long)((p->n + kBK - 1) / kBK);
+  static const int group_rows = [] {
+    const char* e = getenv("PALD_GPU_GROUP_ROWS");  // tuning knob (default kGroupRows)
+    return e ? std::max(1, atoi(e)) : kGroupRows;
+  }();
+  KernelArgs a{p->ds, p->u, p->w, p->c, (int)p->n, (int)p->ld, (int)nbt, (int)tr0, (int)tr1, tiles, 0,
+               tiles * nch, nullptr, group_rows};
+  const int grid = (int)std::min<long long>(tiles, (long long)p->sms * ctas_per_sm(TILE));
+  const bool tri = p->algorithm == PALD_GPU_TRIPLET;
+  const bool split = p->policy == PALD_GPU_INCLUSIVE_SPLIT;
+  const CUtensorMap& md = TILE == 64 ? p->tm_d64 : p->tm_d;
+  const CUtensorMap& mn = TILE == 64 ? p->tm_dnu64 : p->tm_dnu;
+  const CUtensorMap& mw = TILE == 64 ? p->tm_w64 : p->tm_w;
+  if (!p->exact) {
+    return tri     ? launch_tile<1, true, true, false, true, true, false, TILE>(md, mn, mw, a, grid, s)
+           : split ? launch_tile<1, false, false, false, false, true, true, TILE>(md, mn, mw, a, grid, s)
+                   : launch_tile<1, false, true, false, false, true, false, TILE>(md, mn, mw, a, grid, s);
+  }
+  return tri     ? launch_tile<1, true, true, false, true, false, false, TILE>(md, mn, mw, a, grid, s)
+         : split ? launch_tile<1, false, false, false, false, false, true, TILE>(md, mn, mw, a, grid, s)
+                 : launch_tile<1, false, true, false, false, false, false, TILE>(md, mn, mw, a, grid, s);
+}
+
 int plan_cohesion_impl(pald_gpu_plan* p, uint64_t row0, uint64_t row1, cudaStream_t s) {
   if (!p->loaded) return set_error(PALD_GPU_ERR_VALIDATION, "plan has no distances loaded");
   row1 = std::min(row1, p->n);
   if (row0 >= row1) return PALD_GPU_OK;
   if (row0 % kTile != 0 || (row1 % kTile != 0 && row1 != p->n))
     return set_error(PALD_GPU_ERR_VALIDATION, "cohesion row range must be aligned to %d", kTile);
-  const uint64_t tr0 = row0 / kTile, tr1 = (row1 + kTile - 1) / kTile;
-  const long long tiles = (long long)((tr1 - tr0) * p->nb);
-  const long long nch = (long long)((p->n + kBK - 1) / kBK);
-  static const int group_rows = [] {
-    const char* e = getenv("PALD_GPU_GROUP_ROWS");  // tuning knob (default kGroupRows)
-    return e ? std::max(1, atoi(e)) : kGroupRows;
+  // Less than one wave of 128-wide tiles: use 64-wide tiles (4x the tiles,
+  // 2 CTAs per SM) so small problems fill the 148 SMs. Results are
+  // identical: every C entry is the same in-order sum either way.
+  const uint64_t tiles128 = ((row1 - row0 + kTile - 1) / kTile) * p->nb;
+  static const int force_tile = [] {
+    const char* e = getenv("PALD_GPU_COHESION_TILE");  // testing knob: 64 or 128
+    return e ? atoi(e) : 0;
   }();
-  KernelArgs a{p->ds, p->u, p->w, p->c, (int)p->n, (int)p->ld, (int)p->nb, (int)tr0, (int)tr1, tiles, 0,
-               tiles * nch, nullptr, group_rows};
-  const int grid = (int)std::min<long long>(tiles, p->sms);
-  int rc;
-  const bool tri = p->algorithm == PALD_GPU_TRIPLET;
-  const bool split = p->policy == PALD_GPU_INCLUSIVE_SPLIT;
-  const CUtensorMap &md = p->tm_d, &mn = p->tm_dnu, &mw = p->tm_w;
-  if (!p->exact) {
-    rc = tri     ? launch_tile<1, true, true, false, true, true>(md, mn, mw, a, grid, s)
-         : split ? launch_tile<1, false, false, false, false, true, true>(md, mn, mw, a, grid, s)
-                 : launch_tile<1, false, true, false, false, true>(md, mn, mw, a, grid, s);
-  } else {
-    rc = tri     ? launch_tile<1, true, true, false, true, false>(md, mn, mw, a, grid, s)
-         : split ? launch_tile<1, false, false, false, false, false, true>(md, mn, mw, a, grid, s)
-                 : launch_tile<1, false, true, false, false, false>(md, mn, mw, a, grid, s);
-  }
+  const bool small = force_tile ? force_tile == 64 : tiles128 < (uint64_t)p->sms;
+  const int rc = small ? launch_cohesion<64>(p, row0, row1, s) : launch_cohesion<kTile>(p, row0, row1, s);
   if (rc == PALD_GPU_OK) ++p->launches;
   return rc;
 }

@@ -51,17 +51,23 @@ constexpr int kTile = 128;      // pair-tile edge (rows and columns)
 #endif
 constexpr int kBK = PALD_BK;    // third-point chunk per pipeline stage
 constexpr int kThreads = 256;   // 8 warps, 16 x 16 threads, 8 x 8 outputs each
-// Pipeline depth per pass so that stages x stage_bytes fits the 227 KB of
-// shared memory (focus: 2 boxes per stage, cohesion: 3).
-__host__ __device__ constexpr int stages_for(int pass) {
-  return (pass == 0 ? 2 : 3) * kBK * 128 * 4 * 4 <= 200 * 1024 ? 4
-         : (pass == 0 ? 2 : 3) * kBK * 128 * 4 * 3 <= 200 * 1024 ? 3 : 2;
+__host__ __device__ constexpr int box_bytes(int tile) { return kBK * tile * 4; }
+__host__ __device__ constexpr int stage_bytes(int pass, int tile) { return (pass == 0 ? 2 : 3) * box_bytes(tile); }
+// CTAs per SM: 1 for 128-wide tiles (8 x 8 outputs per thread, ~230
+// registers), 2 for the 64-wide small-n tiles (4 x 4 per thread).
+__host__ __device__ constexpr int ctas_per_sm(int tile) { return tile == 128 ? 1 : 2; }
+// Pipeline depth so that stages x stage_bytes fits the shared memory of
+// ctas_per_sm CTAs (227 KB per SM).
+__host__ __device__ constexpr int stages_for(int pass, int tile) {
+  return stage_bytes(pass, tile) * 4 <= 200 * 1024 / ctas_per_sm(tile) ? 4
+         : stage_bytes(pass, tile) * 3 <= 200 * 1024 / ctas_per_sm(tile) ? 3 : 2;
 }
-constexpr int kBoxBytes = kBK * kTile * 4;  // one TMA box (16 KB)
+constexpr int kBoxBytes = kBK * kTile * 4;  // one TMA box of a 128-wide panel (32 KB)
 constexpr float kCmpScale = 0x1p125f;       // S of the FFMA.SAT compare
 
-__host__ __device__ constexpr int stage_bytes(int pass) { return (pass == 0 ? 2 : 3) * kBoxBytes; }
-__host__ __device__ constexpr int smem_bytes(int pass) { return stages_for(pass) * stage_bytes(pass) + 1024; }
+__host__ __device__ constexpr int smem_bytes(int pass, int tile) {
+  return stages_for(pass, tile) * stage_bytes(pass, tile) + 1024;
+}
 
 struct KernelArgs {
   const uint32_t* d;     // layout of D (scaled fp32 bits or integer keys), n x ld
@@ -120,34 +126,41 @@ __device__ __forceinline__ float nu_f(float v) { return __uint_as_float(__float_
 
 // ---------------------------------------------------------------------------
 // Thread layout: 8 warps as a 4 x 2 grid of 4 x 8-thread warp tiles; thread
-// (ty, tx) in 16 x 16 owns rows {ty*4+i, 64+ty*4+i} and columns
-// {tx*4+j, 64+tx*4+j} (i, j < 4) of the 128 x 128 tile. A-panel LDS.128 of a
-// warp touch 4 distinct 16-byte words (broadcast), B-panel loads 8
-// consecutive words: one wavefront each.
-__device__ __forceinline__ int row_off(int ty, int i) { return i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4); }
+// (ty, tx) in 16 x 16 owns TT = TILE/16 rows {h*TILE/2 + ty*4 + i} and TT
+// columns {h*TILE/2 + tx*4 + j} (h < TT/4, i, j < 4) of the TILE x TILE
+// tile: 8 x 8 outputs for TILE 128, 4 x 4 for TILE 64 (small n). A-panel
+// LDS.128 of a warp touch 4 distinct 16-byte words (broadcast), B-panel
+// loads 8 consecutive words: one wavefront each.
+template <int TILE>
+__device__ __forceinline__ int row_off(int ty, int i) {
+  return (i >> 2) * (TILE / 2) + ty * 4 + (i & 3);
+}
+
+template <int TILE, int N>
+__device__ __forceinline__ void lds_vec(const float* __restrict__ row, int t, float (&v)[N]) {
+#pragma unroll
+  for (int h = 0; h < N / 4; ++h) {
+    const float4 q = reinterpret_cast<const float4*>(row)[h * (TILE / 8) + t];
+    v[4 * h + 0] = q.x;
+    v[4 * h + 1] = q.y;
+    v[4 * h + 2] = q.z;
+    v[4 * h + 3] = q.w;
+  }
+}
 
 // One k step of the uniform (no per-element transform) fast path.
-template <int PASS, bool FAST>
+template <int PASS, bool FAST, int TILE, int TT = TILE / 16>
 __device__ __forceinline__ void k_step(const float* __restrict__ sa, const float* __restrict__ sb,
                                        const float* __restrict__ sw, int kk, int ty, int tx,
-                                       const float2 (&thr)[8][4], float2 (&acc)[8][4]) {
-  const float4 a0 = reinterpret_cast<const float4*>(sa + kk * kTile)[ty];
-  const float4 a1 = reinterpret_cast<const float4*>(sa + kk * kTile)[16 + ty];
-  const float4 b0 = reinterpret_cast<const float4*>(sb + kk * kTile)[tx];
-  const float4 b1 = reinterpret_cast<const float4*>(sb + kk * kTile)[16 + tx];
-  const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-  const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-  float w[8];
-  if (PASS == 1) {
-    const float4 w0 = reinterpret_cast<const float4*>(sw + kk * kTile)[ty];
-    const float4 w1 = reinterpret_cast<const float4*>(sw + kk * kTile)[16 + ty];
-    w[0] = w0.x; w[1] = w0.y; w[2] = w0.z; w[3] = w0.w;
-    w[4] = w1.x; w[5] = w1.y; w[6] = w1.z; w[7] = w1.w;
-  }
+                                       const float2 (&thr)[TT][TT / 2], float2 (&acc)[TT][TT / 2]) {
+  float a[TT], b[TT], w[TT];
+  lds_vec<TILE>(sa + kk * TILE, ty, a);
+  lds_vec<TILE>(sb + kk * TILE, tx, b);
+  if (PASS == 1) lds_vec<TILE>(sw + kk * TILE, ty, w);
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
+  for (int i = 0; i < TT; ++i) {
 #pragma unroll
-    for (int jp = 0; jp < 4; ++jp) {
+    for (int jp = 0; jp < TT / 2; ++jp) {
       if (FAST) {
         const float m0 = fminf(a[i], b[2 * jp]);
         const float m1 = fminf(a[i], b[2 * jp + 1]);
@@ -179,28 +192,25 @@ __device__ __forceinline__ void k_step(const float* __restrict__ sa, const float
 
 // One k step with per-element transforms (chunks that cross the row or
 // column tile, and the ragged last chunk).
-template <int PASS, bool FAST>
+template <int PASS, bool FAST, int TILE, int TT = TILE / 16>
 __device__ __forceinline__ void k_step_sel(const float* __restrict__ sa, const float* __restrict__ sb,
                                            const float* __restrict__ sw, int kk, int kg, int ty,
                                            int tx, int r0, int c0, bool a_in, bool b_in,
-                                           const float2 (&thr)[8][4], float2 (&acc)[8][4]) {
-  float a[8], b[8], w[8];
+                                           const float2 (&thr)[TT][TT / 2], float2 (&acc)[TT][TT / 2]) {
+  float a[TT], b[TT], w[TT];
+  lds_vec<TILE>(sa + kk * TILE, ty, a);
+  lds_vec<TILE>(sb + kk * TILE, tx, b);
+  if (PASS == 1) lds_vec<TILE>(sw + kk * TILE, ty, w);
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    a[i] = sa[kk * kTile + row_off(ty, i)];
-    if (PASS == 1) w[i] = sw[kk * kTile + row_off(ty, i)];
-    b[i] = sb[kk * kTile + row_off(tx, i)];
-  }
+  for (int i = 0; i < TT; ++i) {
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-#pragma unroll
-    for (int jp = 0; jp < 4; ++jp) {
+    for (int jp = 0; jp < TT / 2; ++jp) {
       float kv[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int j = 2 * jp + h;
-        const bool nua = a_in && (kg < c0 + row_off(tx, j));
-        const bool nub = b_in && (kg < r0 + row_off(ty, i));
+        const bool nua = a_in && (kg < c0 + row_off<TILE>(tx, j));
+        const bool nub = b_in && (kg < r0 + row_off<TILE>(ty, i));
         const uint32_t av = nua ? nu_bits(__float_as_uint(a[i])) : __float_as_uint(a[i]);
         const uint32_t bv = nub ? nu_bits(__float_as_uint(b[j])) : __float_as_uint(b[j]);
         const float t = (h == 0) ? thr[i][jp].x : thr[i][jp].y;
@@ -229,22 +239,23 @@ __device__ __forceinline__ void k_step_sel(const float* __restrict__ sa, const f
 // pair, (w/2) * ([T < min(A', B)] + [T < min(A', nu(B))]); the sum of the
 // two indicators (0, 1, 2) times w/2 is one exact product, so each pair still
 // adds a single correctly rounded term, in ascending y.
-template <bool FAST>
+template <bool FAST, int TILE, int TT = TILE / 16>
 __device__ __forceinline__ void k_step_split(const float* __restrict__ sa, const float* __restrict__ sb,
                                              const float* __restrict__ sw, int kk, int ty, int tx,
-                                             const float2 (&thr)[8][4], float2 (&acc)[8][4]) {
-  float a[8], b[8], bn[8], wh[8];
+                                             const float2 (&thr)[TT][TT / 2], float2 (&acc)[TT][TT / 2]) {
+  float a[TT], b[TT], bn[TT], wh[TT];
+  lds_vec<TILE>(sa + kk * TILE, ty, a);
+  lds_vec<TILE>(sb + kk * TILE, tx, b);
+  lds_vec<TILE>(sw + kk * TILE, ty, wh);
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    a[i] = sa[kk * kTile + row_off(ty, i)];
-    wh[i] = 0.5f * sw[kk * kTile + row_off(ty, i)];
-    b[i] = sb[kk * kTile + row_off(tx, i)];
+  for (int i = 0; i < TT; ++i) {
+    wh[i] *= 0.5f;
     bn[i] = nu_f(b[i]);
   }
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
+  for (int i = 0; i < TT; ++i) {
 #pragma unroll
-    for (int jp = 0; jp < 4; ++jp) {
+    for (int jp = 0; jp < TT / 2; ++jp) {
       float k1[2], k2[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -372,8 +383,9 @@ __device__ __forceinline__ WorkSplit make_split(const KernelArgs& a, int C, int 
 // mbarrier pipeline that runs across tile boundaries. A stage is refilled by
 // the last warp to finish with it (shared-memory arrival counter), so no
 // block-wide barrier sits in the main loop.
-template <int PASS, bool A_NU, bool B_NU, bool T_NU, bool ZERO_DIAG, bool FAST, bool SPLIT = false>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int PASS, bool A_NU, bool B_NU, bool T_NU, bool ZERO_DIAG, bool FAST, bool SPLIT = false,
+          int TILE = kTile>
+__global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE))
     pald_tile_kernel(const __grid_constant__ CUtensorMap tm_d,
                      const __grid_constant__ CUtensorMap tm_dnu,
                      const __grid_constant__ CUtensorMap tm_w, const KernelArgs args) {
@@ -381,7 +393,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   // Align the pipeline buffers to 1 KB with an offset into the same array,
   // so the compiler keeps the shared address space (LDS, not generic LD).
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  constexpr int kStages = stages_for(PASS);
+  constexpr int kStages = stages_for(PASS, TILE);
+  constexpr int TT = TILE / 16;  // outputs per thread per dimension
+  constexpr int BOX = box_bytes(TILE);
   __shared__ uint64_t full_bar[kStages];
   __shared__ uint32_t done_cnt[kStages];
 
@@ -424,11 +438,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto run_c0 = [&](int ri) { return ri < ws.full ? 0 : s_rem[ri - ws.full][1]; };
   auto run_c1 = [&](int ri) { return ri < ws.full ? nchunks : s_rem[ri - ws.full][2]; };
 
-  constexpr int SB = stage_bytes(PASS);
+  constexpr int SB = stage_bytes(PASS, TILE);
   auto issue = [&](int t, int ch, int s) {
     int tr, tc;
     tile_coords<PASS>(args, t, tr, tc);
-    const int r0 = tr * kTile, c0 = tc * kTile;
+    const int r0 = tr * TILE, c0 = tc * TILE;
     const int k0 = ch * kBK, k1 = min(k0 + kBK, n);
     // Uniform per-chunk transform choice: the whole chunk lies below the
     // column (A) / row (B) tile => every element takes nu().
@@ -437,8 +451,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* st = smem + s * SB;
     mbar_expect_tx(&full_bar[s], SB);
     tma_load_2d(st, ma, r0, k0, &full_bar[s]);
-    tma_load_2d(st + kBoxBytes, mb, c0, k0, &full_bar[s]);
-    if (PASS == 1) tma_load_2d(st + 2 * kBoxBytes, &tm_w, r0, k0, &full_bar[s]);
+    tma_load_2d(st + BOX, mb, c0, k0, &full_bar[s]);
+    if (PASS == 1) tma_load_2d(st + 2 * BOX, &tm_w, r0, k0, &full_bar[s]);
   };
   // Producer iterator (run index, chunk) of unit p + kStages, kept by every
   // warp's lane 0 so that whichever warp releases a stage can refill it.
@@ -463,17 +477,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int t = run_t(ri), ch_begin = run_c0(ri), ch_end = run_c1(ri);
     int tr, tc;
     tile_coords<PASS>(args, t, tr, tc);
-    const int r0 = tr * kTile, c0 = tc * kTile;
-    float2 thr[8][4];
-    float2 acc[8][4];
+    const int r0 = tr * TILE, c0 = tc * TILE;
+    float2 thr[TT][TT / 2];
+    float2 acc[TT][TT / 2];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < TT; ++i) {
 #pragma unroll
-      for (int jp = 0; jp < 4; ++jp) {
+      for (int jp = 0; jp < TT / 2; ++jp) {
         uint32_t t2[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int r = r0 + row_off(ty, i), c = c0 + row_off(tx, 2 * jp + h);
+          const int r = r0 + row_off<TILE>(ty, i), c = c0 + row_off<TILE>(tx, 2 * jp + h);
           uint32_t tv = (r < n && c < n) ? __ldg(args.d + (size_t)r * ld + c) : 0u;
           if (T_NU) tv = nu_bits(tv);
           t2[h] = tv;
@@ -493,20 +507,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&full_bar[s], (p / kStages) & 1);
       const uint8_t* st = smem + s * SB;
       const float* sa = reinterpret_cast<const float*>(st);
-      const float* sb = reinterpret_cast<const float*>(st + kBoxBytes);
-      const float* sw = reinterpret_cast<const float*>(st + 2 * kBoxBytes);
+      const float* sb = reinterpret_cast<const float*>(st + BOX);
+      const float* sw = reinterpret_cast<const float*>(st + 2 * BOX);
       const int k0 = ch * kBK;
-      const bool a_in = A_NU && (k0 >= c0) && (k0 < c0 + kTile);
-      const bool b_in = B_NU && (k0 >= r0) && (k0 < r0 + kTile);
+      const bool a_in = A_NU && (k0 >= c0) && (k0 < c0 + TILE);
+      const bool b_in = B_NU && (k0 >= r0) && (k0 < r0 + TILE);
       const int kmax = min(kBK, n - k0);
       if (PASS == 1 && SPLIT) {
-        for (int kk = 0; kk < kmax; ++kk) k_step_split<FAST>(sa, sb, sw, kk, ty, tx, thr, acc);
+        for (int kk = 0; kk < kmax; ++kk) k_step_split<FAST, TILE>(sa, sb, sw, kk, ty, tx, thr, acc);
       } else if (!a_in && !b_in && kmax == kBK) {
 #pragma unroll 2
-        for (int kk = 0; kk < kBK; ++kk) k_step<PASS, FAST>(sa, sb, sw, kk, ty, tx, thr, acc);
+        for (int kk = 0; kk < kBK; ++kk) k_step<PASS, FAST, TILE>(sa, sb, sw, kk, ty, tx, thr, acc);
       } else {
         for (int kk = 0; kk < kmax; ++kk)
-          k_step_sel<PASS, FAST>(sa, sb, sw, kk, k0 + kk, ty, tx, r0, c0, a_in, b_in, thr, acc);
+          k_step_sel<PASS, FAST, TILE>(sa, sb, sw, kk, k0 + kk, ty, tx, r0, c0, a_in, b_in, thr, acc);
       }
       // Release the stage: the last warp to arrive refills it.
       __syncwarp();
@@ -521,37 +535,41 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---- flush ------------------------------------------------------------
     if (PASS == 0) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int r = r0 + row_off(ty, i);
+      for (int i = 0; i < TT; ++i) {
+        const int r = r0 + row_off<TILE>(ty, i);
         if (r >= n) continue;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int c = c0 + row_off(tx, j);
+        for (int j = 0; j < TT; ++j) {
+          const int c = c0 + row_off<TILE>(tx, j);
           const float v = (j & 1) ? acc[i][j >> 1].y : acc[i][j >> 1].x;
           if (c < n) atomicAdd(args.w + (size_t)r * ld + c, v);  // RED.ADD.F32, exact
         }
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int r = r0 + row_off(ty, i);
+      for (int i = 0; i < TT; ++i) {
+        const int r = r0 + row_off<TILE>(ty, i);
         if (r >= n) continue;
-        float v[8];
+        float v[TT];
 #pragma unroll
-        for (int jp = 0; jp < 4; ++jp) {
+        for (int jp = 0; jp < TT / 2; ++jp) {
           v[2 * jp] = acc[i][jp].x;
           v[2 * jp + 1] = acc[i][jp].y;
         }
         if (ZERO_DIAG) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            if (c0 + row_off(tx, j) == r) v[j] = 0.f;
+          for (int j = 0; j < TT; ++j)
+            if (c0 + row_off<TILE>(tx, j) == r) v[j] = 0.f;
         }
         float* crow = args.c + (size_t)r * ld;
         // Columns past n land in the row padding (ld >= round_up(n, 32)).
-        const int ca = c0 + tx * 4, cb = c0 + 64 + tx * 4;
-        if (ca < n) *reinterpret_cast<float4*>(crow + ca) = make_float4(v[0], v[1], v[2], v[3]);
-        if (cb < n) *reinterpret_cast<float4*>(crow + cb) = make_float4(v[4], v[5], v[6], v[7]);
+#pragma unroll
+        for (int h = 0; h < TT / 4; ++h) {
+          const int cc = c0 + h * (TILE / 2) + tx * 4;
+          if (cc < n)
+            *reinterpret_cast<float4*>(crow + cc) =
+                make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
+        }
       }
     }
   }
