@@ -78,7 +78,7 @@ typedef struct pald_gpu_opts {
   int32_t device;         /* CUDA device ordinal; -1 = current device */
   /* Block-size hints of the reference drivers (b, b_focus, b_cohesion).
    * Validated >= 1 exactly like blocked.hpp:372 / :431; the GPU tile shape
-   * is fixed (128 x 128 x 32), so they do not change results -- neither do
+   * is fixed (128 x 128 x 64), so they do not change results -- neither do
    * they in the reference (C bits of blocked_pairwise<float> are
    * independent of b). */
   uint64_t block;
@@ -124,7 +124,7 @@ int pald_gpu_cohesion_f32_device(const float* dD, uint64_t ldd, uint64_t n,
 /* ---- Staged plan: the building blocks of the multi-GPU drivers --------
  * A plan owns the device workspace for one n on one device.
  * Pass 1 (focus) is split into work units (a 128 x 128 upper-triangular
- * pair tile x a 32-point chunk of third points). focus_counts(part, parts)
+ * pair tile x a 64-point chunk of third points). focus_counts(part, parts)
  * accumulates the integer focus counts of share `part` of `parts` equal
  * shares of the units into the W buffer; focus_finish turns the counts
  * into U and W = 1/U (both triangles). A multi-GPU driver gives each rank

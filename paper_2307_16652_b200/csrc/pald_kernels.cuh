@@ -379,7 +379,7 @@ __device__ __forceinline__ WorkSplit make_split(const KernelArgs& a, int C, int 
 //            count buffers before the finish;
 //   cohesion (PASS 1): whole tiles only, so every C entry is one in-order
 //            fp32 sum (bit-identical to the reference).
-// TMA streams 32-row chunks of the A/B(/W) panels through a 4-stage
+// TMA streams 64-row chunks of the A/B(/W) panels through a 2-4 stage
 // mbarrier pipeline that runs across tile boundaries. A stage is refilled by
 // the last warp to finish with it (shared-memory arrival counter), so no
 // block-wide barrier sits in the main loop.

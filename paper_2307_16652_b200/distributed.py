@@ -3,7 +3,7 @@
 Work decomposition:
   * D is replicated (every rank lays out the same fp32 matrix).
   * Pass 1 (focus): the work units (upper-triangular 128x128 pair tile x
-    32-point chunk of third points) are split into equal contiguous shares,
+    64-point chunk of third points) are split into equal contiguous shares,
     one per rank (exact balance; the reference's analogue is the z-split of
     parallel.hpp:185-204 with private partial counts summed). Each rank
     accumulates integer focus counts; one SUM all-reduce of the count
