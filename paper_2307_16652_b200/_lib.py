@@ -87,7 +87,10 @@ def load(path: Path | None = None) -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    import os
+
+    env = os.environ.get("PALD_GPU_LIB")  # A/B experiments: load another build
+    p = Path(path) if path else (Path(env) if env else LIB_PATH)
     if not p.exists():
         try:
             from ._build import build
@@ -122,7 +125,9 @@ def load(path: Path | None = None) -> C.CDLL:
         "pald_gpu_strong_ties": (i32, [vp, u64, u64, vp, vp, vp, u64, vp, vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
-        f = getattr(lib, name)
+        f = getattr(lib, name, None)
+        if f is None:  # only possible for an older build loaded via PALD_GPU_LIB
+            continue
         f.restype = res
         f.argtypes = args
     _lib = lib

@@ -49,6 +49,11 @@ constexpr int kTile = 128;      // pair-tile edge (rows and columns)
 #ifndef PALD_BK
 #define PALD_BK 64
 #endif
+#ifndef PALD_KUNROLL  // unroll of the fast k loop (scheduling knob)
+#define PALD_KUNROLL 2
+#endif
+constexpr int kKUnroll = PALD_KUNROLL;
+
 constexpr int kBK = PALD_BK;    // third-point chunk per pipeline stage
 constexpr int kThreads = 256;   // 8 warps, 16 x 16 threads, 8 x 8 outputs each
 __host__ __device__ constexpr int box_bytes(int tile) { return kBK * tile * 4; }
@@ -133,6 +138,7 @@ __device__ __forceinline__ float nu_f(float v) { return __uint_as_float(__float_
 // loads 8 consecutive words: one wavefront each.
 template <int TILE>
 __device__ __forceinline__ int row_off(int ty, int i) {
+  if constexpr (TILE == 128) return i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4);
   return (i >> 2) * (TILE / 2) + ty * 4 + (i & 3);
 }
 
@@ -154,9 +160,26 @@ __device__ __forceinline__ void k_step(const float* __restrict__ sa, const float
                                        const float* __restrict__ sw, int kk, int ty, int tx,
                                        const float2 (&thr)[TT][TT / 2], float2 (&acc)[TT][TT / 2]) {
   float a[TT], b[TT], w[TT];
-  lds_vec<TILE>(sa + kk * TILE, ty, a);
-  lds_vec<TILE>(sb + kk * TILE, tx, b);
-  if (PASS == 1) lds_vec<TILE>(sw + kk * TILE, ty, w);
+  if constexpr (TILE == 128) {
+    const float4 a0 = reinterpret_cast<const float4*>(sa + kk * TILE)[ty];
+    const float4 a1 = reinterpret_cast<const float4*>(sa + kk * TILE)[16 + ty];
+    const float4 b0 = reinterpret_cast<const float4*>(sb + kk * TILE)[tx];
+    const float4 b1 = reinterpret_cast<const float4*>(sb + kk * TILE)[16 + tx];
+    a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w;
+    a[4] = a1.x; a[5] = a1.y; a[6] = a1.z; a[7] = a1.w;
+    b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w;
+    b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
+    if (PASS == 1) {
+      const float4 w0 = reinterpret_cast<const float4*>(sw + kk * TILE)[ty];
+      const float4 w1 = reinterpret_cast<const float4*>(sw + kk * TILE)[16 + ty];
+      w[0] = w0.x; w[1] = w0.y; w[2] = w0.z; w[3] = w0.w;
+      w[4] = w1.x; w[5] = w1.y; w[6] = w1.z; w[7] = w1.w;
+    }
+  } else {
+    lds_vec<TILE>(sa + kk * TILE, ty, a);
+    lds_vec<TILE>(sb + kk * TILE, tx, b);
+    if (PASS == 1) lds_vec<TILE>(sw + kk * TILE, ty, w);
+  }
 #pragma unroll
   for (int i = 0; i < TT; ++i) {
 #pragma unroll
@@ -198,9 +221,18 @@ __device__ __forceinline__ void k_step_sel(const float* __restrict__ sa, const f
                                            int tx, int r0, int c0, bool a_in, bool b_in,
                                            const float2 (&thr)[TT][TT / 2], float2 (&acc)[TT][TT / 2]) {
   float a[TT], b[TT], w[TT];
-  lds_vec<TILE>(sa + kk * TILE, ty, a);
-  lds_vec<TILE>(sb + kk * TILE, tx, b);
-  if (PASS == 1) lds_vec<TILE>(sw + kk * TILE, ty, w);
+  if constexpr (TILE == 128) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      a[i] = sa[kk * TILE + row_off<TILE>(ty, i)];
+      if (PASS == 1) w[i] = sw[kk * TILE + row_off<TILE>(ty, i)];
+      b[i] = sb[kk * TILE + row_off<TILE>(tx, i)];
+    }
+  } else {
+    lds_vec<TILE>(sa + kk * TILE, ty, a);
+    lds_vec<TILE>(sb + kk * TILE, tx, b);
+    if (PASS == 1) lds_vec<TILE>(sw + kk * TILE, ty, w);
+  }
 #pragma unroll
   for (int i = 0; i < TT; ++i) {
 #pragma unroll
@@ -516,7 +548,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE))
       if (PASS == 1 && SPLIT) {
         for (int kk = 0; kk < kmax; ++kk) k_step_split<FAST, TILE>(sa, sb, sw, kk, ty, tx, thr, acc);
       } else if (!a_in && !b_in && kmax == kBK) {
-#pragma unroll 2
+#pragma unroll kKUnroll
         for (int kk = 0; kk < kBK; ++kk) k_step<PASS, FAST, TILE>(sa, sb, sw, kk, ty, tx, thr, acc);
       } else {
         for (int kk = 0; kk < kmax; ++kk)
@@ -563,12 +595,18 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE))
         }
         float* crow = args.c + (size_t)r * ld;
         // Columns past n land in the row padding (ld >= round_up(n, 32)).
+        if constexpr (TILE == 128) {
+          const int ca = c0 + tx * 4, cb = c0 + 64 + tx * 4;
+          if (ca < n) *reinterpret_cast<float4*>(crow + ca) = make_float4(v[0], v[1], v[2], v[3]);
+          if (cb < n) *reinterpret_cast<float4*>(crow + cb) = make_float4(v[4], v[5], v[6], v[7]);
+        } else {
 #pragma unroll
-        for (int h = 0; h < TT / 4; ++h) {
-          const int cc = c0 + h * (TILE / 2) + tx * 4;
-          if (cc < n)
-            *reinterpret_cast<float4*>(crow + cc) =
-                make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
+          for (int h = 0; h < TT / 4; ++h) {
+            const int cc = c0 + h * (TILE / 2) + tx * 4;
+            if (cc < n)
+              *reinterpret_cast<float4*>(crow + cc) =
+                  make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
+          }
         }
       }
     }
