@@ -188,6 +188,36 @@ class Engine:
                                                      ys.data_ptr(), sv.data_ptr(), cnt.data_ptr(), st))
         return float(thr_out.item()), xs, ys, sv
 
+    def normalized_cohesion(self, diag: torch.Tensor | None = None) -> torch.Tensor:
+        """normalize (reference.hpp:223-228) on the device: double(C) * (1/(n-1)),
+        the reference's double arithmetic, with an optional fill_diagonal."""
+        c = self.C.double()
+        if diag is not None:
+            c.diagonal().copy_(diag)
+        return c * (1.0 / float(self.n - 1))
+
+    def nearest_neighbors(self, focus: int, k: int, diag: torch.Tensor | None = None):
+        """analyze.hpp:62-75: top-k points by min(c'_fz, c'_zf), strongest
+        first, ties toward the smaller index (stable sort). Returns (z, strength)."""
+        from .api import ValidationError
+
+        if focus < 0 or focus >= self.n:
+            raise ValidationError("focus point out of range")
+        if k >= self.n:
+            raise ValidationError("k must be smaller than the point count")
+        scale = 1.0 / float(self.n - 1)
+        row = self.C[focus].double()
+        col = self.C[:, focus].double()
+        if diag is not None:
+            row[focus] = diag[focus]
+            col[focus] = diag[focus]
+        s = torch.minimum(row * scale, col * scale)
+        idx = torch.arange(self.n, device=s.device)
+        keep = idx != focus
+        s, idx = s[keep], idx[keep]
+        order = torch.sort(s, descending=True, stable=True).indices[:k]
+        return idx[order], s[order]
+
     @property
     def exact_path(self) -> bool:
         b = _lib.Buffers()

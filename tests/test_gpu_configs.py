@@ -332,3 +332,20 @@ def test_epilogue_depths_and_strong_ties(oracle, alg):
     # explicit threshold override
     thr2, xs2, _, _ = e.strong_ties(diag, threshold=ref_thr * 2)
     assert thr2 == ref_thr * 2 and xs2.numel() == sum(1 for t in edges if t[2] >= ref_thr * 2)
+
+
+def test_nearest_neighbors_and_normalized(oracle):
+    """analyze.hpp:62-75 (stable top-k) and normalize on the device."""
+    n = 150
+    d = int_upper(n, 31)  # ties in C -> the stable tie-break matters
+    e = run(torch.from_numpy(d).cuda(), "pairwise")
+    cn = e.normalized_cohesion().cpu().numpy()
+    c = e.C.cpu().numpy().astype(np.float64)
+    oracle.normalize(c)
+    assert np.array_equal(cn, c)
+    for focus, k in ((0, 5), (77, 20), (149, 149 - 1)):
+        z, s = e.nearest_neighbors(focus, k)
+        allz = [(zz, min(c[focus, zz], c[zz, focus])) for zz in range(n) if zz != focus]
+        ref = sorted(allz, key=lambda t: -t[1])[:k]  # Python sort is stable
+        assert z.cpu().tolist() == [t[0] for t in ref]
+        assert s.cpu().tolist() == [t[1] for t in ref]

@@ -94,3 +94,51 @@ def test_pairwise_inclusive_split_bit_exact(oracle, n, kind, exact):
     torch.cuda.synchronize()
     assert np.array_equal(e.U.cpu().numpy(), u_ref)
     assert np.array_equal(e.C.cpu().numpy().view(np.uint32), c_ref.view(np.uint32))
+
+
+def _random_case(seed):
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(2, 420))
+    kind = rng.choice(["uniform", "int3", "int16", "points2d", "wide"])
+    if kind == "uniform":
+        d = random_upper(n, seed)
+    elif kind == "int3":
+        d = int_upper(n, seed, 1, 3)
+    elif kind == "int16":
+        d = int_upper(n, seed)
+    elif kind == "points2d":
+        p = rng.integers(0, 40, size=(n, 2)).astype(np.float64)  # many exact distance ties
+        p += rng.random((n, 2)) * 1e-9 * (rng.random() < 0.5)
+        diff = p[:, None, :] - p[None, :, :]
+        d = np.sqrt((diff ** 2).sum(-1)).astype(np.float32)
+        iu = np.triu_indices(n, 1)
+        zero = d[iu] == 0
+        d[iu[0][zero], iu[1][zero]] = d[iu[1][zero], iu[0][zero]] = 1000.0  # keep D valid
+    else:
+        d = random_upper(n, seed, 1e-3, 1e3)
+    return n, str(kind), d
+
+
+@pytest.mark.parametrize("seed", list(range(24)))
+def test_randomized_sweep(oracle, seed):
+    """Random sizes (ragged tiles and chunks) and tie structures through every
+    kernel variant: pairwise strict/split and triplet, fast and exact paths."""
+    from paper_2307_16652_b200.engine import Engine
+    import torch
+
+    n, kind, d = _random_case(seed)
+    D = torch.from_numpy(np.ascontiguousarray(d)).cuda()
+    exact = bool(seed % 2)
+    for policy in ("strict", "split"):
+        e = Engine(n, "pairwise", force_exact=exact, policy=policy)
+        e.run(D)
+        torch.cuda.synchronize()
+        u_ref, c_ref = oracle.pairwise_f32(d, policy=0 if policy == "strict" else 1)
+        assert np.array_equal(e.U.cpu().numpy(), u_ref), (n, kind, policy)
+        assert np.array_equal(e.C.cpu().numpy().view(np.uint32), c_ref.view(np.uint32)), (n, kind, policy)
+    e = Engine(n, "triplet", force_exact=exact)
+    e.run(D)
+    torch.cuda.synchronize()
+    u_ref, c_ref = oracle.triplet_f64(d)
+    assert np.array_equal(e.U.cpu().numpy(), u_ref), (n, kind, "triplet")
+    assert max_rel_diff(e.C.cpu().numpy(), c_ref) <= TOL, (n, kind, "triplet")
