@@ -638,18 +638,26 @@ int pald_gpu_cohesion_f32(const float* D, uint64_t n, const pald_gpu_opts* o, in
   const auto t_start = std::chrono::steady_clock::now();
   pald_gpu_plan* p = nullptr;
   if ((rc = get_cached_plan(dev, n, o, &p))) return rc;
-  cudaStream_t s = nullptr;
+  cudaStream_t s = nullptr, sc = nullptr;  // compute stream, copy-out stream
   PALD_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  PALD_CUDA(cudaStreamCreateWithFlags(&sc, cudaStreamNonBlocking));
   struct StreamGuard {
-    cudaStream_t s;
-    ~StreamGuard() { cudaStreamDestroy(s); }
-  } sg{s};
-  cudaEvent_t ev[4];
+    cudaStream_t a, b;
+    ~StreamGuard() {
+      cudaStreamDestroy(a);
+      cudaStreamDestroy(b);
+    }
+  } sg{s, sc};
+  // Pass 2 runs in row bands; each band's C rows are copied to the host on
+  // the copy stream while the next band computes, and U is copied during
+  // pass 2 (it is final after pass 1). Only the last band's copy is exposed.
+  constexpr int kBands = 8;
+  cudaEvent_t ev[4 + kBands];
   for (auto& e : ev) PALD_CUDA(cudaEventCreate(&e));
   struct EvGuard {
     cudaEvent_t* e;
     ~EvGuard() {
-      for (int i = 0; i < 4; ++i) cudaEventDestroy(e[i]);
+      for (int i = 0; i < 4 + kBands; ++i) cudaEventDestroy(e[i]);
     }
   } eg{ev};
   PALD_CUDA(cudaEventRecord(ev[0], s));
@@ -657,11 +665,23 @@ int pald_gpu_cohesion_f32(const float* D, uint64_t n, const pald_gpu_opts* o, in
   PALD_CUDA(cudaEventRecord(ev[1], s));
   if ((rc = plan_focus_impl(p, s))) return rc;
   PALD_CUDA(cudaEventRecord(ev[2], s));
-  if ((rc = plan_cohesion_impl(p, 0, n, s))) return rc;
+  if (U_out) {
+    PALD_CUDA(cudaStreamWaitEvent(sc, ev[2], 0));
+    PALD_CUDA(cudaMemcpy2DAsync(U_out, n * 4, p->u, p->ld * 4, n * 4, n, cudaMemcpyDeviceToHost, sc));
+  }
+  const uint64_t rows_per_band = std::max<uint64_t>(kTile, (n / kBands + kTile - 1) / kTile * kTile);
+  int nb_used = 0;
+  for (uint64_t r0 = 0; r0 < n; r0 += rows_per_band, ++nb_used) {
+    const uint64_t r1 = std::min(n, r0 + rows_per_band);
+    if ((rc = plan_cohesion_impl(p, r0, r1, s))) return rc;
+    PALD_CUDA(cudaEventRecord(ev[4 + nb_used], s));
+    PALD_CUDA(cudaStreamWaitEvent(sc, ev[4 + nb_used], 0));
+    PALD_CUDA(cudaMemcpy2DAsync(C_out + r0 * n, n * 4, p->c + r0 * p->ld, p->ld * 4, n * 4, r1 - r0,
+                                cudaMemcpyDeviceToHost, sc));
+  }
   PALD_CUDA(cudaEventRecord(ev[3], s));
-  if (U_out) PALD_CUDA(cudaMemcpy2DAsync(U_out, n * 4, p->u, p->ld * 4, n * 4, n, cudaMemcpyDeviceToHost, s));
-  PALD_CUDA(cudaMemcpy2DAsync(C_out, n * 4, p->c, p->ld * 4, n * 4, n, cudaMemcpyDeviceToHost, s));
   PALD_CUDA(cudaStreamSynchronize(s));
+  PALD_CUDA(cudaStreamSynchronize(sc));
   if (times) {
     float f = 0, c = 0;
     PALD_CUDA(cudaEventElapsedTime(&f, ev[1], ev[2]));
