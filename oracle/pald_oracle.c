@@ -175,21 +175,25 @@ static void pairwise_row_f32(const float* d, uint64_t n, uint64_t x, int32_t* ur
     const float* ry = d + y * n;
     const float w = wrow[y];
     if (policy == ORACLE_STRICT) {
+      /* The masked arithmetic of blocked.hpp:145-148, literally: adding
+       * r*s*w with r, s in {0, 1} is exact for finite w, and reproduces the
+       * reference's 0*inf = NaN when a pair has u = 0 (an off-diagonal
+       * distance that underflows to 0 in fp32). */
       if (y > x) {
         const float dxy = rx[y];  /* pair (x, y): cx update */
         for (uint64_t z = 0; z < n; ++z) {
           const float dxz = rx[z], dyz = ry[z];
-          const int r = ((dxz < dyz ? dxz : dyz) < dxy);
-          const int s = (dxz < dyz);
-          if (r && s) crow[z] += w;
+          const float r = (dxz < dyz ? dxz : dyz) < dxy ? 1.0f : 0.0f;
+          const float s = dxz < dyz ? 1.0f : 0.0f;
+          crow[z] += r * s * w;
         }
       } else {
         const float dyx = ry[x];  /* pair (y, x): cy update, x is the second point */
         for (uint64_t z = 0; z < n; ++z) {
           const float dyz = ry[z], dxz = rx[z];
-          const int r = ((dyz < dxz ? dyz : dxz) < dyx);
-          const int s = (dyz < dxz);
-          if (r && !s) crow[z] += w;
+          const float r = (dyz < dxz ? dyz : dxz) < dyx ? 1.0f : 0.0f;
+          const float s = dyz < dxz ? 1.0f : 0.0f;
+          crow[z] += r * (1.0f - s) * w;
         }
       }
     } else {
@@ -207,7 +211,7 @@ static void pairwise_row_f32(const float* d, uint64_t n, uint64_t x, int32_t* ur
           const float sy = (dyz < dxz ? 1.0f : 0.0f) + 0.5f * (dyz == dxz ? 1.0f : 0.0f);
           share = 1.0f - sy;
         }
-        if (r != 0.0f && share != 0.0f) crow[z] += r * share * w;
+        crow[z] += r * share * w;
       }
     }
   }

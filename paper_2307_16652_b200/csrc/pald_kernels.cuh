@@ -205,8 +205,10 @@ __device__ __forceinline__ void k_step(const float* __restrict__ sa, const float
           acc[i][jp].x += (m0 < t0) ? 1.f : 0.f;
           acc[i][jp].y += (m1 < t1) ? 1.f : 0.f;
         } else {
-          acc[i][jp].x = __fadd_rn(acc[i][jp].x, (t0 < m0) ? w[i] : 0.f);
-          acc[i][jp].y = __fadd_rn(acc[i][jp].y, (t1 < m1) ? w[i] : 0.f);
+          // fma(k, w, acc) as on the fast path: exact for finite w, and
+          // 0 * inf = NaN like the reference's masked update when u = 0
+          const float2 k2 = make_float2((t0 < m0) ? 1.f : 0.f, (t1 < m1) ? 1.f : 0.f);
+          acc[i][jp] = __ffma2_rn(k2, make_float2(w[i], w[i]), acc[i][jp]);
         }
       }
     }

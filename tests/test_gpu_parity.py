@@ -142,3 +142,41 @@ def test_randomized_sweep(oracle, seed):
     u_ref, c_ref = oracle.triplet_f64(d)
     assert np.array_equal(e.U.cpu().numpy(), u_ref), (n, kind, "triplet")
     assert max_rel_diff(e.C.cpu().numpy(), c_ref) <= TOL, (n, kind, "triplet")
+
+
+@pytest.mark.parametrize("extreme", ["underflow", "overflow", "both"])
+def test_valid_double_inputs_that_degenerate_in_fp32(oracle, extreme):
+    """A DistanceMatrix is validated in double (types.hpp:45-65); its fp32
+    conversion (to_real<float>, blocked.hpp:91-96) may contain exact 0 or inf
+    off the diagonal. The reference float path compares them as is; so must
+    we (integer-key path), through the reference-shaped API."""
+    import paper_2307_16652_b200 as pg
+
+    n = 97
+    rng = np.random.default_rng(5)
+    d = np.zeros((n, n))
+    iu = np.triu_indices(n, 1)
+    v = rng.uniform(0.5, 2.0, iu[0].size)
+    pick = rng.random(iu[0].size)
+    if extreme in ("underflow", "both"):
+        v[pick < 0.1] = 1e-50 * (1 + pick[pick < 0.1])  # -> +0.0f
+    if extreme in ("overflow", "both"):
+        v[pick > 0.9] = 1e300 * (1 + pick[pick > 0.9])  # -> +inf
+    d[iu] = v
+    d[(iu[1], iu[0])] = v
+    dm = pg.DistanceMatrix(n, d)
+    d32 = d.astype(np.float32)
+    r = pg.blocked_pairwise(dm, 8)
+    u_ref, c_ref = oracle.pairwise_f32(d32)
+    assert np.array_equal(r.focus.sizes, u_ref)
+    # u = 0 pairs (fp32 distance 0) make the reference's masked update add
+    # 0*inf = NaN (blocked.hpp:147-148); the NaN rows must coincide
+    assert np.array_equal(r.cohesion.values, c_ref.astype(np.float64), equal_nan=True)
+    rs = pg.blocked_pairwise(dm, 8, pg.Policy.InclusiveSplit)
+    us_ref, cs_ref = oracle.pairwise_f32(d32, policy=1)
+    assert np.array_equal(rs.focus.sizes, us_ref)
+    assert np.array_equal(rs.cohesion.values, cs_ref.astype(np.float64))
+    t = pg.blocked_triplet(dm, 4, 4)
+    ut_ref, ct_ref = oracle.triplet_f64(d32)
+    assert np.array_equal(t.focus.sizes, ut_ref)
+    assert max_rel_diff(t.cohesion.values, ct_ref) <= TOL

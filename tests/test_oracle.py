@@ -156,3 +156,22 @@ def test_triplet_rows_oracle_matches_full(oracle):
         ur, cr = oracle.triplet_rows_f64(d, rows)
         assert np.array_equal(ur, u[rows])
         assert np.max(np.abs(cr - c[rows])) < 1e-12
+
+
+def test_oracle_matches_reference_on_fp32_degenerate_input(oracle, reference):
+    """Distances valid in double that underflow to 0 in fp32 give u = 0 and
+    w = inf; the reference's masked fp32 update then adds 0*inf = NaN. The
+    restatement reproduces that exactly (same NaN rows, same finite values)."""
+    n = 40
+    rng = np.random.default_rng(5)
+    d = np.zeros((n, n))
+    iu = np.triu_indices(n, 1)
+    v = rng.uniform(0.5, 2.0, iu[0].size)
+    v[rng.random(iu[0].size) < 0.02] = 1e-50
+    d[iu] = v
+    d[(iu[1], iu[0])] = v
+    ur, cr, _ = reference.blocked_pairwise(d, 8, use_float=True)
+    uo, co = oracle.pairwise_f32(d.astype(np.float32))
+    assert np.array_equal(uo, ur)
+    assert np.array_equal(co.astype(np.float64), cr, equal_nan=True)
+    assert np.isnan(cr).any()
