@@ -1,0 +1,46 @@
+"""Helper for tests/test_gpu_sharded.py: the multi-rank driver
+(ShardedRunner) with the REAL GPU engine, 2-3 processes sharing one GPU,
+collectives over gloo (host-mediated, so no kernel waits on another rank).
+Each rank checks its U and C against a single-process run."""
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = Path(__file__).resolve().parents[2]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+from helpers import int_upper  # noqa: E402
+from paper_2307_16652_b200.distributed import ShardedRunner  # noqa: E402
+from paper_2307_16652_b200.engine import Engine  # noqa: E402
+
+
+def main():
+    n, alg = int(sys.argv[1]), sys.argv[2]
+    dist.init_process_group("gloo")
+    rank, world = dist.get_rank(), dist.get_world_size()
+    torch.cuda.set_device(0)
+    D = torch.from_numpy(int_upper(n, 17)).cuda()
+    ref = Engine(n, alg)
+    ref.run(D)
+    eng = Engine(n, alg)
+    runner = ShardedRunner(eng)
+    for _ in range(2):  # repeated steps reuse the plan
+        runner.step(D)
+    torch.cuda.synchronize()
+    ok_u = torch.equal(eng.U, ref.U)
+    ok_c = torch.equal(eng.C.view(torch.int32), ref.C.view(torch.int32))
+    flags = torch.tensor([int(ok_u), int(ok_c)], dtype=torch.int32)
+    dist.all_reduce(flags, op=dist.ReduceOp.MIN)
+    if rank == 0:
+        print("shares", runner.plan.focus_share, "rows", runner.plan.cohesion_rows, "ok", flags.tolist())
+    dist.destroy_process_group()
+    sys.exit(0 if flags.tolist() == [1, 1] else 1)
+
+
+if __name__ == "__main__":
+    main()

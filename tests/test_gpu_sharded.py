@@ -1,0 +1,28 @@
+"""The multi-rank path with the real GPU engine (torchrun, gloo, ranks
+sharing cuda:0): results bit-identical to one process."""
+import socket
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+SCRIPT = Path(__file__).resolve().parent / "scripts" / "sharded_gpu.py"
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("world,n,alg", [(2, 700, "pairwise"), (3, 513, "triplet"), (2, 300, "triplet")])
+def test_sharded_real_engine(world, n, alg):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}", str(SCRIPT), str(n), alg]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    assert "ok [1, 1]" in out.stdout
