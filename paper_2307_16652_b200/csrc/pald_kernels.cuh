@@ -53,6 +53,9 @@ constexpr int kTile = 128;      // pair-tile edge (rows and columns)
 #define PALD_KUNROLL 2
 #endif
 constexpr int kKUnroll = PALD_KUNROLL;
+#ifndef PALD_COH_ACC  // cohesion accumulate: 0 = packed FFMA2 (default), 1 = scalar FFMA
+#define PALD_COH_ACC 0
+#endif
 
 constexpr int kBK = PALD_BK;    // third-point chunk per pipeline stage
 constexpr int kThreads = 256;   // 8 warps, 16 x 16 threads, 8 x 8 outputs each
@@ -194,7 +197,12 @@ __device__ __forceinline__ void k_step(const float* __restrict__ sa, const float
         } else {
           const float k0f = __saturatef(__fmaf_rn(m0, kCmpScale, thr[i][jp].x));
           const float k1f = __saturatef(__fmaf_rn(m1, kCmpScale, thr[i][jp].y));
+#if PALD_COH_ACC == 1
+          acc[i][jp].x = __fmaf_rn(k0f, w[i], acc[i][jp].x);
+          acc[i][jp].y = __fmaf_rn(k1f, w[i], acc[i][jp].y);
+#else
           acc[i][jp] = __ffma2_rn(make_float2(k0f, k1f), make_float2(w[i], w[i]), acc[i][jp]);
+#endif
         }
       } else {
         const uint32_t ai = __float_as_uint(a[i]);
