@@ -66,9 +66,12 @@ __host__ __device__ constexpr int stage_bytes(int pass, int tile) { return (pass
 __host__ __device__ constexpr int ctas_per_sm(int tile) { return tile == 128 ? 1 : 2; }
 // Pipeline depth so that stages x stage_bytes fits the shared memory of
 // ctas_per_sm CTAs (227 KB per SM).
+#ifndef PALD_SMEM_BUDGET_KB
+#define PALD_SMEM_BUDGET_KB 200
+#endif
 __host__ __device__ constexpr int stages_for(int pass, int tile) {
-  return stage_bytes(pass, tile) * 4 <= 200 * 1024 / ctas_per_sm(tile) ? 4
-         : stage_bytes(pass, tile) * 3 <= 200 * 1024 / ctas_per_sm(tile) ? 3 : 2;
+  return stage_bytes(pass, tile) * 4 <= PALD_SMEM_BUDGET_KB * 1024 / ctas_per_sm(tile) ? 4
+         : stage_bytes(pass, tile) * 3 <= PALD_SMEM_BUDGET_KB * 1024 / ctas_per_sm(tile) ? 3 : 2;
 }
 constexpr int kBoxBytes = kBK * kTile * 4;  // one TMA box of a 128-wide panel (32 KB)
 constexpr float kCmpScale = 0x1p125f;       // S of the FFMA.SAT compare

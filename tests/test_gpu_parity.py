@@ -180,3 +180,53 @@ def test_valid_double_inputs_that_degenerate_in_fp32(oracle, extreme):
     ut_ref, ct_ref = oracle.triplet_f64(d32)
     assert np.array_equal(t.focus.sizes, ut_ref)
     assert max_rel_diff(t.cohesion.values, ct_ref) <= TOL
+
+
+def test_device_api_with_leading_dimensions(oracle):
+    """pald_gpu_cohesion_f32_device: strided device buffers (ld > n),
+    asynchronous on a user stream, U optional."""
+    import ctypes as C
+
+    import torch
+    from paper_2307_16652_b200 import _lib
+    from paper_2307_16652_b200.api import _raise_for
+
+    lib = _lib.load()
+    n = 211
+    d = int_upper(n, 12)
+    Dbig = torch.zeros((n, n + 13), dtype=torch.float32, device="cuda")
+    Dbig[:, :n] = torch.from_numpy(d).cuda()
+    U = torch.full((n, n + 5), -7, dtype=torch.int32, device="cuda")
+    Cm = torch.full((n, n + 3), 5.0, dtype=torch.float32, device="cuda")
+    s = torch.cuda.Stream()
+    for alg in (_lib.PAIRWISE, _lib.TRIPLET):
+        opts = _lib.make_opts(algorithm=alg)
+        _raise_for(lib.pald_gpu_cohesion_f32_device(Dbig.data_ptr(), n + 13, n, C.byref(opts),
+                                                    U.data_ptr(), n + 5, Cm.data_ptr(), n + 3,
+                                                    s.cuda_stream))
+        s.synchronize()
+        if alg == _lib.PAIRWISE:
+            u_ref, c_ref = oracle.pairwise_f32(d)
+            assert np.array_equal(Cm[:, :n].cpu().numpy().view(np.uint32), c_ref.view(np.uint32))
+        else:
+            u_ref, c_ref = oracle.triplet_f64(d)
+            assert max_rel_diff(Cm[:, :n].cpu().numpy(), c_ref) <= TOL
+        assert np.array_equal(U[:, :n].cpu().numpy(), u_ref)
+        assert bool((U[:, n:] == -7).all()) and bool((Cm[:, n:] == 5.0).all())  # padding untouched
+    # U may be NULL
+    opts = _lib.make_opts()
+    _raise_for(lib.pald_gpu_cohesion_f32_device(Dbig.data_ptr(), n + 13, n, C.byref(opts), None, 0,
+                                                Cm.data_ptr(), n + 3, None))
+    torch.cuda.synchronize()
+    # a plan can be loaded from host memory, and re-run
+    from paper_2307_16652_b200.engine import Engine
+
+    e = Engine(n, "pairwise")
+    for _ in range(2):
+        e.load_host(np.ascontiguousarray(d))
+        e.focus()
+        e.cohesion()
+    torch.cuda.synchronize()
+    u_ref, c_ref = oracle.pairwise_f32(d)
+    assert np.array_equal(e.U.cpu().numpy(), u_ref)
+    assert np.array_equal(e.C.cpu().numpy().view(np.uint32), c_ref.view(np.uint32))
