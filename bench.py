@@ -47,6 +47,13 @@ REASONS = {
 }
 N_SM = 148
 LANES_PER_SM = 128
+DATA_DESC = {
+    "points_uniform_3d": "synthetic: seeded points i.i.d. U[0,1)^3 (numpy PCG64), fp32 Euclidean D computed on the GPU",
+    "points_uniform_2d": "synthetic: seeded points i.i.d. U[0,1)^2 (numpy PCG64), fp32 Euclidean D computed on the GPU",
+    "gmm_16d_8c": "synthetic: seeded 16-D Gaussian mixture (8 centres U[0,1)^16, std 0.1), fp32 Euclidean D on the GPU",
+    "upper_uniform01": "synthetic: seeded symmetric D, upper triangle i.i.d. U(0,1) fp32 (zeros resampled), mirrored",
+    "upper_int_1_16": "synthetic: seeded symmetric D, upper triangle i.i.d. integers {1..16} as fp32, mirrored",
+}
 
 
 def measured_peaks() -> dict:
@@ -414,10 +421,18 @@ def main() -> None:
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist_on = world > 1
+    # Test hook only: PALD_BENCH_BACKEND=gloo runs the multi-rank code path
+    # with ranks sharing the visible GPUs (collectives through the host).
+    backend = os.environ.get("PALD_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if dist_on:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     D, cfg = make_input(args.config, torch.device("cuda", local), args.seed)
     n = cfg.n
@@ -457,7 +472,7 @@ def main() -> None:
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f32",
-        "data": "synthetic: seeded points i.i.d. U[0,1)^3 (numpy PCG64), fp32 Euclidean D computed on the GPU",
+        "data": DATA_DESC.get(cfg.kind, "synthetic"),
         "config": {"workload": cfg.name, "n": n, "algorithm": "pairwise", "seed": args.seed,
                    "parallelism": f"pair-tile sharding x{world}",
                    "l2": "inputs larger than L2 (D = %.1f GiB > 126 MB)" % (n * n * 4 / 2 ** 30)},
