@@ -199,6 +199,17 @@ int pald_gpu_strong_ties(const float* dC, uint64_t ldc, uint64_t n, const double
                          uint32_t* xs, uint32_t* ys, double* strength, uint64_t* count_out,
                          void* stream);
 
+/* The reference's binary matrix format ("PALD", version 1, width 4 or 8,
+ * u64 n, n*n little-endian row-major values; ingest.hpp:214-283).
+ * read_binary_header gives n and the width; read_distance_binary streams
+ * the payload to the device and applies validate_distances
+ * (ingest.hpp:116-149: finite, >= 0, zero diagonal, symmetric within 1e-9
+ * relative -> averaged in double, positive) on the GPU, writing the fp32
+ * matrix (to_real<float>) to dD (n x ldd). Errors carry the reference's
+ * messages: 2 (ValidationError), 4 (IoError, cannot open). */
+int pald_gpu_read_binary_header(const char* path, uint64_t* n_out, int32_t* width_out);
+int pald_gpu_read_distance_binary(const char* path, float* dD, uint64_t ldd, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

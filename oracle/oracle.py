@@ -180,6 +180,7 @@ class Reference:
             "ref_normalize_and_depths": (_i32, [_vp, _u64, _vp]),
             "ref_default_block_config": (_i32, [_u64, _u64, _vp]),
             "ref_parallel_pairwise_prefix_f32": (_i32, [_vp, _u64, _u64, _i32, _u64, d, _vp, _vp]),
+            "ref_read_distance_binary": (_i32, [C.c_char_p, _u64, C.POINTER(C.c_uint64), _vp]),
         }
         for k, (r, a) in sigs.items():
             f = getattr(lib, k)
@@ -250,6 +251,16 @@ class Reference:
 
     def fill_diagonal(self, u, c):
         self._check(self.lib.ref_fill_diagonal(_ptr(np.ascontiguousarray(u, np.int32)), u.shape[0], _ptr(c)))
+
+    def read_distance_binary(self, path, cap=4096):
+        """(status, message, D) of the reference's read_distance_binary."""
+        n = C.c_uint64(0)
+        out = np.empty(cap * cap, np.float64)
+        rc = self.lib.ref_read_distance_binary(str(path).encode(), cap, C.byref(n), _ptr(out))
+        if rc:
+            return rc, self.lib.ref_last_error().decode(), None
+        k = int(n.value)
+        return 0, "", out[: k * k].reshape(k, k).copy()
 
     def default_block_config(self, element_bytes=4, cache_bytes=0):
         out = np.zeros(3, np.uint64)

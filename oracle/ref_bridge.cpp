@@ -179,6 +179,15 @@ int ref_normalize_and_depths(double* c, uint64_t n, double* depths) {
   });
 }
 
+// read_distance_binary, ingest.hpp:280-283 (values copied when n <= cap)
+int ref_read_distance_binary(const char* path, uint64_t cap, uint64_t* n_out, double* out) {
+  return guarded([&] {
+    const auto d = pald::read_distance_binary(path);
+    *n_out = d.size();
+    if (d.size() <= cap) std::memcpy(out, d.values().data(), sizeof(double) * d.size() * d.size());
+  });
+}
+
 // default_block_config, blocked.hpp:510-518 (cache_bytes 0 = detect)
 int ref_default_block_config(uint64_t element_bytes, uint64_t cache_bytes, uint64_t* out3) {
   return guarded([&] {

@@ -17,7 +17,7 @@ LIB_DIR = PKG_DIR / "lib"
 LIB_PATH = LIB_DIR / "libpald_gpu.so"
 INCLUDE = PKG_DIR.parent / "include"
 
-SOURCES = [CSRC / "pald_gpu.cu", CSRC / "pald_epilogue.cu"]
+SOURCES = [CSRC / "pald_gpu.cu", CSRC / "pald_epilogue.cu", CSRC / "pald_io.cu"]
 DEPS = SOURCES + [CSRC / "pald_kernels.cuh", CSRC / "pald_internal.h", INCLUDE / "pald_gpu.h"]
 
 NVCC_FLAGS = [

@@ -39,6 +39,8 @@ EXPORTED_SYMBOLS = (
     "pald_gpu_points_to_distances",
     "pald_gpu_local_depths",
     "pald_gpu_strong_ties",
+    "pald_gpu_read_binary_header",
+    "pald_gpu_read_distance_binary",
 )
 
 
@@ -123,6 +125,8 @@ def load(path: Path | None = None) -> C.CDLL:
         "pald_gpu_points_to_distances": (i32, [vp, u64, u64, vp, u64, vp]),
         "pald_gpu_local_depths": (i32, [vp, u64, u64, vp, vp, vp]),
         "pald_gpu_strong_ties": (i32, [vp, u64, u64, vp, vp, vp, u64, vp, vp, vp, vp, vp]),
+        "pald_gpu_read_binary_header": (i32, [C.c_char_p, C.POINTER(u64), C.POINTER(C.c_int32)]),
+        "pald_gpu_read_distance_binary": (i32, [C.c_char_p, vp, u64, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name, None)
