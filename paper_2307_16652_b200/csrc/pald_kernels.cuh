@@ -58,7 +58,7 @@ constexpr int kKUnroll = PALD_KUNROLL;
 #endif
 
 constexpr int kBK = PALD_BK;    // third-point chunk per pipeline stage
-constexpr int kThreads = 256;   // 8 warps, 16 x 16 threads, 8 x 8 outputs each
+constexpr int kThreads = 256;   // 8 warps, 16 x 16 threads (8 x 8 outputs each on 128-wide tiles)
 __host__ __device__ constexpr int box_bytes(int tile) { return kBK * tile * 4; }
 __host__ __device__ constexpr int stage_bytes(int pass, int tile) { return (pass == 0 ? 2 : 3) * box_bytes(tile); }
 // CTAs per SM: 1 for 128-wide tiles (8 x 8 outputs per thread, ~230
