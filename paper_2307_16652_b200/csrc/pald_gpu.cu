@@ -22,6 +22,7 @@
 #include "../../include/pald_gpu.h"
 #include "pald_internal.h"
 #include "pald_kernels.cuh"
+#include "pald_sym.cuh"
 
 using namespace pald_gpu;
 
@@ -168,12 +169,13 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-int make_map(CUtensorMap* map, const void* base, uint64_t n, uint64_t ld, int box_cols = kTile) {
+int make_map(CUtensorMap* map, const void* base, uint64_t n, uint64_t ld, int box_cols = kTile,
+             int box_rows = kBK) {
   auto encode = get_encode();
   if (!encode) return set_error(PALD_GPU_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {n, n};
   cuuint64_t strides[1] = {ld * 4};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(kBK)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims,
                       strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -241,6 +243,11 @@ struct pald_gpu_plan {
   Stats* stats_host = nullptr;
   CUtensorMap tm_d, tm_dnu, tm_w;        // 128-wide boxes
   CUtensorMap tm_d64, tm_dnu64, tm_w64;  // 64-wide boxes (small-n cohesion tiles)
+  CUtensorMap tm_d32, tm_w32;            // 128 x 32 boxes (tile-pair cohesion)
+  uint32_t* sym_flags = nullptr;         // tie flags per (tile pair, 32-wide k chunk)
+  uint32_t* sym_tile_flags = nullptr;
+  int sym_nw = 0;
+  bool sym_ready = false;                // tie scan done for the loaded D
   bool loaded = false;
   bool exact = false;
   bool focus_dirty = false;
@@ -260,6 +267,8 @@ struct pald_gpu_plan {
     cudaFree(stats);
     cudaFreeHost(stats_host);
     cudaFree(focus_tiles);
+    cudaFree(sym_flags);
+    cudaFree(sym_tile_flags);
     cudaSetDevice(prev);
   }
 };
@@ -276,6 +285,18 @@ struct DeviceGuard {
     if (prev >= 0) cudaSetDevice(prev);
   }
 };
+
+// Tile-pair cohesion (pald_sym.cuh): PALD_GPU_SYM=0 selects the one-sided
+// kernel everywhere, 2 the pair kernel wherever it applies (A/B and tests),
+// default 1 = by the cost model (sym_preferred).
+int sym_mode() {
+  static const int m = [] {
+    const char* e = getenv("PALD_GPU_SYM");
+    return e ? atoi(e) : 1;
+  }();
+  return m;
+}
+bool sym_enabled() { return sym_mode() != 0; }
 
 int plan_alloc(pald_gpu_plan* p) {
   const size_t bytes = p->n * p->ld * 4;
@@ -309,6 +330,13 @@ int plan_alloc(pald_gpu_plan* p) {
   if ((rc = make_map(&p->tm_d64, p->ds, p->n, p->ld, 64))) return rc;
   if ((rc = make_map(&p->tm_dnu64, p->dnu, p->n, p->ld, 64))) return rc;
   if ((rc = make_map(&p->tm_w64, p->w, p->n, p->ld, 64))) return rc;
+  if (p->algorithm == PALD_GPU_PAIRWISE && p->policy == PALD_GPU_STRICT) {
+    if ((rc = make_map(&p->tm_d32, p->ds, p->n, p->ld, kTile, kSymBK))) return rc;
+    if ((rc = make_map(&p->tm_w32, p->w, p->n, p->ld, kTile, kSymBK))) return rc;
+    p->sym_nw = (int)(((p->n + kSymBK - 1) / kSymBK + 31) / 32);
+    PALD_CUDA(cudaMalloc(&p->sym_flags, p->nb * p->nb * p->sym_nw * sizeof(uint32_t)));
+    PALD_CUDA(cudaMalloc(&p->sym_tile_flags, p->nb * sizeof(uint32_t)));
+  }
   // The memsets above run on the legacy default stream; callers may use
   // non-blocking streams, so finish them before the plan is handed out.
   PALD_CUDA(cudaDeviceSynchronize());
@@ -360,6 +388,23 @@ int plan_load_impl(pald_gpu_plan* p, const float* dD, uint64_t ldd, cudaStream_t
   ++p->launches;
   PALD_CUDA(cudaMemsetAsync(p->u, 0, p->n * p->ld * 4, s));
   PALD_CUDA(cudaMemsetAsync(p->w, 0, p->n * p->ld * 4, s));
+  p->sym_ready = false;
+  if (fast && p->sym_flags && sym_enabled()) {
+    // Duplicate scan of the columns of D for the tile-pair cohesion kernel.
+    PALD_CUDA(cudaMemsetAsync(p->sym_flags, 0, p->nb * p->nb * p->sym_nw * sizeof(uint32_t), s));
+    PALD_CUDA(cudaMemsetAsync(p->sym_tile_flags, 0, p->nb * sizeof(uint32_t), s));
+    static bool attr_done[64] = {};
+    if (!attr_done[p->device & 63]) {
+      PALD_CUDA(cudaFuncSetAttribute(tie_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTieSmem));
+      attr_done[p->device & 63] = true;
+    }
+    const int passes = (int)((p->n + kTieCap * 3 / 4 - 1) / (kTieCap * 3 / 4));
+    tie_scan_kernel<<<(unsigned)std::min<uint64_t>(p->n, (uint64_t)p->sms), kTieThreads, kTieSmem, s>>>(
+        p->ds, n, (int)p->ld, (int)p->nb, p->sym_nw, passes, p->sym_flags, p->sym_tile_flags);
+    PALD_CUDA(cudaGetLastError());
+    ++p->launches;
+    p->sym_ready = true;
+  }
   p->loaded = true;
   p->focus_dirty = false;
   return PALD_GPU_OK;
@@ -449,6 +494,36 @@ int launch_cohesion(pald_gpu_plan* p, uint64_t row0, uint64_t row1, cudaStream_t
                  : launch_tile<1, false, true, false, false, false, false, TILE>(md, mn, mw, a, grid, s);
 }
 
+// Tile-pair cohesion over pairs [t0, t1) of the grouped upper-triangular
+// order; writes both C[P][Q] and C[Q][P] of each pair.
+int launch_sym(pald_gpu_plan* p, int t0, int t1, cudaStream_t s) {
+  if (t1 <= t0) return PALD_GPU_OK;
+  static bool attr_done[64] = {};
+  if (!attr_done[p->device & 63]) {
+    PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
+    attr_done[p->device & 63] = true;
+  }
+  SymArgs a{p->ds, p->c, p->focus_tiles, p->sym_flags, p->sym_tile_flags,
+            (int)p->n, (int)p->ld, (int)p->nb, p->sym_nw, t0, t1};
+  const int grid = std::min(t1 - t0, p->sms);
+  pald_sym_cohesion_kernel<<<grid, kThreads, kSymSmem, s>>>(p->tm_d32, p->tm_w32, a);
+  PALD_CUDA(cudaGetLastError());
+  return PALD_GPU_OK;
+}
+
+// Rounds-based cost model (in one-sided 128-tile times): a pair does twice
+// the outputs at ~1.4x the time of a one-sided tile (tools/microbench3.cu);
+// 64-wide one-sided tiles run 2 per SM at ~0.52 of a 128-tile time.
+bool sym_preferred(const pald_gpu_plan* p) {
+  if (sym_mode() == 2) return true;
+  const double sms = p->sms, nb = (double)p->nb, nb64 = (double)((p->n + 63) / 64);
+  const double pairs = nb * (nb + 1) / 2;
+  const double t_sym = std::ceil(pairs / sms) * 1.44;
+  const double t_128 = std::ceil(nb * nb / sms);
+  const double t_64 = std::ceil(nb64 * nb64 / (2 * sms)) * 0.52;
+  return t_sym < std::min(t_128, t_64);
+}
+
 int plan_cohesion_impl(pald_gpu_plan* p, uint64_t row0, uint64_t row1, cudaStream_t s) {
   if (!p->loaded) return set_error(PALD_GPU_ERR_VALIDATION, "plan has no distances loaded");
   row1 = std::min(row1, p->n);
@@ -459,6 +534,11 @@ int plan_cohesion_impl(pald_gpu_plan* p, uint64_t row0, uint64_t row1, cudaStrea
   // 2 CTAs per SM) so small problems fill the 148 SMs. Results are
   // identical: every C entry is the same in-order sum either way.
   const uint64_t tiles128 = ((row1 - row0 + kTile - 1) / kTile) * p->nb;
+  if (row0 == 0 && row1 == p->n && p->sym_ready && sym_preferred(p)) {
+    const int rc = launch_sym(p, 0, (int)(p->nb * (p->nb + 1) / 2), s);
+    if (rc == PALD_GPU_OK) ++p->launches;
+    return rc;
+  }
   static const int force_tile = [] {
     const char* e = getenv("PALD_GPU_COHESION_TILE");  // testing knob: 64 or 128
     return e ? atoi(e) : 0;

@@ -1,0 +1,391 @@
+// pald_sym.cuh -- pass 2 (cohesion) over tile PAIRS: one min + one compare
+// per (r, c, k) feeds both C[r][c] and C[c][r].
+//
+// Gather form (pald_kernels.cuh): C[r][c] = sum_k W_rk [T_rc < min(A'_rk, B'_kc)]
+// with A = D[k][r], B = D[k][c], T = D[r][c]. The transposed output reads
+// T_cr = T_rc and the same two distances with the roles of A and B swapped:
+//
+//   C[c][r] = sum_k W_ck [T_rc < min(B''_kc, A''_rk)]
+//
+// so without the nu() transforms both indicators are the same number
+// [T_rc < min(d_kr, d_kc)]. The transforms only change a comparison when
+// the two compared values are EQUAL (T < nu(x) <=> T <= x), so:
+//
+//   * pairwise Strict (B' = nu(B) iff k < r; for the transposed output
+//     nu(d_kr) iff k < c): both outputs equal the shared strict indicator
+//     unless T_rc == d_kc or T_rc == d_kr for some k not in {r, c}, i.e.
+//     unless column c of D holds d_rc twice (rows r and k) or column r holds
+//     d_cr twice (rows c and k). A per-column duplicate scan at load time
+//     (tie_scan_kernel) flags every (tile pair, 32-wide k chunk) block that
+//     can contain such a tie; flagged blocks take the per-element exact
+//     step (two mins, the nu() of each output), unflagged blocks the shared
+//     step. k in {r, c} needs no flag: the min then contains d_rr = 0 or
+//     d_cc = 0 and both indicators are 0 (T > 0: the fast path requires
+//     positive off-diagonal distances), unless the nu'd zero is compared
+//     with T = 0, which is itself a duplicate of column c (d_rc = d_cc = 0)
+//     and flagged.
+//
+// Every C entry is still one fp32 sum over k ascending of the same terms as
+// the one-sided kernel (bit-identical to the reference); only the number of
+// FMNMX / FFMA.SAT instructions per output halves (tools/microbench3.cu:
+// 49 vs 36 output combos per SM-cycle).
+#pragma once
+
+#include "pald_kernels.cuh"
+
+namespace pald_gpu {
+
+constexpr int kSymBK = 32;                         // k chunk per stage
+constexpr int kSymStages = 3;
+constexpr int kSymBox = kSymBK * kTile * 4;        // one 32 x 128 fp32 box (16 KB)
+constexpr int kSymStageBytes = 4 * kSymBox;        // A, B, W rows, W cols
+constexpr int kSymSmem = kSymStages * kSymStageBytes + 1024;
+
+// Tie scan: buckets and capacity of one pass over a column in shared memory.
+constexpr int kTieBuckets = 4096;
+constexpr int kTieCap = 16384;
+constexpr int kTieThreads = 1024;
+constexpr int kTieMaxBucket = 64;  // larger buckets flag the whole tile
+constexpr int kTieSmem = kTieCap * 8 + kTieBuckets * 8;
+
+struct SymArgs {
+  const uint32_t* d;          // scaled fp32 layout of D (n x ld)
+  float* c;                   // cohesion (n x ld)
+  const int2* tiles;          // tile pairs (P <= Q), grouped order
+  const uint32_t* flags;      // [nb * nb][nw] chunk bits of pair (P, Q), P <= Q
+  const uint32_t* tile_flags; // [nb]: every block of this tile is flagged
+  int n, ld, nb, nw;
+  int tile_begin, tile_end;   // share of the tile-pair list
+};
+
+__device__ __forceinline__ uint32_t tie_hash(uint32_t key) { return key * 0x9E3779B1u; }
+
+// Flags for the duplicate pairs of column j. One CTA per column (row j of
+// the symmetric layout, read coalesced); `passes` hash partitions of the
+// column are bucketed in shared memory in turn and compared within buckets.
+__global__ void __launch_bounds__(kTieThreads)
+    tie_scan_kernel(const uint32_t* __restrict__ d, int n, int ld, int nb, int nw, int passes,
+                    uint32_t* __restrict__ flags, uint32_t* __restrict__ tile_flags) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint32_t* keys = reinterpret_cast<uint32_t*>(smem_raw);
+  uint32_t* idx = keys + kTieCap;
+  uint32_t* cnt = idx + kTieCap;
+  uint32_t* pos = cnt + kTieBuckets;
+  __shared__ uint32_t warp_sums[kTieThreads / 32];
+  __shared__ int overflow;
+  const int tid = threadIdx.x;
+  for (int j = blockIdx.x; j < n; j += gridDim.x) {
+    const uint32_t* row = d + (size_t)j * ld;
+    const int tj = j / kTile;
+    for (int pass = 0; pass < passes; ++pass) {
+      for (int b = tid; b < kTieBuckets; b += kTieThreads) cnt[b] = 0;
+      if (tid == 0) overflow = 0;
+      __syncthreads();
+      for (int i = tid; i < n; i += kTieThreads) {
+        const uint32_t h = tie_hash(row[i]);
+        if ((int)(((uint64_t)h * (uint32_t)passes) >> 32) != pass) continue;
+        atomicAdd(&cnt[h & (kTieBuckets - 1)], 1u);
+      }
+      __syncthreads();
+      // exclusive scan of cnt -> pos (4 buckets per thread)
+      uint32_t loc[4], s = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        loc[q] = s;
+        s += cnt[tid * 4 + q];
+      }
+      uint32_t incl = s;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if ((tid & 31) >= o) incl += v;
+      }
+      if ((tid & 31) == 31) warp_sums[tid >> 5] = incl;
+      __syncthreads();
+      if (tid < 32) {
+        uint32_t ws = warp_sums[tid], wi = ws;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t v = __shfl_up_sync(0xffffffffu, wi, o);
+          if (tid >= o) wi += v;
+        }
+        warp_sums[tid] = wi - ws;  // exclusive prefix of the warps
+      }
+      __syncthreads();
+      const uint32_t base = warp_sums[tid >> 5] + incl - s;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) pos[tid * 4 + q] = base + loc[q];
+      if (tid == kTieThreads - 1 && base + s > (uint32_t)kTieCap) overflow = 1;
+      __syncthreads();
+      if (overflow) {  // too many values in this partition: flag the tile
+        if (tid == 0) atomicOr(&tile_flags[tj], 1u);
+        __syncthreads();
+        break;
+      }
+      for (int i = tid; i < n; i += kTieThreads) {
+        const uint32_t key = row[i], h = tie_hash(key);
+        if ((int)(((uint64_t)h * (uint32_t)passes) >> 32) != pass) continue;
+        const uint32_t o = atomicAdd(&pos[h & (kTieBuckets - 1)], 1u);
+        keys[o] = key;
+        idx[o] = (uint32_t)i;
+      }
+      __syncthreads();
+      for (int b = tid; b < kTieBuckets; b += kTieThreads) {
+        const uint32_t hi = pos[b], lo = hi - cnt[b];
+        if (hi - lo > (uint32_t)kTieMaxBucket) {
+          atomicOr(&tile_flags[tj], 1u);
+          continue;
+        }
+        for (uint32_t e1 = lo; e1 < hi; ++e1) {
+          const uint32_t k1 = keys[e1];
+          for (uint32_t e2 = e1 + 1; e2 < hi; ++e2) {
+            if (keys[e2] != k1) continue;
+            // column j holds the same value at rows a and b: flag
+            // (pair {tile(j), tile(a)}, chunk(b)) and the mirror
+            const int a = (int)idx[e1], bb = (int)idx[e2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int x = h ? bb : a, k = h ? a : bb;
+              const int tx = x / kTile, P = min(tj, tx), Q = max(tj, tx);
+              const int ch = k / kSymBK;
+              atomicOr(&flags[((size_t)P * nb + Q) * nw + (ch >> 5)], 1u << (ch & 31));
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Shared step: one min + one compare per (r, c) pair, two accumulates.
+__device__ __forceinline__ void sym_step(const float* __restrict__ sa, const float* __restrict__ sb,
+                                         const float* __restrict__ sw, const float* __restrict__ sv,
+                                         int kk, int ty, int tx, const float2 (&thr)[8][4],
+                                         float2 (&acc)[8][4], float2 (&act)[8][4]) {
+  float a[8], b[8], w[8], v[8];
+  {
+    const float4 a0 = reinterpret_cast<const float4*>(sa + kk * kTile)[ty];
+    const float4 a1 = reinterpret_cast<const float4*>(sa + kk * kTile)[16 + ty];
+    const float4 b0 = reinterpret_cast<const float4*>(sb + kk * kTile)[tx];
+    const float4 b1 = reinterpret_cast<const float4*>(sb + kk * kTile)[16 + tx];
+    const float4 w0 = reinterpret_cast<const float4*>(sw + kk * kTile)[ty];
+    const float4 w1 = reinterpret_cast<const float4*>(sw + kk * kTile)[16 + ty];
+    const float4 v0 = reinterpret_cast<const float4*>(sv + kk * kTile)[tx];
+    const float4 v1 = reinterpret_cast<const float4*>(sv + kk * kTile)[16 + tx];
+    a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w;
+    a[4] = a1.x; a[5] = a1.y; a[6] = a1.z; a[7] = a1.w;
+    b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w;
+    b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
+    w[0] = w0.x; w[1] = w0.y; w[2] = w0.z; w[3] = w0.w;
+    w[4] = w1.x; w[5] = w1.y; w[6] = w1.z; w[7] = w1.w;
+    v[0] = v0.x; v[1] = v0.y; v[2] = v0.z; v[3] = v0.w;
+    v[4] = v1.x; v[5] = v1.y; v[6] = v1.z; v[7] = v1.w;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+#pragma unroll
+    for (int jp = 0; jp < 4; ++jp) {
+      const float m0 = fminf(a[i], b[2 * jp]);
+      const float m1 = fminf(a[i], b[2 * jp + 1]);
+      const float2 kv = make_float2(__saturatef(__fmaf_rn(m0, kCmpScale, thr[i][jp].x)),
+                                    __saturatef(__fmaf_rn(m1, kCmpScale, thr[i][jp].y)));
+      acc[i][jp] = __ffma2_rn(kv, make_float2(w[i], w[i]), acc[i][jp]);
+      act[i][jp] = __ffma2_rn(kv, make_float2(v[2 * jp], v[2 * jp + 1]), act[i][jp]);
+    }
+  }
+}
+
+// Exact step (flagged blocks, ragged last chunk): each output with its own
+// nu(): C[r][c] uses min(d_kr, nu(d_kc) iff k < r), C[c][r] uses
+// min(d_kc, nu(d_kr) iff k < c) -- pairwise Strict, blocked.hpp:126-186.
+__device__ __forceinline__ void sym_step_exact(const float* __restrict__ sa,
+                                               const float* __restrict__ sb,
+                                               const float* __restrict__ sw,
+                                               const float* __restrict__ sv, int kk, int kg,
+                                               int ty, int tx, int r0, int c0,
+                                               const float2 (&thr)[8][4], float2 (&acc)[8][4],
+                                               float2 (&act)[8][4]) {
+  float a[8], b[8], w[8], v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    a[i] = sa[kk * kTile + row_off<kTile>(ty, i)];
+    w[i] = sw[kk * kTile + row_off<kTile>(ty, i)];
+    b[i] = sb[kk * kTile + row_off<kTile>(tx, i)];
+    v[i] = sv[kk * kTile + row_off<kTile>(tx, i)];
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const bool below_r = kg < r0 + row_off<kTile>(ty, i);
+    const float an = nu_f(a[i]);
+#pragma unroll
+    for (int jp = 0; jp < 4; ++jp) {
+      float kd[2], kt[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = 2 * jp + h;
+        const bool below_c = kg < c0 + row_off<kTile>(tx, j);
+        const float t = h ? thr[i][jp].y : thr[i][jp].x;
+        const float md = fminf(a[i], below_r ? nu_f(b[j]) : b[j]);
+        const float mt = fminf(b[j], below_c ? an : a[i]);
+        kd[h] = __saturatef(__fmaf_rn(md, kCmpScale, t));
+        kt[h] = __saturatef(__fmaf_rn(mt, kCmpScale, t));
+      }
+      acc[i][jp] = __ffma2_rn(make_float2(kd[0], kd[1]), make_float2(w[i], w[i]), acc[i][jp]);
+      act[i][jp] = __ffma2_rn(make_float2(kt[0], kt[1]), make_float2(v[2 * jp], v[2 * jp + 1]),
+                              act[i][jp]);
+    }
+  }
+}
+
+// Persistent pass-2 kernel over the tile pairs [tile_begin, tile_end) of the
+// grouped upper-triangular order (P <= Q). CTA g takes pairs
+// tile_begin + g, + G, ...; each pair streams all k chunks through a
+// 3-stage TMA/mbarrier pipeline (four 32 x 128 boxes per stage) and writes
+// C[P rows][Q cols] and, for P < Q, C[Q rows][P cols]. Pairwise Strict
+// cohesion on the fast (scaled fp32) layout.
+__global__ void __launch_bounds__(kThreads, 1)
+    pald_sym_cohesion_kernel(const __grid_constant__ CUtensorMap tm_d,
+                             const __grid_constant__ CUtensorMap tm_w, const SymArgs args) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  __shared__ uint64_t full_bar[kSymStages];
+  __shared__ uint32_t done_cnt[kSymStages];
+  const int tid = threadIdx.x;
+  const int n = args.n, ld = args.ld;
+  const int nch = (n + kSymBK - 1) / kSymBK;
+  const int G = gridDim.x, g = blockIdx.x;
+  const int first = args.tile_begin + g;
+  const int R = first < args.tile_end ? (args.tile_end - 1 - first) / G + 1 : 0;
+  const int P = R * nch;
+  if (P <= 0) return;
+  if (tid == 0) {
+    for (int s = 0; s < kSymStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      done_cnt[s] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  auto issue = [&](int ri, int ch, int s) {
+    const int2 tp = args.tiles[first + ri * G];
+    const int r0 = tp.x * kTile, c0 = tp.y * kTile, k0 = ch * kSymBK;
+    uint8_t* st = smem + s * kSymStageBytes;
+    mbar_expect_tx(&full_bar[s], kSymStageBytes);
+    tma_load_2d(st, &tm_d, r0, k0, &full_bar[s]);
+    tma_load_2d(st + kSymBox, &tm_d, c0, k0, &full_bar[s]);
+    tma_load_2d(st + 2 * kSymBox, &tm_w, r0, k0, &full_bar[s]);
+    tma_load_2d(st + 3 * kSymBox, &tm_w, c0, k0, &full_bar[s]);
+  };
+  int pr_ri = 0, pr_ch = 0;
+  auto pr_advance = [&]() {
+    if (++pr_ch == nch) {
+      pr_ch = 0;
+      ++pr_ri;
+    }
+  };
+  for (int p = 0; p < kSymStages && p < P; ++p) {
+    if (tid == 0) issue(pr_ri, pr_ch, p);
+    pr_advance();
+  }
+
+  const int warp = tid >> 5, lane = tid & 31;
+  const int ty = (warp >> 1) * 4 + (lane >> 3);
+  const int tx = (warp & 1) * 8 + (lane & 7);
+
+  int p = 0;
+  for (int ri = 0; ri < R; ++ri) {
+    const int2 tp = args.tiles[first + ri * G];
+    const int r0 = tp.x * kTile, c0 = tp.y * kTile;
+    const bool diag = tp.x == tp.y;
+    const uint32_t* fl = args.flags + ((size_t)tp.x * args.nb + tp.y) * args.nw;
+    const bool all_flagged = (__ldg(args.tile_flags + tp.x) | __ldg(args.tile_flags + tp.y)) != 0u;
+    float2 thr[8][4], acc[8][4], act[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+#pragma unroll
+      for (int jp = 0; jp < 4; ++jp) {
+        float t2[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = r0 + row_off<kTile>(ty, i), c = c0 + row_off<kTile>(tx, 2 * jp + h);
+          const uint32_t tv = (r < n && c < n) ? __ldg(args.d + (size_t)r * ld + c) : 0u;
+          t2[h] = __uint_as_float(tv) * -kCmpScale;
+        }
+        thr[i][jp] = make_float2(t2[0], t2[1]);
+        acc[i][jp] = make_float2(0.f, 0.f);
+        act[i][jp] = make_float2(0.f, 0.f);
+      }
+    }
+    for (int ch = 0; ch < nch; ++ch, ++p) {
+      const int s = p % kSymStages;
+      mbar_wait(&full_bar[s], (p / kSymStages) & 1);
+      const uint8_t* st = smem + s * kSymStageBytes;
+      const float* sa = reinterpret_cast<const float*>(st);
+      const float* sb = reinterpret_cast<const float*>(st + kSymBox);
+      const float* sw = reinterpret_cast<const float*>(st + 2 * kSymBox);
+      const float* sv = reinterpret_cast<const float*>(st + 3 * kSymBox);
+      const int k0 = ch * kSymBK;
+      const int kmax = min(kSymBK, n - k0);
+      const bool flagged = all_flagged || ((__ldg(fl + (ch >> 5)) >> (ch & 31)) & 1u);
+      if (!flagged && kmax == kSymBK) {
+#pragma unroll 2
+        for (int kk = 0; kk < kSymBK; ++kk) sym_step(sa, sb, sw, sv, kk, ty, tx, thr, acc, act);
+      } else {
+        for (int kk = 0; kk < kmax; ++kk)
+          sym_step_exact(sa, sb, sw, sv, kk, k0 + kk, ty, tx, r0, c0, thr, acc, act);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        const uint32_t old = atomicAdd(&done_cnt[s], 1u);
+        if (old == (uint32_t)(p / kSymStages + 1) * (kThreads / 32) - 1u && p + kSymStages < P)
+          issue(pr_ri, pr_ch, s);
+        pr_advance();
+      }
+    }
+    // ---- flush: C[r][c] (rows of P, columns of Q) ------------------------
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = r0 + row_off<kTile>(ty, i);
+      if (r >= n) continue;
+      float* crow = args.c + (size_t)r * ld;
+      const int ca = c0 + tx * 4, cb = c0 + 64 + tx * 4;
+      if (ca < n)
+        *reinterpret_cast<float4*>(crow + ca) =
+            make_float4(acc[i][0].x, acc[i][0].y, acc[i][1].x, acc[i][1].y);
+      if (cb < n)
+        *reinterpret_cast<float4*>(crow + cb) =
+            make_float4(acc[i][2].x, acc[i][2].y, acc[i][3].x, acc[i][3].y);
+    }
+    // ---- C[c][r] (rows of Q, columns of P); the diagonal pair already
+    // wrote every entry of its tile above.
+    if (!diag) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int c = c0 + row_off<kTile>(tx, j);
+        if (c >= n) continue;
+        float* crow = args.c + (size_t)c * ld;
+        const int ra = r0 + ty * 4, rb = r0 + 64 + ty * 4;
+        const int jp = j >> 1;
+        if ((j & 1) == 0) {
+          if (ra < n)
+            *reinterpret_cast<float4*>(crow + ra) =
+                make_float4(act[0][jp].x, act[1][jp].x, act[2][jp].x, act[3][jp].x);
+          if (rb < n)
+            *reinterpret_cast<float4*>(crow + rb) =
+                make_float4(act[4][jp].x, act[5][jp].x, act[6][jp].x, act[7][jp].x);
+        } else {
+          if (ra < n)
+            *reinterpret_cast<float4*>(crow + ra) =
+                make_float4(act[0][jp].y, act[1][jp].y, act[2][jp].y, act[3][jp].y);
+          if (rb < n)
+            *reinterpret_cast<float4*>(crow + rb) =
+                make_float4(act[4][jp].y, act[5][jp].y, act[6][jp].y, act[7][jp].y);
+        }
+      }
+    }
+  }
+}
+
+}  // namespace pald_gpu

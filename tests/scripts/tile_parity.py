@@ -1,5 +1,9 @@
 """Helper run in a subprocess by tests/test_gpu_tiles.py: parity of the
-cohesion kernel at the tile width forced by PALD_GPU_COHESION_TILE."""
+cohesion kernel at the tile width forced by PALD_GPU_COHESION_TILE, or of
+the tile-pair kernel forced by PALD_GPU_SYM=2. Kinds: "rand" (no ties),
+"ties" (integers 1..16: every block tied, whole tiles flagged), "fewties"
+(values on a 2^-9 grid: a few duplicates per column, so flagged and
+unflagged blocks mix)."""
 import sys
 from pathlib import Path
 
@@ -19,8 +23,13 @@ def main():
     o = Oracle()
     sizes = [int(x) for x in sys.argv[1:]] or [2, 65, 129, 300]
     for n in sizes:
-        for kind in ("rand", "ties"):
-            d = random_upper(n, n) if kind == "rand" else int_upper(n, n)
+        for kind in ("rand", "ties", "fewties"):
+            if kind == "rand":
+                d = random_upper(n, n)
+            elif kind == "ties":
+                d = int_upper(n, n)
+            else:
+                d = (np.round(random_upper(n, n + 1) * 512) / 512).astype(np.float32)
             D = torch.from_numpy(d).cuda()
             for policy in ("strict", "split"):
                 for exact in (False, True):

@@ -1,6 +1,7 @@
-"""Both cohesion tile widths (128 and the small-n 64) at the same sizes,
-forced through PALD_GPU_COHESION_TILE in a subprocess (the launcher reads
-it once per process)."""
+"""Both cohesion tile widths (128 and the small-n 64) and the tile-pair
+kernel (pald_sym.cuh) at the same sizes, forced through
+PALD_GPU_COHESION_TILE / PALD_GPU_SYM in a subprocess (the launcher reads
+them once per process)."""
 import os
 import subprocess
 import sys
@@ -12,9 +13,13 @@ pytestmark = pytest.mark.gpu
 SCRIPT = Path(__file__).resolve().parent / "scripts" / "tile_parity.py"
 
 
-@pytest.mark.parametrize("tile,sizes", [("128", ["2", "65", "129", "300"]), ("64", ["3", "64", "257", "520"])])
-def test_cohesion_tile_width(tile, sizes):
-    env = dict(os.environ, PALD_GPU_COHESION_TILE=tile)
+@pytest.mark.parametrize("tile,sym,sizes", [
+    ("128", "0", ["2", "65", "129", "300"]),
+    ("64", "0", ["3", "64", "257", "520"]),
+    ("128", "2", ["2", "127", "128", "129", "300", "520"]),
+])
+def test_cohesion_tile_width(tile, sym, sizes):
+    env = dict(os.environ, PALD_GPU_COHESION_TILE=tile, PALD_GPU_SYM=sym)
     out = subprocess.run([sys.executable, str(SCRIPT), *sizes], env=env, capture_output=True, text=True,
                          timeout=900)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-4000:]
