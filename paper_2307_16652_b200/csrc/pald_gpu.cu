@@ -244,9 +244,11 @@ struct pald_gpu_plan {
   CUtensorMap tm_d, tm_dnu, tm_w;        // 128-wide boxes
   CUtensorMap tm_d64, tm_dnu64, tm_w64;  // 64-wide boxes (small-n cohesion tiles)
   CUtensorMap tm_d32, tm_w32;            // 128 x 32 boxes (tile-pair cohesion)
-  uint32_t* sym_flags = nullptr;         // tie flags per (tile pair, 32-wide k chunk)
+  uint32_t* sym_masks = nullptr;         // tie k-masks per (tile pair, 32-wide k chunk)
   uint32_t* sym_tile_flags = nullptr;
-  int sym_nw = 0;
+  unsigned long long* sym_count = nullptr;
+  int sym_nch = 0;
+  double sym_marked = 0;                 // share of (pair, k) steps on the exact step
   bool sym_ready = false;                // tie scan done for the loaded D
   bool loaded = false;
   bool exact = false;
@@ -267,8 +269,9 @@ struct pald_gpu_plan {
     cudaFree(stats);
     cudaFreeHost(stats_host);
     cudaFree(focus_tiles);
-    cudaFree(sym_flags);
+    cudaFree(sym_masks);
     cudaFree(sym_tile_flags);
+    cudaFree(sym_count);
     cudaSetDevice(prev);
   }
 };
@@ -297,6 +300,8 @@ int sym_mode() {
   return m;
 }
 bool sym_enabled() { return sym_mode() != 0; }
+
+size_t sym_mask_words(const pald_gpu_plan* p) { return p->nb * (p->nb + 1) / 2 * p->sym_nch; }
 
 int plan_alloc(pald_gpu_plan* p) {
   const size_t bytes = p->n * p->ld * 4;
@@ -333,9 +338,10 @@ int plan_alloc(pald_gpu_plan* p) {
   if (p->algorithm == PALD_GPU_PAIRWISE && p->policy == PALD_GPU_STRICT) {
     if ((rc = make_map(&p->tm_d32, p->ds, p->n, p->ld, kTile, kSymBK))) return rc;
     if ((rc = make_map(&p->tm_w32, p->w, p->n, p->ld, kTile, kSymBK))) return rc;
-    p->sym_nw = (int)(((p->n + kSymBK - 1) / kSymBK + 31) / 32);
-    PALD_CUDA(cudaMalloc(&p->sym_flags, p->nb * p->nb * p->sym_nw * sizeof(uint32_t)));
+    p->sym_nch = (int)((p->n + kSymBK - 1) / kSymBK);
+    PALD_CUDA(cudaMalloc(&p->sym_masks, sym_mask_words(p) * sizeof(uint32_t)));
     PALD_CUDA(cudaMalloc(&p->sym_tile_flags, p->nb * sizeof(uint32_t)));
+    PALD_CUDA(cudaMalloc(&p->sym_count, sizeof(unsigned long long)));
   }
   // The memsets above run on the legacy default stream; callers may use
   // non-blocking streams, so finish them before the plan is handed out.
@@ -389,10 +395,12 @@ int plan_load_impl(pald_gpu_plan* p, const float* dD, uint64_t ldd, cudaStream_t
   PALD_CUDA(cudaMemsetAsync(p->u, 0, p->n * p->ld * 4, s));
   PALD_CUDA(cudaMemsetAsync(p->w, 0, p->n * p->ld * 4, s));
   p->sym_ready = false;
-  if (fast && p->sym_flags && sym_enabled()) {
+  if (fast && p->sym_masks && sym_enabled()) {
     // Duplicate scan of the columns of D for the tile-pair cohesion kernel.
-    PALD_CUDA(cudaMemsetAsync(p->sym_flags, 0, p->nb * p->nb * p->sym_nw * sizeof(uint32_t), s));
+    const size_t words = sym_mask_words(p);
+    PALD_CUDA(cudaMemsetAsync(p->sym_masks, 0, words * sizeof(uint32_t), s));
     PALD_CUDA(cudaMemsetAsync(p->sym_tile_flags, 0, p->nb * sizeof(uint32_t), s));
+    PALD_CUDA(cudaMemsetAsync(p->sym_count, 0, sizeof(unsigned long long), s));
     static bool attr_done[64] = {};
     if (!attr_done[p->device & 63]) {
       PALD_CUDA(cudaFuncSetAttribute(tie_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTieSmem));
@@ -400,10 +408,29 @@ int plan_load_impl(pald_gpu_plan* p, const float* dD, uint64_t ldd, cudaStream_t
     }
     const int passes = (int)((p->n + kTieCap * 3 / 4 - 1) / (kTieCap * 3 / 4));
     tie_scan_kernel<<<(unsigned)std::min<uint64_t>(p->n, (uint64_t)p->sms), kTieThreads, kTieSmem, s>>>(
-        p->ds, n, (int)p->ld, (int)p->nb, p->sym_nw, passes, p->sym_flags, p->sym_tile_flags);
+        p->ds, n, (int)p->ld, (int)p->nb, p->sym_nch, passes, p->sym_masks, p->sym_tile_flags);
     PALD_CUDA(cudaGetLastError());
-    ++p->launches;
+    tie_count_kernel<<<(unsigned)p->sms * 4, 256, 0, s>>>(p->sym_masks, words, p->sym_count);
+    PALD_CUDA(cudaGetLastError());
+    p->launches += 2;
+    unsigned long long marked = 0;
+    std::vector<uint32_t> tf(p->nb);
+    PALD_CUDA(cudaMemcpyAsync(&marked, p->sym_count, sizeof(marked), cudaMemcpyDeviceToHost, s));
+    PALD_CUDA(cudaMemcpyAsync(tf.data(), p->sym_tile_flags, tf.size() * 4, cudaMemcpyDeviceToHost, s));
+    PALD_CUDA(cudaStreamSynchronize(s));
+    // Pairs touching a fully marked tile run the exact step everywhere.
+    uint64_t full_pairs = 0, flagged_tiles = 0;
+    for (uint64_t P = 0; P < p->nb; ++P) {
+      flagged_tiles += tf[P] != 0;
+      for (uint64_t Q = P; Q < p->nb; ++Q) full_pairs += (tf[P] | tf[Q]) != 0;
+    }
+    const double pairs = (double)(p->nb * (p->nb + 1) / 2);
+    const double steps = pairs * (double)p->n;
+    p->sym_marked = std::min(1.0, ((double)marked + (double)full_pairs * (double)p->n) / steps);
     p->sym_ready = true;
+    if (getenv("PALD_GPU_DEBUG_TIES"))
+      fprintf(stderr, "[pald_gpu] tie scan: %.4f%% of (pair, k) steps exact, %llu of %llu tiles fully\n",
+              100.0 * p->sym_marked, (unsigned long long)flagged_tiles, (unsigned long long)p->nb);
   }
   p->loaded = true;
   p->focus_dirty = false;
@@ -503,8 +530,8 @@ int launch_sym(pald_gpu_plan* p, int t0, int t1, cudaStream_t s) {
     PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
     attr_done[p->device & 63] = true;
   }
-  SymArgs a{p->ds, p->c, p->focus_tiles, p->sym_flags, p->sym_tile_flags,
-            (int)p->n, (int)p->ld, (int)p->nb, p->sym_nw, t0, t1};
+  SymArgs a{p->ds, p->c, p->focus_tiles, p->sym_masks, p->sym_tile_flags,
+            (int)p->n, (int)p->ld, (int)p->nb, p->sym_nch, t0, t1};
   const int grid = std::min(t1 - t0, p->sms);
   pald_sym_cohesion_kernel<<<grid, kThreads, kSymSmem, s>>>(p->tm_d32, p->tm_w32, a);
   PALD_CUDA(cudaGetLastError());
@@ -512,13 +539,14 @@ int launch_sym(pald_gpu_plan* p, int t0, int t1, cudaStream_t s) {
 }
 
 // Rounds-based cost model (in one-sided 128-tile times): a pair does twice
-// the outputs at ~1.4x the time of a one-sided tile (tools/microbench3.cu);
-// 64-wide one-sided tiles run 2 per SM at ~0.52 of a 128-tile time.
+// the outputs at ~1.44x the time of a one-sided tile (tools/microbench3.cu),
+// its exact k steps ~2.45x slower than shared ones (measured on all-tied
+// data); 64-wide one-sided tiles run 2 per SM at ~0.52 of a 128-tile time.
 bool sym_preferred(const pald_gpu_plan* p) {
   if (sym_mode() == 2) return true;
   const double sms = p->sms, nb = (double)p->nb, nb64 = (double)((p->n + 63) / 64);
   const double pairs = nb * (nb + 1) / 2;
-  const double t_sym = std::ceil(pairs / sms) * 1.44;
+  const double t_sym = std::ceil(pairs / sms) * 1.44 * (1.0 + 1.45 * p->sym_marked);
   const double t_128 = std::ceil(nb * nb / sms);
   const double t_64 = std::ceil(nb64 * nb64 / (2 * sms)) * 0.52;
   return t_sym < std::min(t_128, t_64);

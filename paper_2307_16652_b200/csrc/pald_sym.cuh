@@ -16,10 +16,10 @@
 //     unless T_rc == d_kc or T_rc == d_kr for some k not in {r, c}, i.e.
 //     unless column c of D holds d_rc twice (rows r and k) or column r holds
 //     d_cr twice (rows c and k). A per-column duplicate scan at load time
-//     (tie_scan_kernel) flags every (tile pair, 32-wide k chunk) block that
-//     can contain such a tie; flagged blocks take the per-element exact
-//     step (two mins, the nu() of each output), unflagged blocks the shared
-//     step. k in {r, c} needs no flag: the min then contains d_rr = 0 or
+//     (tie_scan_kernel) marks every third point k that can meet such a tie
+//     in a tile pair (one 32-bit mask per (tile pair, 32-wide k chunk)); the
+//     marked k steps take the per-element exact step (two mins, the nu() of
+//     each output), all others the shared step. k in {r, c} needs no flag: the min then contains d_rr = 0 or
 //     d_cc = 0 and both indicators are 0 (T > 0: the fast path requires
 //     positive off-diagonal distances), unless the nu'd zero is compared
 //     with T = 0, which is itself a duplicate of column c (d_rc = d_cc = 0)
@@ -52,20 +52,24 @@ struct SymArgs {
   const uint32_t* d;          // scaled fp32 layout of D (n x ld)
   float* c;                   // cohesion (n x ld)
   const int2* tiles;          // tile pairs (P <= Q), grouped order
-  const uint32_t* flags;      // [nb * nb][nw] chunk bits of pair (P, Q), P <= Q
-  const uint32_t* tile_flags; // [nb]: every block of this tile is flagged
-  int n, ld, nb, nw;
+  const uint32_t* masks;      // [pair_index(P, Q)][nch]: k bits of each 32-wide chunk
+  const uint32_t* tile_flags; // [nb]: every k of every pair of this tile is marked
+  int n, ld, nb, nch;
   int tile_begin, tile_end;   // share of the tile-pair list
 };
 
 __device__ __forceinline__ uint32_t tie_hash(uint32_t key) { return key * 0x9E3779B1u; }
+// Index of tile pair (P, Q), P <= Q, in row-major upper-triangular order.
+__host__ __device__ __forceinline__ size_t pair_index(int P, int Q, int nb) {
+  return (size_t)P * (2 * nb - P + 1) / 2 + (Q - P);
+}
 
 // Flags for the duplicate pairs of column j. One CTA per column (row j of
 // the symmetric layout, read coalesced); `passes` hash partitions of the
 // column are bucketed in shared memory in turn and compared within buckets.
 __global__ void __launch_bounds__(kTieThreads)
-    tie_scan_kernel(const uint32_t* __restrict__ d, int n, int ld, int nb, int nw, int passes,
-                    uint32_t* __restrict__ flags, uint32_t* __restrict__ tile_flags) {
+    tie_scan_kernel(const uint32_t* __restrict__ d, int n, int ld, int nb, int nch, int passes,
+                    uint32_t* __restrict__ masks, uint32_t* __restrict__ tile_flags) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint32_t* keys = reinterpret_cast<uint32_t*>(smem_raw);
   uint32_t* idx = keys + kTieCap;
@@ -140,15 +144,14 @@ __global__ void __launch_bounds__(kTieThreads)
           const uint32_t k1 = keys[e1];
           for (uint32_t e2 = e1 + 1; e2 < hi; ++e2) {
             if (keys[e2] != k1) continue;
-            // column j holds the same value at rows a and b: flag
-            // (pair {tile(j), tile(a)}, chunk(b)) and the mirror
+            // column j holds the same value at rows a and b: mark k = b
+            // in pair {tile(j), tile(a)} and k = a in pair {tile(j), tile(b)}
             const int a = (int)idx[e1], bb = (int)idx[e2];
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int x = h ? bb : a, k = h ? a : bb;
               const int tx = x / kTile, P = min(tj, tx), Q = max(tj, tx);
-              const int ch = k / kSymBK;
-              atomicOr(&flags[((size_t)P * nb + Q) * nw + (ch >> 5)], 1u << (ch & 31));
+              atomicOr(&masks[pair_index(P, Q, nb) * nch + k / kSymBK], 1u << (k % kSymBK));
             }
           }
         }
@@ -156,6 +159,18 @@ __global__ void __launch_bounds__(kTieThreads)
       __syncthreads();
     }
   }
+}
+
+// Number of marked (pair, k) steps, for the cost model of the launcher.
+__global__ void tie_count_kernel(const uint32_t* __restrict__ masks, size_t words,
+                                 unsigned long long* __restrict__ out) {
+  unsigned long long c = 0;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < words;
+       i += (size_t)gridDim.x * blockDim.x)
+    c += __popc(masks[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
 }
 
 // Shared step: one min + one compare per (r, c) pair, two accumulates.
@@ -253,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint32_t done_cnt[kSymStages];
   const int tid = threadIdx.x;
   const int n = args.n, ld = args.ld;
-  const int nch = (n + kSymBK - 1) / kSymBK;
+  const int nch = args.nch;
   const int G = gridDim.x, g = blockIdx.x;
   const int first = args.tile_begin + g;
   const int R = first < args.tile_end ? (args.tile_end - 1 - first) / G + 1 : 0;
@@ -299,8 +314,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int2 tp = args.tiles[first + ri * G];
     const int r0 = tp.x * kTile, c0 = tp.y * kTile;
     const bool diag = tp.x == tp.y;
-    const uint32_t* fl = args.flags + ((size_t)tp.x * args.nb + tp.y) * args.nw;
-    const bool all_flagged = (__ldg(args.tile_flags + tp.x) | __ldg(args.tile_flags + tp.y)) != 0u;
+    const uint32_t* mk = args.masks + pair_index(tp.x, tp.y, args.nb) * nch;
+    const bool all_marked = (__ldg(args.tile_flags + tp.x) | __ldg(args.tile_flags + tp.y)) != 0u;
     float2 thr[8][4], acc[8][4], act[8][4];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -328,13 +343,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float* sv = reinterpret_cast<const float*>(st + 3 * kSymBox);
       const int k0 = ch * kSymBK;
       const int kmax = min(kSymBK, n - k0);
-      const bool flagged = all_flagged || ((__ldg(fl + (ch >> 5)) >> (ch & 31)) & 1u);
-      if (!flagged && kmax == kSymBK) {
+      const uint32_t m = all_marked ? 0xffffffffu : __ldg(mk + ch);
+      if (m == 0u && kmax == kSymBK) {
 #pragma unroll 2
         for (int kk = 0; kk < kSymBK; ++kk) sym_step(sa, sb, sw, sv, kk, ty, tx, thr, acc, act);
       } else {
-        for (int kk = 0; kk < kmax; ++kk)
-          sym_step_exact(sa, sb, sw, sv, kk, k0 + kk, ty, tx, r0, c0, thr, acc, act);
+        for (int kk = 0; kk < kmax; ++kk) {
+          if ((m >> kk) & 1u)
+            sym_step_exact(sa, sb, sw, sv, kk, k0 + kk, ty, tx, r0, c0, thr, acc, act);
+          else
+            sym_step(sa, sb, sw, sv, kk, ty, tx, thr, acc, act);
+        }
       }
       __syncwarp();
       if (lane == 0) {
