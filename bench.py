@@ -265,9 +265,9 @@ def time_engine_steps(engine, runner, D, steps: int, warmup: int, dist_on: bool)
         e[2].record(stream)
         runner.exchange_focus()
         e[3].record(stream)
-        engine.cohesion(*p.cohesion_rows)
+        runner.cohesion()
         e[4].record(stream)
-        runner.gather_cohesion()
+        runner.assemble_cohesion()
         e[5].record(stream)
     end.record(stream)
     torch.cuda.synchronize()
@@ -337,8 +337,8 @@ def e2e_sharded(engine, runner, D_dev, steps: int, warmup: int, rank: int):
         p = runner.plan
         engine.focus_counts(*p.focus_share)
         runner.exchange_focus()
-        engine.cohesion(*p.cohesion_rows)
-        runner.gather_cohesion()
+        runner.cohesion()
+        runner.assemble_cohesion()
         if rank == 0:
             u_h.copy_(engine.U)
             c_h.copy_(engine.C)
@@ -385,6 +385,7 @@ def secondary_configs(steps: int) -> dict:
             "n": n, "algorithm": alg, "triplets_per_s": n ** 3 / step, "ms_per_step": step * 1e3,
             "focus_ms": foc * 1e3, "cohesion_ms": coh * 1e3,
             "issue_roofline_frac_step": w / (step * peak), "exact_path": eng.exact_path,
+            "cohesion_kernel": eng.info()["cohesion_kernel"],
         }
         del eng, D
         torch.cuda.empty_cache()
@@ -452,9 +453,10 @@ def main() -> None:
     step_ms_max = float(t[0])
     value = n ** 3 / (step_ms_max / 1e3)
 
-    # dominant kernel: pass 2 (cohesion) on this rank's rows
-    r0, r1 = runner.plan.cohesion_rows
-    coh_ops = 2.0 * (r1 - r0) * n * n  # 3 cmp + 1 FMA per (x<y, z) = 2 per ordered (x, y, z)
+    # dominant kernel: pass 2 (cohesion), this rank's share (1/world of the
+    # C entries: equal tile-pair or tile-row shares)
+    info = engine.info()
+    coh_ops = 2.0 * n ** 3 / world  # 3 cmp + 1 FMA per (x<y, z) = 2 per ordered (x, y, z)
     coh_s = phases["cohesion"] / 1e3
     achieved = coh_ops / coh_s
     part, parts = runner.plan.focus_share
@@ -474,10 +476,10 @@ def main() -> None:
         "dtype": "f32",
         "data": DATA_DESC.get(cfg.kind, "synthetic"),
         "config": {"workload": cfg.name, "n": n, "algorithm": "pairwise", "seed": args.seed,
-                   "parallelism": f"pair-tile sharding x{world}",
+                   "parallelism": f"tile-pair shares x{world} (pass 1 units, pass 2 pairs; NCCL all-reduce)",
                    "l2": "inputs larger than L2 (D = %.1f GiB > 126 MB)" % (n * n * 4 / 2 ** 30)},
         "roofline": {
-            "bound": "issue", "kernel": "pald_tile_kernel<cohesion>",
+            "bound": "issue", "kernel": info["cohesion_kernel"],
             "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Gop/s",
             "frac": achieved / peak,
             "traffic": load_traffic("cohesion", n),
@@ -491,6 +493,8 @@ def main() -> None:
         "gpu_launches": launches,
         "clocks": clk,
         "exact_path": engine.exact_path,
+        "tie_scan": {"exact_step_share": info["exact_step_share"],
+                     "note": "share of (tile pair, k) steps of the pair kernel on the per-element exact step"},
     }
 
     if rank == 0 and world == 1:

@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define PALD_GPU_ABI_VERSION 1
+#define PALD_GPU_ABI_VERSION 2
 
 /* Algorithm variant: blocked_pairwise / parallel_pairwise (blocked.hpp:368,
  * parallel.hpp:159) vs blocked_triplet / parallel_triplet (blocked.hpp:424,
@@ -131,7 +131,12 @@ int pald_gpu_cohesion_f32_device(const float* dD, uint64_t ldd, uint64_t n,
  * one share and SUMs the W buffers over ranks between the two calls
  * (integer counts < 2^24 in fp32: exact, order-independent).
  * Pass 2 (cohesion) writes C rows [row_begin, row_end) (tile aligned);
- * each row is one in-order sum, so row bands need no reduction. */
+ * each row is one in-order sum, so row bands need no reduction.
+ * cohesion_share(part, parts) instead zeroes C and computes share `part`
+ * of `parts` of the whole pass-2 work (tile pairs on the pair kernel, row
+ * bands otherwise): every C entry belongs to exactly one share and is one
+ * in-order sum there, so the elementwise SUM of the C buffers over the
+ * parts is the full C, bit-identical to one device. */
 typedef struct pald_gpu_plan pald_gpu_plan;
 
 typedef struct pald_gpu_buffers {
@@ -160,9 +165,29 @@ int pald_gpu_plan_focus_counts(pald_gpu_plan* plan, uint64_t part, uint64_t part
 int pald_gpu_plan_focus_finish(pald_gpu_plan* plan, void* stream);
 int pald_gpu_plan_cohesion(pald_gpu_plan* plan, uint64_t row_begin, uint64_t row_end,
                            void* stream);
+int pald_gpu_plan_cohesion_share(pald_gpu_plan* plan, uint64_t part, uint64_t parts,
+                                 void* stream);
 int pald_gpu_plan_buffers(const pald_gpu_plan* plan, pald_gpu_buffers* out);
 /* Kernel launches issued by this plan so far (evidence counter). */
 uint64_t pald_gpu_plan_launches(const pald_gpu_plan* plan);
+
+/* Which pass-2 kernel the last cohesion call ran, and the tie statistics
+ * of the loaded D that chose it. */
+enum {
+  PALD_GPU_KERNEL_NONE = 0,
+  PALD_GPU_KERNEL_TILE128 = 1, /* one-sided 128 x 128 output tiles */
+  PALD_GPU_KERNEL_TILE64 = 2,  /* one-sided 64 x 64 tiles (small n) */
+  PALD_GPU_KERNEL_PAIRS = 3    /* tile pairs: C[P][Q] and C[Q][P] together */
+};
+typedef struct pald_gpu_plan_info {
+  uint32_t struct_size;       /* sizeof(pald_gpu_plan_info) */
+  int32_t cohesion_kernel;    /* PALD_GPU_KERNEL_* of the last cohesion call */
+  int32_t exact_path;         /* 1: integer-key compare path */
+  int32_t pair_kernel_ready;  /* 1: tie scan done, the pair kernel may run */
+  double exact_step_share;    /* share of (pair, k) steps on the exact step */
+  uint64_t launches;
+} pald_gpu_plan_info;
+int pald_gpu_plan_get_info(const pald_gpu_plan* plan, pald_gpu_plan_info* out);
 
 /* Number of pass-1 work units of the plan. */
 uint64_t pald_gpu_focus_units(const pald_gpu_plan* plan);

@@ -32,8 +32,10 @@ EXPORTED_SYMBOLS = (
     "pald_gpu_plan_focus_counts",
     "pald_gpu_plan_focus_finish",
     "pald_gpu_plan_cohesion",
+    "pald_gpu_plan_cohesion_share",
     "pald_gpu_plan_buffers",
     "pald_gpu_plan_launches",
+    "pald_gpu_plan_get_info",
     "pald_gpu_focus_units",
     "pald_gpu_fill_diagonal",
     "pald_gpu_points_to_distances",
@@ -81,6 +83,20 @@ class Buffers(C.Structure):
     ]
 
 
+class PlanInfo(C.Structure):
+    _fields_ = [
+        ("struct_size", C.c_uint32),
+        ("cohesion_kernel", C.c_int32),
+        ("exact_path", C.c_int32),
+        ("pair_kernel_ready", C.c_int32),
+        ("exact_step_share", C.c_double),
+        ("launches", C.c_uint64),
+    ]
+
+
+KERNEL_NAMES = {0: "none", 1: "pald_tile_kernel<cohesion,128>", 2: "pald_tile_kernel<cohesion,64>",
+                3: "pald_sym_cohesion_kernel"}
+
 _lib = None
 
 
@@ -118,6 +134,8 @@ def load(path: Path | None = None) -> C.CDLL:
         "pald_gpu_plan_focus_counts": (i32, [vp, u64, u64, vp]),
         "pald_gpu_plan_focus_finish": (i32, [vp, vp]),
         "pald_gpu_plan_cohesion": (i32, [vp, u64, u64, vp]),
+        "pald_gpu_plan_cohesion_share": (i32, [vp, u64, u64, vp]),
+        "pald_gpu_plan_get_info": (i32, [vp, C.POINTER(PlanInfo)]),
         "pald_gpu_plan_buffers": (i32, [vp, C.POINTER(Buffers)]),
         "pald_gpu_plan_launches": (u64, [vp]),
         "pald_gpu_focus_units": (u64, [vp]),

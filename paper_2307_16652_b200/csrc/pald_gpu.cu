@@ -249,6 +249,7 @@ struct pald_gpu_plan {
   unsigned long long* sym_count = nullptr;
   int sym_nch = 0;
   double sym_marked = 0;                 // share of (pair, k) steps on the exact step
+  int last_kernel = PALD_GPU_KERNEL_NONE;
   bool sym_ready = false;                // tie scan done for the loaded D
   bool loaded = false;
   bool exact = false;
@@ -564,7 +565,10 @@ int plan_cohesion_impl(pald_gpu_plan* p, uint64_t row0, uint64_t row1, cudaStrea
   const uint64_t tiles128 = ((row1 - row0 + kTile - 1) / kTile) * p->nb;
   if (row0 == 0 && row1 == p->n && p->sym_ready && sym_preferred(p)) {
     const int rc = launch_sym(p, 0, (int)(p->nb * (p->nb + 1) / 2), s);
-    if (rc == PALD_GPU_OK) ++p->launches;
+    if (rc == PALD_GPU_OK) {
+      ++p->launches;
+      p->last_kernel = PALD_GPU_KERNEL_PAIRS;
+    }
     return rc;
   }
   static const int force_tile = [] {
@@ -573,8 +577,32 @@ int plan_cohesion_impl(pald_gpu_plan* p, uint64_t row0, uint64_t row1, cudaStrea
   }();
   const bool small = force_tile ? force_tile == 64 : tiles128 < (uint64_t)p->sms;
   const int rc = small ? launch_cohesion<64>(p, row0, row1, s) : launch_cohesion<kTile>(p, row0, row1, s);
-  if (rc == PALD_GPU_OK) ++p->launches;
+  if (rc == PALD_GPU_OK) {
+    ++p->launches;
+    p->last_kernel = small ? PALD_GPU_KERNEL_TILE64 : PALD_GPU_KERNEL_TILE128;
+  }
   return rc;
+}
+
+// Share `part` of `parts` of pass 2 into a zeroed C (see pald_gpu.h).
+int plan_cohesion_share_impl(pald_gpu_plan* p, uint64_t part, uint64_t parts, cudaStream_t s) {
+  if (!p->loaded) return set_error(PALD_GPU_ERR_VALIDATION, "plan has no distances loaded");
+  if (parts < 1 || part >= parts) return set_error(PALD_GPU_ERR_VALIDATION, "invalid share %llu of %llu",
+                                                   (unsigned long long)part, (unsigned long long)parts);
+  if (parts == 1) return plan_cohesion_impl(p, 0, p->n, s);
+  PALD_CUDA(cudaMemsetAsync(p->c, 0, p->n * p->ld * 4, s));
+  if (p->sym_ready && sym_preferred(p)) {
+    const uint64_t pairs = p->nb * (p->nb + 1) / 2;
+    const int rc = launch_sym(p, (int)(pairs * part / parts), (int)(pairs * (part + 1) / parts), s);
+    if (rc == PALD_GPU_OK) {
+      ++p->launches;
+      p->last_kernel = PALD_GPU_KERNEL_PAIRS;
+    }
+    return rc;
+  }
+  // Row bands of whole tile rows (every row costs the same).
+  const uint64_t t0 = p->nb * part / parts, t1 = p->nb * (part + 1) / parts;
+  return plan_cohesion_impl(p, std::min(p->n, t0 * kTile), std::min(p->n, t1 * kTile), s);
 }
 
 // One cached plan per device for the one-shot APIs.
@@ -695,6 +723,24 @@ int pald_gpu_plan_cohesion(pald_gpu_plan* p, uint64_t r0, uint64_t r1, void* str
   return plan_cohesion_impl(p, r0, r1, static_cast<cudaStream_t>(stream));
 }
 
+int pald_gpu_plan_cohesion_share(pald_gpu_plan* p, uint64_t part, uint64_t parts, void* stream) {
+  if (!p) return set_error(PALD_GPU_ERR_VALIDATION, "null plan");
+  DeviceGuard g(p->device);
+  return plan_cohesion_share_impl(p, part, parts, static_cast<cudaStream_t>(stream));
+}
+
+int pald_gpu_plan_get_info(const pald_gpu_plan* p, pald_gpu_plan_info* out) {
+  if (!p || !out) return set_error(PALD_GPU_ERR_VALIDATION, "null argument");
+  if (out->struct_size < sizeof(pald_gpu_plan_info))
+    return set_error(PALD_GPU_ERR_VALIDATION, "pald_gpu_plan_info.struct_size too small");
+  out->cohesion_kernel = p->last_kernel;
+  out->exact_path = p->exact ? 1 : 0;
+  out->pair_kernel_ready = p->sym_ready ? 1 : 0;
+  out->exact_step_share = p->sym_marked;
+  out->launches = p->launches;
+  return PALD_GPU_OK;
+}
+
 int pald_gpu_plan_buffers(const pald_gpu_plan* p, pald_gpu_buffers* out) {
   if (!p || !out) return set_error(PALD_GPU_ERR_VALIDATION, "null argument");
   out->U = p->u;
@@ -759,15 +805,25 @@ int pald_gpu_cohesion_f32(const float* D, uint64_t n, const pald_gpu_opts* o, in
   // Pass 2 runs in row bands; each band's C rows are copied to the host on
   // the copy stream while the next band computes, and U is copied during
   // pass 2 (it is final after pass 1). Only the last band's copy is exposed.
+  // On the pair kernel a band is a run of whole raster groups of the pair
+  // list: once groups [0, g] are done, tile rows [0, kGroupRows * (g + 1))
+  // are complete (a pair (P <= Q) writes rows P and Q, and P lies in its
+  // group). Bands alternate between two compute streams (they write
+  // disjoint entries) so that one band's tail overlaps the next band.
   constexpr int kBands = 8;
   cudaEvent_t ev[4 + kBands];
-  for (auto& e : ev) PALD_CUDA(cudaEventCreate(&e));
+  for (int i = 0; i < 4 + kBands; ++i)
+    PALD_CUDA(cudaEventCreateWithFlags(&ev[i], i < 4 ? cudaEventDefault : cudaEventDisableTiming));
+  cudaStream_t s2 = nullptr;
+  PALD_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
   struct EvGuard {
     cudaEvent_t* e;
+    cudaStream_t s2;
     ~EvGuard() {
       for (int i = 0; i < 4 + kBands; ++i) cudaEventDestroy(e[i]);
+      cudaStreamDestroy(s2);
     }
-  } eg{ev};
+  } eg{ev, s2};
   PALD_CUDA(cudaEventRecord(ev[0], s));
   if ((rc = pald_gpu_plan_load_host(p, D, s))) return rc;
   PALD_CUDA(cudaEventRecord(ev[1], s));
@@ -777,15 +833,41 @@ int pald_gpu_cohesion_f32(const float* D, uint64_t n, const pald_gpu_opts* o, in
     PALD_CUDA(cudaStreamWaitEvent(sc, ev[2], 0));
     PALD_CUDA(cudaMemcpy2DAsync(U_out, n * 4, p->u, p->ld * 4, n * 4, n, cudaMemcpyDeviceToHost, sc));
   }
-  const uint64_t rows_per_band = std::max<uint64_t>(kTile, (n / kBands + kTile - 1) / kTile * kTile);
-  int nb_used = 0;
-  for (uint64_t r0 = 0; r0 < n; r0 += rows_per_band, ++nb_used) {
-    const uint64_t r1 = std::min(n, r0 + rows_per_band);
-    if ((rc = plan_cohesion_impl(p, r0, r1, s))) return rc;
-    PALD_CUDA(cudaEventRecord(ev[4 + nb_used], s));
-    PALD_CUDA(cudaStreamWaitEvent(sc, ev[4 + nb_used], 0));
-    PALD_CUDA(cudaMemcpy2DAsync(C_out + r0 * n, n * 4, p->c + r0 * p->ld, p->ld * 4, n * 4, r1 - r0,
-                                cudaMemcpyDeviceToHost, sc));
+  if (p->sym_ready && sym_preferred(p)) {
+    PALD_CUDA(cudaStreamWaitEvent(s2, ev[2], 0));
+    const int nb = (int)p->nb;
+    const uint64_t pairs = p->nb * (p->nb + 1) / 2;
+    int t0 = 0, t1 = 0, band = 0, g_row0 = 0;
+    for (int g0 = 0; g0 < nb; g0 += kGroupRows) {
+      const int g1 = std::min(nb, g0 + kGroupRows);
+      for (int r = g0; r < g1; ++r) t1 += nb - r;  // pairs of the group
+      const uint64_t target = pairs * (uint64_t)(band + 1) / kBands;
+      if ((uint64_t)t1 < target && g1 < nb) continue;  // extend the band by one more group
+      cudaStream_t cs = (band & 1) ? s2 : s;
+      if ((rc = launch_sym(p, t0, t1, cs))) return rc;
+      ++p->launches;
+      PALD_CUDA(cudaEventRecord(ev[4 + band], cs));
+      PALD_CUDA(cudaStreamWaitEvent(sc, ev[4 + band], 0));
+      const uint64_t r0 = (uint64_t)g_row0 * kTile, r1 = std::min(n, (uint64_t)g1 * kTile);
+      PALD_CUDA(cudaMemcpy2DAsync(C_out + r0 * n, n * 4, p->c + r0 * p->ld, p->ld * 4, n * 4, r1 - r0,
+                                  cudaMemcpyDeviceToHost, sc));
+      t0 = t1;
+      g_row0 = g1;
+      ++band;
+    }
+    p->last_kernel = PALD_GPU_KERNEL_PAIRS;
+    for (int b = std::max(0, band - 2); b < band; ++b) PALD_CUDA(cudaStreamWaitEvent(s, ev[4 + b], 0));
+  } else {
+    const uint64_t rows_per_band = std::max<uint64_t>(kTile, (n / kBands + kTile - 1) / kTile * kTile);
+    int nb_used = 0;
+    for (uint64_t r0 = 0; r0 < n; r0 += rows_per_band, ++nb_used) {
+      const uint64_t r1 = std::min(n, r0 + rows_per_band);
+      if ((rc = plan_cohesion_impl(p, r0, r1, s))) return rc;
+      PALD_CUDA(cudaEventRecord(ev[4 + nb_used], s));
+      PALD_CUDA(cudaStreamWaitEvent(sc, ev[4 + nb_used], 0));
+      PALD_CUDA(cudaMemcpy2DAsync(C_out + r0 * n, n * 4, p->c + r0 * p->ld, p->ld * 4, n * 4, r1 - r0,
+                                  cudaMemcpyDeviceToHost, sc));
+    }
   }
   PALD_CUDA(cudaEventRecord(ev[3], s));
   PALD_CUDA(cudaStreamSynchronize(s));

@@ -9,12 +9,15 @@ Work decomposition:
     accumulates integer focus counts; one SUM all-reduce of the count
     buffer (exact: integers < 2^24 in fp32) and a local finish give every
     rank the full U and W = 1/U.
-  * Pass 2 (cohesion): C rows are split into equal bands of tile rows (each
-    row costs the same n^2 work). No reduction is needed: each C row is a
-    complete in-order sum on one rank (bit-identical to 1 GPU), and the
-    bands are all-gathered.
+  * Pass 2 (cohesion): the engine's cohesion_share(rank, world) computes an
+    equal share of the pass-2 work into a zeroed C -- contiguous ranges of
+    the tile-pair list on the pair kernel (each pair writes C[P][Q] and
+    C[Q][P]), tile-row bands on the one-sided kernel. Every C entry is one
+    complete in-order sum on exactly one rank (bit-identical to 1 GPU) and
+    0 on the others, so one SUM all-reduce of C assembles it exactly.
 The exchange steps are real data dependencies (W between the passes, C at
-the end); nothing else crosses ranks.
+the end); nothing else crosses ranks. ``cohesion_row_split`` / the row-band
+all-gather remain for engines without cohesion_share.
 """
 from __future__ import annotations
 
@@ -79,6 +82,12 @@ class ShardedRunner:
             dist.all_reduce(self.engine.full_W(), op=dist.ReduceOp.SUM, group=self.group)
         self.engine.focus_finish()
 
+    def reduce_cohesion(self) -> None:
+        """SUM of the per-rank C shares (disjoint supports: exact)."""
+        if self.world > 1:
+            e = self.engine
+            dist.all_reduce(e.row_block_C(0, e.n), op=dist.ReduceOp.SUM, group=self.group)
+
     def gather_cohesion(self) -> None:
         if self.world == 1:
             return
@@ -98,10 +107,26 @@ class ShardedRunner:
                 src = self._recv[k * p.band_rows * ld: k * p.band_rows * ld + (b - a) * ld]
                 e.row_block_C(a, b).copy_(src)
 
+    def cohesion(self, stream=None) -> None:
+        """This rank's share of pass 2."""
+        e = self.engine
+        if getattr(e, "cohesion_share", None) is not None:
+            e.cohesion_share(self.rank, self.world, stream=stream)
+        else:
+            e.cohesion(*self.plan.cohesion_rows, stream=stream)
+
+    def assemble_cohesion(self) -> None:
+        """Full C on every rank: SUM all-reduce of the shares (or the
+        row-band all-gather for engines without cohesion_share)."""
+        if getattr(self.engine, "cohesion_share", None) is not None:
+            self.reduce_cohesion()
+        else:
+            self.gather_cohesion()
+
     def step(self, D, stream=None) -> None:
         e, p = self.engine, self.plan
         e.load(D, stream)
         e.focus_counts(*p.focus_share, stream=stream)
         self.exchange_focus()
-        e.cohesion(*p.cohesion_rows, stream=stream)
-        self.gather_cohesion()
+        self.cohesion(stream=stream)
+        self.assemble_cohesion()

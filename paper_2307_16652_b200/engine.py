@@ -38,6 +38,8 @@ class Engine:
       focus()                 pass 1: U and W = 1/U
         = focus_counts(part, parts) + focus_finish()   (multi-GPU split)
       cohesion(r0, r1)        pass 2 over C rows [r0, r1)
+      cohesion_share(p, q)    pass 2, share p of q into a zeroed C (multi-GPU:
+                              the SUM of the q buffers is the full C)
     Views: ``U``, ``W``, ``C`` (n x n, strided by ld).
     """
 
@@ -141,6 +143,21 @@ class Engine:
             row_end = self.n
         _raise_for(self.lib.pald_gpu_plan_cohesion(self._plan, row_begin, row_end,
                                                    self._stream(stream)))
+
+    def cohesion_share(self, part: int = 0, parts: int = 1, stream=None) -> None:
+        """Pass 2, share `part` of `parts` (tile pairs or row bands) into a
+        zeroed C: every entry is computed by exactly one share."""
+        _raise_for(self.lib.pald_gpu_plan_cohesion_share(self._plan, part, parts,
+                                                         self._stream(stream)))
+
+    def info(self) -> dict:
+        """Pass-2 kernel of the last cohesion call and the tie statistics."""
+        i = _lib.PlanInfo()
+        i.struct_size = C.sizeof(_lib.PlanInfo)
+        _raise_for(self.lib.pald_gpu_plan_get_info(self._plan, C.byref(i)))
+        return {"cohesion_kernel": _lib.KERNEL_NAMES.get(i.cohesion_kernel, str(i.cohesion_kernel)),
+                "exact_path": bool(i.exact_path), "pair_kernel_ready": bool(i.pair_kernel_ready),
+                "exact_step_share": i.exact_step_share, "launches": int(i.launches)}
 
     def run(self, D: torch.Tensor, stream=None) -> None:
         self.load(D, stream)

@@ -14,17 +14,18 @@ ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 
-from helpers import int_upper  # noqa: E402
+from helpers import int_upper, random_upper  # noqa: E402
 from paper_2307_16652_b200.distributed import ShardedRunner  # noqa: E402
 from paper_2307_16652_b200.engine import Engine  # noqa: E402
 
 
 def main():
     n, alg = int(sys.argv[1]), sys.argv[2]
+    kind = sys.argv[3] if len(sys.argv) > 3 else "ties"
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
     torch.cuda.set_device(0)
-    D = torch.from_numpy(int_upper(n, 17)).cuda()
+    D = torch.from_numpy(int_upper(n, 17) if kind == "ties" else random_upper(n, 17)).cuda()
     ref = Engine(n, alg)
     ref.run(D)
     eng = Engine(n, alg)
@@ -37,7 +38,7 @@ def main():
     flags = torch.tensor([int(ok_u), int(ok_c)], dtype=torch.int32)
     dist.all_reduce(flags, op=dist.ReduceOp.MIN)
     if rank == 0:
-        print("shares", runner.plan.focus_share, "rows", runner.plan.cohesion_rows, "ok", flags.tolist())
+        print("shares", runner.plan.focus_share, "kernel", eng.info()["cohesion_kernel"], "ok", flags.tolist())
     dist.destroy_process_group()
     sys.exit(0 if flags.tolist() == [1, 1] else 1)
 

@@ -2,10 +2,12 @@
 
 The sharded driver (paper_2307_16652_b200.distributed) runs unchanged; the
 GPU engine is replaced by a CPU stand-in with the same staged interface
-(load / focus / cohesion / buffer views) whose arithmetic is the oracle's
-restatement, so what is tested here is exactly the decomposition and the
-exchange: tile-row split of pass 1, SUM all-reduce of U and W, row-band
-split of pass 2 computed from the *exchanged* W, and the C all-gather.
+(load / focus / cohesion / cohesion_share / buffer views) whose arithmetic
+is the oracle's restatement, so what is tested here is exactly the
+decomposition and the exchange: unit shares of pass 1, SUM all-reduce of
+the counts, tile-pair shares of pass 2 computed from the *exchanged* W and
+the SUM all-reduce of C (or, for engines without cohesion_share, row bands
+and the C all-gather).
 """
 import os
 import socket
@@ -87,27 +89,48 @@ class CpuEngine:
                 U[r, c] = U[c, r] = u
                 W[r, c] = W[c, r] = float(np.float32(1) / np.float32(u))
 
-    def cohesion(self, r0, r1, stream=None):
+    def _cohesion_row(self, r):
         d, n = self.d, self.n
         w = self.W.numpy()
         dn = np.nextafter(d, np.float32(np.inf))
-        C = self.C
+        acc = np.zeros(n, np.float32)
+        for k in range(n):
+            b = dn[k] if k < r else d[k]
+            m = np.minimum(d[r, k], b)
+            acc = np.where(d[r] < m, (acc + w[r, k]).astype(np.float32), acc)
+        return acc
+
+    def cohesion(self, r0, r1, stream=None):
         for r in range(r0, r1):
-            acc = np.zeros(n, np.float32)
-            for k in range(n):
-                b = dn[k] if k < r else d[k]
-                m = np.minimum(d[r, k], b)
-                acc = np.where(d[r] < m, (acc + w[r, k]).astype(np.float32), acc)
-            C[r] = torch.from_numpy(acc)
+            self.C[r] = torch.from_numpy(self._cohesion_row(r))
+
+    def cohesion_share(self, part, parts, stream=None):
+        """The GPU engine's pair-kernel decomposition: zero C, then compute
+        both C[P][Q] and C[Q][P] for the tile pairs (P <= Q) of share
+        `part` of the upper-triangular pair list."""
+        n, T, nb = self.n, self.tile, self.tiles_per_dim
+        self._c.zero_()
+        pairs = [(P, Q) for P in range(nb) for Q in range(P, nb)]
+        full = np.stack([self._cohesion_row(r) for r in range(n)])
+        C = self.C
+        for P, Q in pairs[len(pairs) * part // parts: len(pairs) * (part + 1) // parts]:
+            rp, rq = slice(P * T, min(n, P * T + T)), slice(Q * T, min(n, Q * T + T))
+            C[rp, rq] = torch.from_numpy(full[rp, rq])
+            C[rq, rp] = torch.from_numpy(full[rq, rp])
 
 
-def _worker(rank, world, port, n, tile, d, out):
+class CpuEngineRows(CpuEngine):
+    """Stand-in without cohesion_share: the row-band all-gather path."""
+    cohesion_share = None
+
+
+def _worker(rank, world, port, n, tile, d, out, rows=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2307_16652_b200.distributed import ShardedRunner
 
-    eng = CpuEngine(n, tile)
+    eng = CpuEngineRows(n, tile) if rows else CpuEngine(n, tile)
     runner = ShardedRunner(eng)
     runner.step(torch.from_numpy(d))
     out[rank] = (eng.U.numpy().copy(), eng.C.numpy().copy(), runner.plan)
@@ -123,12 +146,15 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("world,n,tile,kind", [(2, 21, 4, "ties"), (2, 16, 4, "rand"), (3, 23, 4, "ties")])
-def test_sharded_equals_single(oracle, world, n, tile, kind):
+@pytest.mark.parametrize("world,n,tile,kind,rows", [
+    (2, 21, 4, "ties", False), (2, 16, 4, "rand", False), (3, 23, 4, "ties", False),
+    (2, 21, 4, "ties", True), (3, 23, 4, "rand", True),
+])
+def test_sharded_equals_single(oracle, world, n, tile, kind, rows):
     d = int_upper(n, n) if kind == "ties" else random_upper(n, n)
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(world, _free_port(), n, tile, d, out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), n, tile, d, out, rows), nprocs=world, join=True)
     u_ref, c_ref = oracle.pairwise_f32(d)
     covered = []
     for r in range(world):

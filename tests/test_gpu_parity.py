@@ -230,3 +230,29 @@ def test_device_api_with_leading_dimensions(oracle):
     u_ref, c_ref = oracle.pairwise_f32(d)
     assert np.array_equal(e.U.cpu().numpy(), u_ref)
     assert np.array_equal(e.C.cpu().numpy().view(np.uint32), c_ref.view(np.uint32))
+
+
+@pytest.mark.parametrize("n,kind", [(2500, "rand"), (4200, "rand"), (2500, "fewties")])
+def test_host_api_pair_bands_match_one_sided(n, kind):
+    """The one-shot host API runs the pair kernel in bands of raster groups
+    on two streams with the D2H of finished row bands overlapped; it must
+    equal the one-sided kernel (engine row ranges) bit for bit, at sizes
+    with several raster groups (nb > 16)."""
+    import torch
+
+    from paper_2307_16652_b200.engine import Engine
+
+    d = random_upper(n, 11)
+    if kind == "fewties":
+        d = (np.round(d * 512) / 512).astype(np.float32)
+    u, c = run_gpu(d, "pairwise")
+    eng = Engine(n, "pairwise")
+    eng.load(torch.from_numpy(d).cuda())
+    eng.focus()
+    h = (n // 2) // 128 * 128
+    eng.cohesion(0, h)  # partial row ranges: the one-sided kernel
+    eng.cohesion(h, n)
+    torch.cuda.synchronize()
+    assert eng.info()["cohesion_kernel"].startswith("pald_tile_kernel")
+    assert np.array_equal(u, eng.U.cpu().numpy())
+    assert np.array_equal(c.view(np.uint32), eng.C.cpu().numpy().view(np.uint32))

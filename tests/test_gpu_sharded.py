@@ -1,5 +1,8 @@
 """The multi-rank path with the real GPU engine (torchrun, gloo, ranks
-sharing cuda:0): results bit-identical to one process."""
+sharing cuda:0): results bit-identical to one process. Tied integer data
+takes the one-sided kernel's row bands; random data with PALD_GPU_SYM=2
+the pair kernel's tile-pair shares."""
+import os
 import socket
 import subprocess
 import sys
@@ -19,10 +22,14 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("world,n,alg", [(2, 700, "pairwise"), (3, 513, "triplet"), (2, 300, "triplet")])
-def test_sharded_real_engine(world, n, alg):
+@pytest.mark.parametrize("world,n,alg,kind", [
+    (2, 700, "pairwise", "ties"), (3, 513, "triplet", "ties"), (2, 300, "triplet", "ties"),
+    (2, 700, "pairwise", "rand"), (3, 1000, "pairwise", "rand"),
+])
+def test_sharded_real_engine(world, n, alg, kind):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr=127.0.0.1", f"--master-port={_port()}", str(SCRIPT), str(n), alg]
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+           "--master-addr=127.0.0.1", f"--master-port={_port()}", str(SCRIPT), str(n), alg, kind]
+    env = dict(os.environ, PALD_GPU_SYM="2")
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     assert "ok [1, 1]" in out.stdout
