@@ -243,7 +243,7 @@ struct pald_gpu_plan {
   Stats* stats_host = nullptr;
   CUtensorMap tm_d, tm_dnu, tm_w;        // 128-wide boxes
   CUtensorMap tm_d64, tm_dnu64, tm_w64;  // 64-wide boxes (small-n cohesion tiles)
-  CUtensorMap tm_d32, tm_w32;            // 128 x 32 boxes (tile-pair cohesion)
+  CUtensorMap tm_d32, tm_dnu32, tm_w32;  // 128 x 32 boxes (tile-pair cohesion)
   uint32_t* sym_masks = nullptr;         // tie k-masks per (tile pair, 32-wide k chunk)
   uint32_t* sym_tile_flags = nullptr;
   unsigned long long* sym_count = nullptr;
@@ -336,10 +336,13 @@ int plan_alloc(pald_gpu_plan* p) {
   if ((rc = make_map(&p->tm_d64, p->ds, p->n, p->ld, 64))) return rc;
   if ((rc = make_map(&p->tm_dnu64, p->dnu, p->n, p->ld, 64))) return rc;
   if ((rc = make_map(&p->tm_w64, p->w, p->n, p->ld, 64))) return rc;
-  if (p->algorithm == PALD_GPU_PAIRWISE && p->policy == PALD_GPU_STRICT) {
+  if (p->policy == PALD_GPU_STRICT) {
     if ((rc = make_map(&p->tm_d32, p->ds, p->n, p->ld, kTile, kSymBK))) return rc;
+    if ((rc = make_map(&p->tm_dnu32, p->dnu, p->n, p->ld, kTile, kSymBK))) return rc;
     if ((rc = make_map(&p->tm_w32, p->w, p->n, p->ld, kTile, kSymBK))) return rc;
     p->sym_nch = (int)((p->n + kSymBK - 1) / kSymBK);
+  }
+  if (p->algorithm == PALD_GPU_PAIRWISE && p->policy == PALD_GPU_STRICT) {
     PALD_CUDA(cudaMalloc(&p->sym_masks, sym_mask_words(p) * sizeof(uint32_t)));
     PALD_CUDA(cudaMalloc(&p->sym_tile_flags, p->nb * sizeof(uint32_t)));
     PALD_CUDA(cudaMalloc(&p->sym_count, sizeof(unsigned long long)));
@@ -396,6 +399,14 @@ int plan_load_impl(pald_gpu_plan* p, const float* dD, uint64_t ldd, cudaStream_t
   PALD_CUDA(cudaMemsetAsync(p->u, 0, p->n * p->ld * 4, s));
   PALD_CUDA(cudaMemsetAsync(p->w, 0, p->n * p->ld * 4, s));
   p->sym_ready = false;
+  p->sym_marked = 0;
+  // Triplet: the pair kernel's shared indicator is exact without a scan.
+  // (Its per-element chunks, those inside the row or column tile, are the
+  // cost model's exact share.)
+  if (fast && p->algorithm == PALD_GPU_TRIPLET && sym_enabled()) {
+    p->sym_ready = true;
+    p->sym_marked = std::min(1.0, 2.0 * kTile / (double)p->n);
+  }
   if (fast && p->sym_masks && sym_enabled()) {
     // Duplicate scan of the columns of D for the tile-pair cohesion kernel.
     const size_t words = sym_mask_words(p);
@@ -528,13 +539,17 @@ int launch_sym(pald_gpu_plan* p, int t0, int t1, cudaStream_t s) {
   if (t1 <= t0) return PALD_GPU_OK;
   static bool attr_done[64] = {};
   if (!attr_done[p->device & 63]) {
-    PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
+    PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
+    PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
     attr_done[p->device & 63] = true;
   }
   SymArgs a{p->ds, p->c, p->focus_tiles, p->sym_masks, p->sym_tile_flags,
             (int)p->n, (int)p->ld, (int)p->nb, p->sym_nch, t0, t1};
   const int grid = std::min(t1 - t0, p->sms);
-  pald_sym_cohesion_kernel<<<grid, kThreads, kSymSmem, s>>>(p->tm_d32, p->tm_w32, a);
+  if (p->algorithm == PALD_GPU_TRIPLET)
+    pald_sym_cohesion_kernel<true><<<grid, kThreads, kSymSmem, s>>>(p->tm_d32, p->tm_dnu32, p->tm_w32, a);
+  else
+    pald_sym_cohesion_kernel<false><<<grid, kThreads, kSymSmem, s>>>(p->tm_d32, p->tm_dnu32, p->tm_w32, a);
   PALD_CUDA(cudaGetLastError());
   return PALD_GPU_OK;
 }

@@ -24,6 +24,12 @@
 //     positive off-diagonal distances), unless the nu'd zero is compared
 //     with T = 0, which is itself a duplicate of column c (d_rc = d_cc = 0)
 //     and flagged.
+//   * triplet (A' = nu(d_kr) iff k < c, B' = nu(d_kc) iff k < r; for the
+//     transposed output nu(d_kc) iff k < r and nu(d_kr) iff k < c): the
+//     same two transformed values, so the shared indicator is exact with
+//     no tie scan. Chunks wholly below a tile take the nu'd layout through
+//     the TMA map choice, chunks inside it the per-element step (like the
+//     one-sided kernel); the diagonal of C is forced to 0.
 //
 // Every C entry is still one fp32 sum over k ascending of the same terms as
 // the one-sided kernel (bit-identical to the reference); only the number of
@@ -253,14 +259,53 @@ __device__ __forceinline__ void sym_step_exact(const float* __restrict__ sa,
   }
 }
 
+// Triplet step for chunks inside the row (b_in) or column (a_in) tile:
+// per-element nu() of the shared indicator [T < min(A', B')].
+__device__ __forceinline__ void sym_step_tri_sel(const float* __restrict__ sa,
+                                                 const float* __restrict__ sb,
+                                                 const float* __restrict__ sw,
+                                                 const float* __restrict__ sv, int kk, int kg,
+                                                 int ty, int tx, int r0, int c0, bool a_in,
+                                                 bool b_in, const float2 (&thr)[8][4],
+                                                 float2 (&acc)[8][4], float2 (&act)[8][4]) {
+  float a[8], b[8], w[8], v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    a[i] = sa[kk * kTile + row_off<kTile>(ty, i)];
+    w[i] = sw[kk * kTile + row_off<kTile>(ty, i)];
+    b[i] = sb[kk * kTile + row_off<kTile>(tx, i)];
+    v[i] = sv[kk * kTile + row_off<kTile>(tx, i)];
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const bool nub = b_in && kg < r0 + row_off<kTile>(ty, i);
+#pragma unroll
+    for (int jp = 0; jp < 4; ++jp) {
+      float kv[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = 2 * jp + h;
+        const bool nua = a_in && kg < c0 + row_off<kTile>(tx, j);
+        const float m = fminf(nua ? nu_f(a[i]) : a[i], nub ? nu_f(b[j]) : b[j]);
+        kv[h] = __saturatef(__fmaf_rn(m, kCmpScale, h ? thr[i][jp].y : thr[i][jp].x));
+      }
+      const float2 k2 = make_float2(kv[0], kv[1]);
+      acc[i][jp] = __ffma2_rn(k2, make_float2(w[i], w[i]), acc[i][jp]);
+      act[i][jp] = __ffma2_rn(k2, make_float2(v[2 * jp], v[2 * jp + 1]), act[i][jp]);
+    }
+  }
+}
+
 // Persistent pass-2 kernel over the tile pairs [tile_begin, tile_end) of the
 // grouped upper-triangular order (P <= Q). CTA g takes pairs
 // tile_begin + g, + G, ...; each pair streams all k chunks through a
 // 3-stage TMA/mbarrier pipeline (four 32 x 128 boxes per stage) and writes
 // C[P rows][Q cols] and, for P < Q, C[Q rows][P cols]. Pairwise Strict
-// cohesion on the fast (scaled fp32) layout.
+// (TRI = false) or triplet cohesion on the fast (scaled fp32) layout.
+template <bool TRI>
 __global__ void __launch_bounds__(kThreads, 1)
     pald_sym_cohesion_kernel(const __grid_constant__ CUtensorMap tm_d,
+                             const __grid_constant__ CUtensorMap tm_dnu,
                              const __grid_constant__ CUtensorMap tm_w, const SymArgs args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -287,9 +332,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int2 tp = args.tiles[first + ri * G];
     const int r0 = tp.x * kTile, c0 = tp.y * kTile, k0 = ch * kSymBK;
     uint8_t* st = smem + s * kSymStageBytes;
+    const int k1 = min(k0 + kSymBK, n);
+    // triplet: a chunk wholly below the column (row) tile takes nu() on A (B)
+    const CUtensorMap* ma = (TRI && k1 <= c0) ? &tm_dnu : &tm_d;
+    const CUtensorMap* mb = (TRI && k1 <= r0) ? &tm_dnu : &tm_d;
     mbar_expect_tx(&full_bar[s], kSymStageBytes);
-    tma_load_2d(st, &tm_d, r0, k0, &full_bar[s]);
-    tma_load_2d(st + kSymBox, &tm_d, c0, k0, &full_bar[s]);
+    tma_load_2d(st, ma, r0, k0, &full_bar[s]);
+    tma_load_2d(st + kSymBox, mb, c0, k0, &full_bar[s]);
     tma_load_2d(st + 2 * kSymBox, &tm_w, r0, k0, &full_bar[s]);
     tma_load_2d(st + 3 * kSymBox, &tm_w, c0, k0, &full_bar[s]);
   };
@@ -314,8 +363,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int2 tp = args.tiles[first + ri * G];
     const int r0 = tp.x * kTile, c0 = tp.y * kTile;
     const bool diag = tp.x == tp.y;
-    const uint32_t* mk = args.masks + pair_index(tp.x, tp.y, args.nb) * nch;
-    const bool all_marked = (__ldg(args.tile_flags + tp.x) | __ldg(args.tile_flags + tp.y)) != 0u;
+    const uint32_t* mk = TRI ? nullptr : args.masks + pair_index(tp.x, tp.y, args.nb) * nch;
+    const bool all_marked =
+        !TRI && (__ldg(args.tile_flags + tp.x) | __ldg(args.tile_flags + tp.y)) != 0u;
     float2 thr[8][4], acc[8][4], act[8][4];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -343,6 +393,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float* sv = reinterpret_cast<const float*>(st + 3 * kSymBox);
       const int k0 = ch * kSymBK;
       const int kmax = min(kSymBK, n - k0);
+      if constexpr (TRI) {
+        const bool a_in = k0 >= c0 && k0 < c0 + kTile;
+        const bool b_in = k0 >= r0 && k0 < r0 + kTile;
+        if (!a_in && !b_in && kmax == kSymBK) {
+#pragma unroll 2
+          for (int kk = 0; kk < kSymBK; ++kk) sym_step(sa, sb, sw, sv, kk, ty, tx, thr, acc, act);
+        } else {
+          for (int kk = 0; kk < kmax; ++kk)
+            sym_step_tri_sel(sa, sb, sw, sv, kk, k0 + kk, ty, tx, r0, c0, a_in, b_in, thr, acc, act);
+        }
+      } else {
       const uint32_t m = all_marked ? 0xffffffffu : __ldg(mk + ch);
       if (m == 0u && kmax == kSymBK) {
 #pragma unroll 2
@@ -354,6 +415,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           else
             sym_step(sa, sb, sw, sv, kk, ty, tx, thr, acc, act);
         }
+      }
       }
       __syncwarp();
       if (lane == 0) {
@@ -368,6 +430,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < 8; ++i) {
       const int r = r0 + row_off<kTile>(ty, i);
       if (r >= n) continue;
+      if (TRI && diag) {  // the triplet leaves the diagonal of C at 0
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (c0 + row_off<kTile>(tx, j) != r) continue;
+          if (j & 1)
+            acc[i][j >> 1].y = 0.f;
+          else
+            acc[i][j >> 1].x = 0.f;
+        }
+      }
       float* crow = args.c + (size_t)r * ld;
       const int ca = c0 + tx * 4, cb = c0 + 64 + tx * 4;
       if (ca < n)

@@ -232,8 +232,10 @@ def test_device_api_with_leading_dimensions(oracle):
     assert np.array_equal(e.C.cpu().numpy().view(np.uint32), c_ref.view(np.uint32))
 
 
-@pytest.mark.parametrize("n,kind", [(2500, "rand"), (4200, "rand"), (2500, "fewties")])
-def test_host_api_pair_bands_match_one_sided(n, kind):
+@pytest.mark.parametrize("n,kind,alg", [(2500, "rand", "pairwise"), (4200, "rand", "pairwise"),
+                                        (2500, "fewties", "pairwise"), (2500, "rand", "triplet"),
+                                        (3000, "fewties", "triplet")])
+def test_host_api_pair_bands_match_one_sided(n, kind, alg):
     """The one-shot host API runs the pair kernel in bands of raster groups
     on two streams with the D2H of finished row bands overlapped; it must
     equal the one-sided kernel (engine row ranges) bit for bit, at sizes
@@ -245,8 +247,8 @@ def test_host_api_pair_bands_match_one_sided(n, kind):
     d = random_upper(n, 11)
     if kind == "fewties":
         d = (np.round(d * 512) / 512).astype(np.float32)
-    u, c = run_gpu(d, "pairwise")
-    eng = Engine(n, "pairwise")
+    u, c = run_gpu(d, alg)
+    eng = Engine(n, alg)
     eng.load(torch.from_numpy(d).cuda())
     eng.focus()
     h = (n // 2) // 128 * 128
