@@ -41,6 +41,13 @@
 
 namespace pald_gpu {
 
+#ifndef PALD_SYM_UNROLL  // unroll of the shared k loop (scheduling knob)
+#define PALD_SYM_UNROLL 2
+#endif
+#ifndef PALD_SYM_SCALAR_DIRECT  // 1: C[r][c] accumulated with scalar FFMA
+#define PALD_SYM_SCALAR_DIRECT 0
+#endif
+constexpr int kSymUnroll = PALD_SYM_UNROLL;
 constexpr int kSymBK = 32;                         // k chunk per stage
 constexpr int kSymStages = 3;
 constexpr int kSymBox = kSymBK * kTile * 4;        // one 32 x 128 fp32 box (16 KB)
@@ -211,7 +218,12 @@ __device__ __forceinline__ void sym_step(const float* __restrict__ sa, const flo
       const float m1 = fminf(a[i], b[2 * jp + 1]);
       const float2 kv = make_float2(__saturatef(__fmaf_rn(m0, kCmpScale, thr[i][jp].x)),
                                     __saturatef(__fmaf_rn(m1, kCmpScale, thr[i][jp].y)));
+#if PALD_SYM_SCALAR_DIRECT
+      acc[i][jp].x = __fmaf_rn(kv.x, w[i], acc[i][jp].x);
+      acc[i][jp].y = __fmaf_rn(kv.y, w[i], acc[i][jp].y);
+#else
       acc[i][jp] = __ffma2_rn(kv, make_float2(w[i], w[i]), acc[i][jp]);
+#endif
       act[i][jp] = __ffma2_rn(kv, make_float2(v[2 * jp], v[2 * jp + 1]), act[i][jp]);
     }
   }
@@ -397,7 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool a_in = k0 >= c0 && k0 < c0 + kTile;
         const bool b_in = k0 >= r0 && k0 < r0 + kTile;
         if (!a_in && !b_in && kmax == kSymBK) {
-#pragma unroll 2
+#pragma unroll kSymUnroll
           for (int kk = 0; kk < kSymBK; ++kk) sym_step(sa, sb, sw, sv, kk, ty, tx, thr, acc, act);
         } else {
           for (int kk = 0; kk < kmax; ++kk)
@@ -406,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else {
       const uint32_t m = all_marked ? 0xffffffffu : __ldg(mk + ch);
       if (m == 0u && kmax == kSymBK) {
-#pragma unroll 2
+#pragma unroll kSymUnroll
         for (int kk = 0; kk < kSymBK; ++kk) sym_step(sa, sb, sw, sv, kk, ty, tx, thr, acc, act);
       } else {
         for (int kk = 0; kk < kmax; ++kk) {

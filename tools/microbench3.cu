@@ -7,7 +7,7 @@
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); exit(1);} } while (0)
 __device__ unsigned long long g_cyc[4096];
 
-template <int TM, int TN, bool SYM>
+template <int TM, int TN, bool SYM, int NSET = 0>
 __global__ void __launch_bounds__(128 * 128 / (TM * TN), 1) tile_kernel(float* out, int reps, const float* thr_in) {
   constexpr int NT = 128 * 128 / (TM * TN), BK = 16;
   __shared__ __align__(16) float sA[BK][128];
@@ -60,8 +60,14 @@ __global__ void __launch_bounds__(128 * 128 / (TM * TN), 1) tile_kernel(float* o
 #pragma unroll
         for (int p = 0; p < TN / 2; ++p) {
           const float m0 = fminf(a[i], b[2 * p]), m1 = fminf(a[i], b[2 * p + 1]);
-          const float k0 = __saturatef(__fmaf_rn(m0, 0x1p20f, thr[i][p].x));
-          const float k1 = __saturatef(__fmaf_rn(m1, 0x1p20f, thr[i][p].y));
+          float k0, k1;
+          if (p < NSET) {
+            k0 = (m0 > thr[i][p].x) ? 1.f : 0.f;
+            k1 = (m1 > thr[i][p].y) ? 1.f : 0.f;
+          } else {
+            k0 = __saturatef(__fmaf_rn(m0, 0x1p20f, thr[i][p].x));
+            k1 = __saturatef(__fmaf_rn(m1, 0x1p20f, thr[i][p].y));
+          }
           const float2 kk = make_float2(k0, k1);
           acc[i][p] = __ffma2_rn(kk, make_float2(w[i], w[i]), acc[i][p]);
           if (SYM) act[i][p] = __ffma2_rn(kk, make_float2(v[2 * p], v[2 * p + 1]), act[i][p]);
@@ -81,7 +87,7 @@ __global__ void __launch_bounds__(128 * 128 / (TM * TN), 1) tile_kernel(float* o
   if (threadIdx.x == 0) g_cyc[blockIdx.x] = t1 - t0;
 }
 
-template <int TM, int TN, bool SYM>
+template <int TM, int TN, bool SYM, int NSET = 0>
 void run(const char* name, float* out, const float* thr, int nsm) {
   constexpr int NT = 128 * 128 / (TM * TN);
   const int reps = 1024;
@@ -89,7 +95,7 @@ void run(const char* name, float* out, const float* thr, int nsm) {
   float ms = 0;
   for (int rep = 0; rep < 3; ++rep) {
     cudaEventRecord(e0);
-    tile_kernel<TM, TN, SYM><<<nsm, NT>>>(out, reps, thr);
+    tile_kernel<TM, TN, SYM, NSET><<<nsm, NT>>>(out, reps, thr);
     cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
     CK(cudaGetLastError());
     cudaEventElapsedTime(&ms, e0, e1);
@@ -107,9 +113,12 @@ int main() {
   float* out; CK(cudaMalloc(&out, sizeof(float) * 4096 * 1024));
   float* thr; CK(cudaMalloc(&thr, sizeof(float) * 256 * 512)); CK(cudaMemset(thr, 0, sizeof(float) * 256 * 512));
   run<8, 8, false>("cohesion_8x8_onesided", out, thr, nsm);
+  run<8, 8, false, 1>("cohesion_8x8_onesided_fset1", out, thr, nsm);
+  run<8, 8, false, 2>("cohesion_8x8_onesided_fset2", out, thr, nsm);
   run<8, 8, true>("cohesion_8x8_sym", out, thr, nsm);
-  run<4, 8, true>("cohesion_4x8_sym", out, thr, nsm);
-  run<8, 4, true>("cohesion_8x4_sym", out, thr, nsm);
-  run<4, 4, true>("cohesion_4x4_sym", out, thr, nsm);
+  run<8, 8, true, 1>("cohesion_8x8_sym_fset1", out, thr, nsm);
+  run<8, 8, true, 2>("cohesion_8x8_sym_fset2", out, thr, nsm);
+  run<8, 8, true, 3>("cohesion_8x8_sym_fset3", out, thr, nsm);
+  run<8, 8, true, 4>("cohesion_8x8_sym_fset4", out, thr, nsm);
   return 0;
 }
