@@ -186,10 +186,10 @@ int make_map(CUtensorMap* map, const void* base, uint64_t n, uint64_t ld, int bo
 }
 
 template <int PASS, bool A_NU, bool B_NU, bool T_NU, bool ZD, bool FAST, bool SPLIT = false,
-          int TILE = kTile>
+          int TILE = kTile, bool LIST = false>
 int launch_tile(const CUtensorMap& md, const CUtensorMap& mnu, const CUtensorMap& mw,
                 const KernelArgs& a, int grid, cudaStream_t s) {
-  auto k = pald_tile_kernel<PASS, A_NU, B_NU, T_NU, ZD, FAST, SPLIT, TILE>;
+  auto k = pald_tile_kernel<PASS, A_NU, B_NU, T_NU, ZD, FAST, SPLIT, TILE, LIST>;
   static bool attr_done[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -256,6 +256,10 @@ struct pald_gpu_plan {
   bool focus_dirty = false;
   int sms = 148;
   int2* focus_tiles = nullptr;  // grouped upper-triangular tile order
+  std::vector<int2> pair_order;  // host copy of it (tile pairs of pass 2)
+  int2* tail64 = nullptr;        // 64-wide one-sided tiles of the last partial pair round
+  int tail64_count = 0;
+  int sym_main_pairs = 0;        // pairs of the full-range pair launch (rest: tail64)
   uint64_t launches = 0;
 
   ~pald_gpu_plan() {
@@ -270,6 +274,7 @@ struct pald_gpu_plan {
     cudaFree(stats);
     cudaFreeHost(stats_host);
     cudaFree(focus_tiles);
+    cudaFree(tail64);
     cudaFree(sym_masks);
     cudaFree(sym_tile_flags);
     cudaFree(sym_count);
@@ -327,6 +332,36 @@ int plan_alloc(pald_gpu_plan* p) {
         for (int r = g0; r < std::min(nb, g0 + kGroupRows) && r <= c; ++r) order.push_back(make_int2(r, c));
     PALD_CUDA(cudaMalloc(&p->focus_tiles, order.size() * sizeof(int2)));
     PALD_CUDA(cudaMemcpy(p->focus_tiles, order.data(), order.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    p->pair_order = order;
+  }
+  {
+    // Tail of the full-range pair launch: the last partial round of L < 148
+    // pairs keeps L SMs busy for a whole pair time. When it is cheaper, those
+    // pairs run instead as 64-wide one-sided tiles (2 CTAs/SM, ~0.36 of a
+    // pair time per round; identical in-order sums).
+    const std::vector<int2>& order = p->pair_order;
+    const int G = p->sms, pairs = (int)order.size(), L = pairs > G ? pairs % G : 0;
+    p->sym_main_pairs = pairs;
+    if (L > 0) {
+      std::vector<int2> t64;
+      const int nb64 = (int)((p->n + 63) / 64);
+      for (int i = pairs - L; i < pairs; ++i) {
+        const int P = order[i].x, Q = order[i].y;
+        for (int h = 0; h < (P == Q ? 1 : 2); ++h) {
+          const int R = h ? Q : P, Cc = h ? P : Q;  // direct tile (P, Q), then (Q, P)
+          for (int a = 0; a < 2; ++a)
+            for (int b = 0; b < 2; ++b)
+              if (2 * R + a < nb64 && 2 * Cc + b < nb64) t64.push_back(make_int2(2 * R + a, 2 * Cc + b));
+        }
+      }
+      const double rounds64 = std::ceil((double)t64.size() / (2.0 * G));
+      if (rounds64 * 0.52 / 1.44 < 1.0) {
+        PALD_CUDA(cudaMalloc(&p->tail64, t64.size() * sizeof(int2)));
+        PALD_CUDA(cudaMemcpy(p->tail64, t64.data(), t64.size() * sizeof(int2), cudaMemcpyHostToDevice));
+        p->tail64_count = (int)t64.size();
+        p->sym_main_pairs = pairs - L;
+      }
+    }
   }
   PALD_CUDA(cudaMallocHost(&p->stats_host, sizeof(Stats)));
   int rc;
@@ -354,6 +389,8 @@ int plan_alloc(pald_gpu_plan* p) {
 }
 
 int grid_rows(uint64_t n) { return (int)std::min<uint64_t>(n, 148ull * 16); }
+
+bool sym_wins(const pald_gpu_plan* p, double marked);
 
 int plan_load_impl(pald_gpu_plan* p, const float* dD, uint64_t ldd, cudaStream_t s) {
   const int n = (int)p->n;
@@ -400,14 +437,12 @@ int plan_load_impl(pald_gpu_plan* p, const float* dD, uint64_t ldd, cudaStream_t
   PALD_CUDA(cudaMemsetAsync(p->w, 0, p->n * p->ld * 4, s));
   p->sym_ready = false;
   p->sym_marked = 0;
-  // Triplet: the pair kernel's shared indicator is exact without a scan.
-  // (Its per-element chunks, those inside the row or column tile, are the
-  // cost model's exact share.)
-  if (fast && p->algorithm == PALD_GPU_TRIPLET && sym_enabled()) {
-    p->sym_ready = true;
-    p->sym_marked = std::min(1.0, 2.0 * kTile / (double)p->n);
-  }
-  if (fast && p->sym_masks && sym_enabled()) {
+  // Triplet: the pair kernel's shared indicator is exact without a scan
+  // (its per-element chunks, those inside the row or column tile, cost too
+  // little to enter the cost model: tools/time_n.py). Pairwise: the scan is
+  // skipped where the pair kernel cannot win even tie-free.
+  if (fast && p->algorithm == PALD_GPU_TRIPLET && sym_enabled() && sym_wins(p, 0.0)) p->sym_ready = true;
+  if (fast && p->sym_masks && sym_enabled() && sym_wins(p, 0.0)) {
     // Duplicate scan of the columns of D for the tile-pair cohesion kernel.
     const size_t words = sym_mask_words(p);
     PALD_CUDA(cudaMemsetAsync(p->sym_masks, 0, words * sizeof(uint32_t), s));
@@ -535,6 +570,18 @@ int launch_cohesion(pald_gpu_plan* p, uint64_t row0, uint64_t row1, cudaStream_t
 
 // Tile-pair cohesion over pairs [t0, t1) of the grouped upper-triangular
 // order; writes both C[P][Q] and C[Q][P] of each pair.
+// One-sided pass 2 over an explicit list of 64-wide tiles.
+int launch_cohesion_list64(pald_gpu_plan* p, const int2* list, int count, cudaStream_t s) {
+  const uint64_t nb64 = (p->n + 63) / 64;
+  const long long nch = (long long)((p->n + kBK - 1) / kBK);
+  KernelArgs a{p->ds, p->u, p->w, p->c, (int)p->n, (int)p->ld, (int)nb64, 0, (int)nb64, count, 0,
+               (long long)count * nch, list, kGroupRows};
+  const int grid = std::min(count, p->sms * ctas_per_sm(64));
+  const bool tri = p->algorithm == PALD_GPU_TRIPLET;
+  if (tri) return launch_tile<1, true, true, false, true, true, false, 64, true>(p->tm_d64, p->tm_dnu64, p->tm_w64, a, grid, s);
+  return launch_tile<1, false, true, false, false, true, false, 64, true>(p->tm_d64, p->tm_dnu64, p->tm_w64, a, grid, s);
+}
+
 int launch_sym(pald_gpu_plan* p, int t0, int t1, cudaStream_t s) {
   if (t1 <= t0) return PALD_GPU_OK;
   static bool attr_done[64] = {};
@@ -558,15 +605,17 @@ int launch_sym(pald_gpu_plan* p, int t0, int t1, cudaStream_t s) {
 // the outputs at ~1.44x the time of a one-sided tile (tools/microbench3.cu),
 // its exact k steps ~2.45x slower than shared ones (measured on all-tied
 // data); 64-wide one-sided tiles run 2 per SM at ~0.52 of a 128-tile time.
-bool sym_preferred(const pald_gpu_plan* p) {
+bool sym_wins(const pald_gpu_plan* p, double marked) {
   if (sym_mode() == 2) return true;
   const double sms = p->sms, nb = (double)p->nb, nb64 = (double)((p->n + 63) / 64);
-  const double pairs = nb * (nb + 1) / 2;
-  const double t_sym = std::ceil(pairs / sms) * 1.44 * (1.0 + 1.45 * p->sym_marked);
+  // full-range launch: main pair rounds + the 64-wide tail tiles (if any)
+  const double t_sym = std::ceil(p->sym_main_pairs / sms) * 1.44 * (1.0 + 1.45 * marked) +
+                       (p->tail64_count ? std::ceil(p->tail64_count / (2 * sms)) * 0.52 : 0.0);
   const double t_128 = std::ceil(nb * nb / sms);
   const double t_64 = std::ceil(nb64 * nb64 / (2 * sms)) * 0.52;
   return t_sym < std::min(t_128, t_64);
 }
+bool sym_preferred(const pald_gpu_plan* p) { return sym_wins(p, p->sym_marked); }
 
 int plan_cohesion_impl(pald_gpu_plan* p, uint64_t row0, uint64_t row1, cudaStream_t s) {
   if (!p->loaded) return set_error(PALD_GPU_ERR_VALIDATION, "plan has no distances loaded");
@@ -579,10 +628,14 @@ int plan_cohesion_impl(pald_gpu_plan* p, uint64_t row0, uint64_t row1, cudaStrea
   // identical: every C entry is the same in-order sum either way.
   const uint64_t tiles128 = ((row1 - row0 + kTile - 1) / kTile) * p->nb;
   if (row0 == 0 && row1 == p->n && p->sym_ready && sym_preferred(p)) {
-    const int rc = launch_sym(p, 0, (int)(p->nb * (p->nb + 1) / 2), s);
+    int rc = launch_sym(p, 0, p->sym_main_pairs, s);
     if (rc == PALD_GPU_OK) {
       ++p->launches;
       p->last_kernel = PALD_GPU_KERNEL_PAIRS;
+    }
+    if (rc == PALD_GPU_OK && p->tail64_count > 0) {
+      rc = launch_cohesion_list64(p, p->tail64, p->tail64_count, s);
+      if (rc == PALD_GPU_OK) ++p->launches;
     }
     return rc;
   }

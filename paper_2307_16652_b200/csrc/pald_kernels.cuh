@@ -93,7 +93,8 @@ struct KernelArgs {
   long long total_tiles; // cohesion: tiles covered by this launch
   long long unit_begin;  // work units [unit_begin, unit_end), u = tile*nchunks + chunk, tile
   long long unit_end;    // index in the launch's tile order (focus: the whole upper triangle)
-  const int2* focus_tiles;  // focus tile order: (tile row, tile col), grouped raster
+  const int2* focus_tiles;  // focus tile order: (tile row, tile col), grouped raster;
+                            // pass 2: optional explicit tile list (else the raster)
   int group_rows;           // cohesion raster group height (tile rows)
 };
 
@@ -340,9 +341,9 @@ __device__ __forceinline__ void tri_coords(int t, int nb, int& tr, int& tc) {
 //             all tile columns: groups of kGroupRows rows, column-major inside
 //             a group, so the ~148 concurrently resident tiles share a few
 //             row panels and column panels in L2.
-template <int PASS>
+template <int PASS, bool LIST = false>
 __device__ __forceinline__ void tile_coords(const KernelArgs& a, int t, int& tr, int& tc) {
-  if (PASS == 0) {
+  if (PASS == 0 || LIST) {  // pass 1 order, or an explicit pass-2 tile list
     const int2 v = a.focus_tiles[t];
     tr = v.x;
     tc = v.y;
@@ -429,7 +430,7 @@ __device__ __forceinline__ WorkSplit make_split(const KernelArgs& a, int C, int 
 // the last warp to finish with it (shared-memory arrival counter), so no
 // block-wide barrier sits in the main loop.
 template <int PASS, bool A_NU, bool B_NU, bool T_NU, bool ZERO_DIAG, bool FAST, bool SPLIT = false,
-          int TILE = kTile>
+          int TILE = kTile, bool LIST = false>
 __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE))
     pald_tile_kernel(const __grid_constant__ CUtensorMap tm_d,
                      const __grid_constant__ CUtensorMap tm_dnu,
@@ -486,7 +487,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE))
   constexpr int SB = stage_bytes(PASS, TILE);
   auto issue = [&](int t, int ch, int s) {
     int tr, tc;
-    tile_coords<PASS>(args, t, tr, tc);
+    tile_coords<PASS, LIST>(args, t, tr, tc);
     const int r0 = tr * TILE, c0 = tc * TILE;
     const int k0 = ch * kBK, k1 = min(k0 + kBK, n);
     // Uniform per-chunk transform choice: the whole chunk lies below the
@@ -521,7 +522,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE))
   for (int ri = 0; ri < R; ++ri) {
     const int t = run_t(ri), ch_begin = run_c0(ri), ch_end = run_c1(ri);
     int tr, tc;
-    tile_coords<PASS>(args, t, tr, tc);
+    tile_coords<PASS, LIST>(args, t, tr, tc);
     const int r0 = tr * TILE, c0 = tc * TILE;
     float2 thr[TT][TT / 2];
     float2 acc[TT][TT / 2];

@@ -234,12 +234,15 @@ def test_device_api_with_leading_dimensions(oracle):
 
 @pytest.mark.parametrize("n,kind,alg", [(2500, "rand", "pairwise"), (4200, "rand", "pairwise"),
                                         (2500, "fewties", "pairwise"), (2500, "rand", "triplet"),
-                                        (3000, "fewties", "triplet")])
+                                        (3000, "fewties", "triplet"), (2176, "rand", "pairwise"),
+                                        (2176, "rand", "triplet"), (8192, "rand", "pairwise")])
 def test_host_api_pair_bands_match_one_sided(n, kind, alg):
     """The one-shot host API runs the pair kernel in bands of raster groups
-    on two streams with the D2H of finished row bands overlapped; it must
-    equal the one-sided kernel (engine row ranges) bit for bit, at sizes
-    with several raster groups (nb > 16)."""
+    on two streams with the D2H of finished row bands overlapped, and the
+    engine's full-range pass 2 runs it with the last partial round as
+    64-wide one-sided tiles (n = 2176: 153 pairs = 148 + 5; n = 8192: 2080 =
+    14 x 148 + 8); both must equal the one-sided kernel (engine row ranges)
+    bit for bit, at sizes with several raster groups (nb > 16)."""
     import torch
 
     from paper_2307_16652_b200.engine import Engine
@@ -257,4 +260,11 @@ def test_host_api_pair_bands_match_one_sided(n, kind, alg):
     torch.cuda.synchronize()
     assert eng.info()["cohesion_kernel"].startswith("pald_tile_kernel")
     assert np.array_equal(u, eng.U.cpu().numpy())
-    assert np.array_equal(c.view(np.uint32), eng.C.cpu().numpy().view(np.uint32))
+    c_bands = eng.C.cpu().numpy()
+    assert np.array_equal(c.view(np.uint32), c_bands.view(np.uint32))
+    eng.C.zero_()
+    eng.cohesion()  # full range: pair kernel (+ 64-wide tail tiles)
+    torch.cuda.synchronize()
+    if kind == "rand" and alg == "pairwise":  # else the cost model may keep the one-sided kernel
+        assert eng.info()["cohesion_kernel"] == "pald_sym_cohesion_kernel"
+    assert np.array_equal(eng.C.cpu().numpy().view(np.uint32), c_bands.view(np.uint32))
