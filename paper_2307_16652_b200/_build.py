@@ -18,7 +18,9 @@ LIB_PATH = LIB_DIR / "libpald_gpu.so"
 INCLUDE = PKG_DIR.parent / "include"
 
 SOURCES = [CSRC / "pald_gpu.cu", CSRC / "pald_epilogue.cu", CSRC / "pald_io.cu"]
-DEPS = SOURCES + [CSRC / "pald_kernels.cuh", CSRC / "pald_internal.h", INCLUDE / "pald_gpu.h"]
+def deps() -> list[Path]:
+    """Every file the library is built from (sources, kernel headers, ABI)."""
+    return sorted([*CSRC.glob("*.cu"), *CSRC.glob("*.cuh"), *CSRC.glob("*.h"), *INCLUDE.glob("*.h")])
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -39,7 +41,7 @@ def needs_build() -> bool:
     if not LIB_PATH.exists():
         return True
     t = LIB_PATH.stat().st_mtime
-    return any(p.stat().st_mtime > t for p in DEPS)
+    return any(p.stat().st_mtime > t for p in deps())
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:

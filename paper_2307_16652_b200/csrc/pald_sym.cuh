@@ -71,7 +71,17 @@ struct SymArgs {
   int tile_begin, tile_end;   // share of the tile-pair list
 };
 
-__device__ __forceinline__ uint32_t tie_hash(uint32_t key) { return key * 0x9E3779B1u; }
+// Full-avalanche mix (murmur3 finalizer): the bucket takes the low bits and
+// the partition the high bits, and quantized inputs (values on a coarse
+// grid have zero low mantissa bits) must still spread over both.
+__device__ __forceinline__ uint32_t tie_hash(uint32_t key) {
+  key ^= key >> 16;
+  key *= 0x85ebca6bu;
+  key ^= key >> 13;
+  key *= 0xc2b2ae35u;
+  key ^= key >> 16;
+  return key;
+}
 // Index of tile pair (P, Q), P <= Q, in row-major upper-triangular order.
 __host__ __device__ __forceinline__ size_t pair_index(int P, int Q, int nb) {
   return (size_t)P * (2 * nb - P + 1) / 2 + (Q - P);
@@ -135,6 +145,9 @@ __global__ void __launch_bounds__(kTieThreads)
       if (tid == kTieThreads - 1 && base + s > (uint32_t)kTieCap) overflow = 1;
       __syncthreads();
       if (overflow) {  // too many values in this partition: flag the tile
+#ifdef PALD_TIE_DEBUG
+        if (tid == 0 && j < 4) printf("tie_scan col %d pass %d overflow\n", j, pass);
+#endif
         if (tid == 0) atomicOr(&tile_flags[tj], 1u);
         __syncthreads();
         break;
@@ -150,6 +163,9 @@ __global__ void __launch_bounds__(kTieThreads)
       for (int b = tid; b < kTieBuckets; b += kTieThreads) {
         const uint32_t hi = pos[b], lo = hi - cnt[b];
         if (hi - lo > (uint32_t)kTieMaxBucket) {
+#ifdef PALD_TIE_DEBUG
+          if (j < 4) printf("tie_scan col %d pass %d bucket %d size %u\n", j, pass, b, hi - lo);
+#endif
           atomicOr(&tile_flags[tj], 1u);
           continue;
         }
