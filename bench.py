@@ -259,9 +259,9 @@ def time_engine_steps(engine, runner, D, steps: int, warmup: int, dist_on: bool)
     for s in range(steps):
         e = ev[s]
         e[0].record(stream)
-        engine.load(D)
+        runner.load(D)
         e[1].record(stream)
-        engine.focus_counts(*p.focus_share)
+        runner.focus()
         e[2].record(stream)
         runner.exchange_focus()
         e[3].record(stream)
@@ -334,8 +334,9 @@ def e2e_sharded(engine, runner, D_dev, steps: int, warmup: int, rank: int):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         engine.load_host(d_h)
-        p = runner.plan
-        engine.focus_counts(*p.focus_share)
+        if runner.fused:
+            runner._sync_barrier()
+        runner.focus()
         runner.exchange_focus()
         runner.cohesion()
         runner.assemble_cohesion()
@@ -476,7 +477,9 @@ def main() -> None:
         "dtype": "f32",
         "data": DATA_DESC.get(cfg.kind, "synthetic"),
         "config": {"workload": cfg.name, "n": n, "algorithm": "pairwise", "seed": args.seed,
-                   "parallelism": f"tile-pair shares x{world} (pass 1 units, pass 2 pairs; NCCL all-reduce)",
+                   "parallelism": (f"tile-pair shares x{world}; exchange: "
+                                   + ("fused peer-memory stores over NVLink (CUDA IPC)" if runner.fused
+                                      else "NCCL all-reduces")),
                    "l2": "inputs larger than L2 (D = %.1f GiB > 126 MB)" % (n * n * 4 / 2 ** 30)},
         "roofline": {
             "bound": "issue", "kernel": info["cohesion_kernel"],

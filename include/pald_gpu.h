@@ -189,6 +189,32 @@ typedef struct pald_gpu_plan_info {
 } pald_gpu_plan_info;
 int pald_gpu_plan_get_info(const pald_gpu_plan* plan, pald_gpu_plan_info* out);
 
+/* ---- Fused multi-GPU exchange over peer memory (one node, NVLink) ------
+ * Replaces the two SUM all-reduces of the staged driver: pass-1 partial
+ * counts are added (red.global.add) straight into EVERY rank's W, and the
+ * pair kernel stores each C entry into every rank's C, so after the kernels
+ * finish every rank holds the full counts / the full C. Setup: each rank
+ * exports CUDA IPC handles of its W and C, the handles are all-gathered
+ * (any transport), and each rank attaches all of them (its own included,
+ * index = rank; world <= 8). Per step the caller orders the ranks with a
+ * host barrier after load (every W zeroed), after focus_counts_peers (all
+ * counts in) and after cohesion_share_peers (all of C written).
+ * cohesion_share_peers needs the pair kernel (PALD_GPU_ERR_UNSUPPORTED
+ * otherwise: fall back to cohesion_share + a SUM all-reduce). */
+typedef struct pald_gpu_ipc_handle {
+  unsigned char bytes[64]; /* cudaIpcMemHandle_t */
+} pald_gpu_ipc_handle;
+int pald_gpu_plan_export_buffers(const pald_gpu_plan* plan, pald_gpu_ipc_handle* w,
+                                 pald_gpu_ipc_handle* c);
+int pald_gpu_plan_attach_peers(pald_gpu_plan* plan, int world, int rank,
+                               const pald_gpu_ipc_handle* w_handles,
+                               const pald_gpu_ipc_handle* c_handles);
+int pald_gpu_plan_detach_peers(pald_gpu_plan* plan);
+int pald_gpu_plan_focus_counts_peers(pald_gpu_plan* plan, uint64_t part, uint64_t parts,
+                                     void* stream);
+int pald_gpu_plan_cohesion_share_peers(pald_gpu_plan* plan, uint64_t part, uint64_t parts,
+                                       void* stream);
+
 /* Number of pass-1 work units of the plan. */
 uint64_t pald_gpu_focus_units(const pald_gpu_plan* plan);
 

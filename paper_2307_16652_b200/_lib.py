@@ -36,6 +36,11 @@ EXPORTED_SYMBOLS = (
     "pald_gpu_plan_buffers",
     "pald_gpu_plan_launches",
     "pald_gpu_plan_get_info",
+    "pald_gpu_plan_export_buffers",
+    "pald_gpu_plan_attach_peers",
+    "pald_gpu_plan_detach_peers",
+    "pald_gpu_plan_focus_counts_peers",
+    "pald_gpu_plan_cohesion_share_peers",
     "pald_gpu_focus_units",
     "pald_gpu_fill_diagonal",
     "pald_gpu_points_to_distances",
@@ -94,6 +99,10 @@ class PlanInfo(C.Structure):
     ]
 
 
+class IpcHandle(C.Structure):
+    _fields_ = [("bytes", C.c_ubyte * 64)]
+
+
 KERNEL_NAMES = {0: "none", 1: "pald_tile_kernel<cohesion,128>", 2: "pald_tile_kernel<cohesion,64>",
                 3: "pald_sym_cohesion_kernel"}
 
@@ -136,6 +145,11 @@ def load(path: Path | None = None) -> C.CDLL:
         "pald_gpu_plan_cohesion": (i32, [vp, u64, u64, vp]),
         "pald_gpu_plan_cohesion_share": (i32, [vp, u64, u64, vp]),
         "pald_gpu_plan_get_info": (i32, [vp, C.POINTER(PlanInfo)]),
+        "pald_gpu_plan_export_buffers": (i32, [vp, C.POINTER(IpcHandle), C.POINTER(IpcHandle)]),
+        "pald_gpu_plan_attach_peers": (i32, [vp, i32, i32, C.POINTER(IpcHandle), C.POINTER(IpcHandle)]),
+        "pald_gpu_plan_detach_peers": (i32, [vp]),
+        "pald_gpu_plan_focus_counts_peers": (i32, [vp, u64, u64, vp]),
+        "pald_gpu_plan_cohesion_share_peers": (i32, [vp, u64, u64, vp]),
         "pald_gpu_plan_buffers": (i32, [vp, C.POINTER(Buffers)]),
         "pald_gpu_plan_launches": (u64, [vp]),
         "pald_gpu_focus_units": (u64, [vp]),

@@ -186,10 +186,10 @@ int make_map(CUtensorMap* map, const void* base, uint64_t n, uint64_t ld, int bo
 }
 
 template <int PASS, bool A_NU, bool B_NU, bool T_NU, bool ZD, bool FAST, bool SPLIT = false,
-          int TILE = kTile, bool LIST = false>
+          int TILE = kTile, bool LIST = false, bool PEERS = false>
 int launch_tile(const CUtensorMap& md, const CUtensorMap& mnu, const CUtensorMap& mw,
                 const KernelArgs& a, int grid, cudaStream_t s) {
-  auto k = pald_tile_kernel<PASS, A_NU, B_NU, T_NU, ZD, FAST, SPLIT, TILE, LIST>;
+  auto k = pald_tile_kernel<PASS, A_NU, B_NU, T_NU, ZD, FAST, SPLIT, TILE, LIST, PEERS>;
   static bool attr_done[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -250,6 +250,10 @@ struct pald_gpu_plan {
   int sym_nch = 0;
   double sym_marked = 0;                 // share of (pair, k) steps on the exact step
   int last_kernel = PALD_GPU_KERNEL_NONE;
+  // Fused multi-GPU exchange: every rank's W and C mapped through CUDA IPC.
+  PeerBufs peer_w{}, peer_c{};
+  bool peer_mapped[kMaxPeers] = {};  // opened by this plan (to be closed)
+  int peer_rank = -1;
   bool sym_ready = false;                // tie scan done for the loaded D
   bool loaded = false;
   bool exact = false;
@@ -261,6 +265,18 @@ struct pald_gpu_plan {
   int tail64_count = 0;
   int sym_main_pairs = 0;        // pairs of the full-range pair launch (rest: tail64)
   uint64_t launches = 0;
+
+  void close_peers() {
+    for (int q = 0; q < peer_w.count; ++q) {
+      if (!peer_mapped[q]) continue;
+      cudaIpcCloseMemHandle(peer_w.ptr[q]);
+      cudaIpcCloseMemHandle(peer_c.ptr[q]);
+      peer_mapped[q] = false;
+    }
+    peer_w = PeerBufs{};
+    peer_c = PeerBufs{};
+    peer_rank = -1;
+  }
 
   ~pald_gpu_plan() {
     int prev = 0;
@@ -275,6 +291,7 @@ struct pald_gpu_plan {
     cudaFreeHost(stats_host);
     cudaFree(focus_tiles);
     cudaFree(tail64);
+    close_peers();
     cudaFree(sym_masks);
     cudaFree(sym_tile_flags);
     cudaFree(sym_count);
@@ -490,10 +507,14 @@ uint64_t focus_units(const pald_gpu_plan* p) {
 
 // Pass 1, share `part` of `parts` equal shares of the work units: integer
 // focus counts accumulated into the W buffer.
-int plan_focus_counts_impl(pald_gpu_plan* p, uint64_t part, uint64_t parts, cudaStream_t s) {
+int plan_focus_counts_impl(pald_gpu_plan* p, uint64_t part, uint64_t parts, cudaStream_t s,
+                           bool peers = false) {
   if (!p->loaded) return set_error(PALD_GPU_ERR_VALIDATION, "plan has no distances loaded");
   if (parts < 1 || part >= parts) return set_error(PALD_GPU_ERR_VALIDATION, "invalid share %llu of %llu",
                                                    (unsigned long long)part, (unsigned long long)parts);
+  if (peers && p->peer_rank < 0) return set_error(PALD_GPU_ERR_VALIDATION, "no peers attached");
+  if (peers && p->focus_dirty)  // peers may already be adding into this W
+    return set_error(PALD_GPU_ERR_VALIDATION, "fused pass 1 needs a fresh load (W zeroed on every rank)");
   if (p->focus_dirty) {  // counts accumulate into W: start from zero again
     PALD_CUDA(cudaMemsetAsync(p->u, 0, p->n * p->ld * 4, s));
     PALD_CUDA(cudaMemsetAsync(p->w, 0, p->n * p->ld * 4, s));
@@ -504,13 +525,23 @@ int plan_focus_counts_impl(pald_gpu_plan* p, uint64_t part, uint64_t parts, cuda
   if (ue <= ub) return PALD_GPU_OK;
   const long long tiles = (long long)(p->nb * (p->nb + 1) / 2);
   KernelArgs a{p->ds, p->u, p->w, p->c, (int)p->n, (int)p->ld, (int)p->nb, 0, (int)p->nb, tiles, ub, ue,
-               p->focus_tiles, kGroupRows};
+               p->focus_tiles, kGroupRows, p->peer_w};
   const int grid = (int)std::min<long long>(ue - ub, p->sms);
   int rc;
   const bool tri = p->algorithm == PALD_GPU_TRIPLET;
   const bool split = p->policy == PALD_GPU_INCLUSIVE_SPLIT;
   const CUtensorMap &md = p->tm_d, &mn = p->tm_dnu, &mw = p->tm_w;
-  if (!p->exact) {
+  if (peers) {  // counts RED'd straight into every rank's W over NVLink
+    if (!p->exact) {
+      rc = tri     ? launch_tile<0, true, true, true, false, true, false, kTile, false, true>(md, mn, mw, a, grid, s)
+           : split ? launch_tile<0, false, false, true, false, true, false, kTile, false, true>(md, mn, mw, a, grid, s)
+                   : launch_tile<0, false, false, false, false, true, false, kTile, false, true>(md, mn, mw, a, grid, s);
+    } else {
+      rc = tri     ? launch_tile<0, true, true, true, false, false, false, kTile, false, true>(md, mn, mw, a, grid, s)
+           : split ? launch_tile<0, false, false, true, false, false, false, kTile, false, true>(md, mn, mw, a, grid, s)
+                   : launch_tile<0, false, false, false, false, false, false, kTile, false, true>(md, mn, mw, a, grid, s);
+    }
+  } else if (!p->exact) {
     rc = tri     ? launch_tile<0, true, true, true, false, true>(md, mn, mw, a, grid, s)
          : split ? launch_tile<0, false, false, true, false, true>(md, mn, mw, a, grid, s)  // <= : < nu(T)
                  : launch_tile<0, false, false, false, false, true>(md, mn, mw, a, grid, s);
@@ -582,21 +613,30 @@ int launch_cohesion_list64(pald_gpu_plan* p, const int2* list, int count, cudaSt
   return launch_tile<1, false, true, false, false, true, false, 64, true>(p->tm_d64, p->tm_dnu64, p->tm_w64, a, grid, s);
 }
 
-int launch_sym(pald_gpu_plan* p, int t0, int t1, cudaStream_t s) {
+int launch_sym(pald_gpu_plan* p, int t0, int t1, cudaStream_t s, bool peers = false) {
   if (t1 <= t0) return PALD_GPU_OK;
   static bool attr_done[64] = {};
   if (!attr_done[p->device & 63]) {
     PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
     PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
+    PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
+    PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
     attr_done[p->device & 63] = true;
   }
   SymArgs a{p->ds, p->c, p->focus_tiles, p->sym_masks, p->sym_tile_flags,
-            (int)p->n, (int)p->ld, (int)p->nb, p->sym_nch, t0, t1};
+            (int)p->n, (int)p->ld, (int)p->nb, p->sym_nch, t0, t1, p->peer_c};
   const int grid = std::min(t1 - t0, p->sms);
-  if (p->algorithm == PALD_GPU_TRIPLET)
+  const bool tri = p->algorithm == PALD_GPU_TRIPLET;
+  if (peers) {  // C entries stored straight into every rank's C over NVLink
+    if (tri)
+      pald_sym_cohesion_kernel<true, true><<<grid, kThreads, kSymSmem, s>>>(p->tm_d32, p->tm_dnu32, p->tm_w32, a);
+    else
+      pald_sym_cohesion_kernel<false, true><<<grid, kThreads, kSymSmem, s>>>(p->tm_d32, p->tm_dnu32, p->tm_w32, a);
+  } else if (tri) {
     pald_sym_cohesion_kernel<true><<<grid, kThreads, kSymSmem, s>>>(p->tm_d32, p->tm_dnu32, p->tm_w32, a);
-  else
+  } else {
     pald_sym_cohesion_kernel<false><<<grid, kThreads, kSymSmem, s>>>(p->tm_d32, p->tm_dnu32, p->tm_w32, a);
+  }
   PALD_CUDA(cudaGetLastError());
   return PALD_GPU_OK;
 }
@@ -700,6 +740,24 @@ int get_cached_plan(int dev, uint64_t n, const pald_gpu_opts* o, pald_gpu_plan**
   return PALD_GPU_OK;
 }
 
+// Fused pass-2 share: the pair kernel stores its entries into every rank's C.
+int plan_cohesion_share_peers_impl(pald_gpu_plan* p, uint64_t part, uint64_t parts, cudaStream_t s) {
+  if (!p->loaded) return set_error(PALD_GPU_ERR_VALIDATION, "plan has no distances loaded");
+  if (p->peer_rank < 0) return set_error(PALD_GPU_ERR_VALIDATION, "no peers attached");
+  if (parts < 1 || part >= parts) return set_error(PALD_GPU_ERR_VALIDATION, "invalid share %llu of %llu",
+                                                   (unsigned long long)part, (unsigned long long)parts);
+  if (!(p->sym_ready && sym_preferred(p)))
+    return set_error(PALD_GPU_ERR_UNSUPPORTED,
+                     "fused pass 2 runs on the pair kernel only (use cohesion_share + a SUM all-reduce)");
+  const uint64_t pairs = p->nb * (p->nb + 1) / 2;
+  const int rc = launch_sym(p, (int)(pairs * part / parts), (int)(pairs * (part + 1) / parts), s, true);
+  if (rc == PALD_GPU_OK) {
+    ++p->launches;
+    p->last_kernel = PALD_GPU_KERNEL_PAIRS;
+  }
+  return rc;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -789,6 +847,72 @@ int pald_gpu_plan_cohesion(pald_gpu_plan* p, uint64_t r0, uint64_t r1, void* str
   if (!p) return set_error(PALD_GPU_ERR_VALIDATION, "null plan");
   DeviceGuard g(p->device);
   return plan_cohesion_impl(p, r0, r1, static_cast<cudaStream_t>(stream));
+}
+
+int pald_gpu_plan_export_buffers(const pald_gpu_plan* p, pald_gpu_ipc_handle* w, pald_gpu_ipc_handle* c) {
+  if (!p || !w || !c) return set_error(PALD_GPU_ERR_VALIDATION, "null argument");
+  static_assert(sizeof(pald_gpu_ipc_handle) == sizeof(cudaIpcMemHandle_t), "IPC handle size");
+  DeviceGuard g(p->device);
+  PALD_CUDA(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(w), p->w));
+  PALD_CUDA(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(c), p->c));
+  return PALD_GPU_OK;
+}
+
+int pald_gpu_plan_attach_peers(pald_gpu_plan* p, int world, int rank, const pald_gpu_ipc_handle* w_handles,
+                               const pald_gpu_ipc_handle* c_handles) {
+  if (!p || !w_handles || !c_handles) return set_error(PALD_GPU_ERR_VALIDATION, "null argument");
+  if (world < 1 || world > kMaxPeers || rank < 0 || rank >= world)
+    return set_error(PALD_GPU_ERR_VALIDATION, "peers: world %d / rank %d out of range (max %d)", world, rank,
+                     kMaxPeers);
+  DeviceGuard g(p->device);
+  p->close_peers();
+  for (int q = 0; q < world; ++q) {
+    if (q == rank) {
+      p->peer_w.ptr[q] = p->w;
+      p->peer_c.ptr[q] = p->c;
+      continue;
+    }
+    void *pw = nullptr, *pc = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&pw, *reinterpret_cast<const cudaIpcMemHandle_t*>(&w_handles[q]),
+                                         cudaIpcMemLazyEnablePeerAccess);
+    if (e == cudaSuccess) {
+      e = cudaIpcOpenMemHandle(&pc, *reinterpret_cast<const cudaIpcMemHandle_t*>(&c_handles[q]),
+                               cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) cudaIpcCloseMemHandle(pw);
+    }
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      p->peer_w.count = p->peer_c.count = q;  // close what is open
+      p->close_peers();
+      return set_error(PALD_GPU_ERR_COMM, "cudaIpcOpenMemHandle of rank %d: %s", q, cudaGetErrorString(e));
+    }
+    p->peer_w.ptr[q] = static_cast<float*>(pw);
+    p->peer_c.ptr[q] = static_cast<float*>(pc);
+    p->peer_mapped[q] = true;
+    p->peer_w.count = p->peer_c.count = q + 1;
+  }
+  p->peer_w.count = p->peer_c.count = world;
+  p->peer_rank = rank;
+  return PALD_GPU_OK;
+}
+
+int pald_gpu_plan_detach_peers(pald_gpu_plan* p) {
+  if (!p) return set_error(PALD_GPU_ERR_VALIDATION, "null plan");
+  DeviceGuard g(p->device);
+  p->close_peers();
+  return PALD_GPU_OK;
+}
+
+int pald_gpu_plan_focus_counts_peers(pald_gpu_plan* p, uint64_t part, uint64_t parts, void* stream) {
+  if (!p) return set_error(PALD_GPU_ERR_VALIDATION, "null plan");
+  DeviceGuard g(p->device);
+  return plan_focus_counts_impl(p, part, parts, static_cast<cudaStream_t>(stream), true);
+}
+
+int pald_gpu_plan_cohesion_share_peers(pald_gpu_plan* p, uint64_t part, uint64_t parts, void* stream) {
+  if (!p) return set_error(PALD_GPU_ERR_VALIDATION, "null plan");
+  DeviceGuard g(p->device);
+  return plan_cohesion_share_peers_impl(p, part, parts, static_cast<cudaStream_t>(stream));
 }
 
 int pald_gpu_plan_cohesion_share(pald_gpu_plan* p, uint64_t part, uint64_t parts, void* stream) {

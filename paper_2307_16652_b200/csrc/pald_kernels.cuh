@@ -80,6 +80,15 @@ __host__ __device__ constexpr int smem_bytes(int pass, int tile) {
   return stages_for(pass, tile) * stage_bytes(pass, tile) + 1024;
 }
 
+// Multi-GPU exchange over peer memory: the same buffer (W or C) of every
+// rank of one node, mapped into this process (CUDA IPC over NVLink; the
+// calling rank's own buffer included).
+constexpr int kMaxPeers = 8;
+struct PeerBufs {
+  float* ptr[kMaxPeers];
+  int count;
+};
+
 struct KernelArgs {
   const uint32_t* d;     // layout of D (scaled fp32 bits or integer keys), n x ld
   int32_t* u;            // focus sizes
@@ -96,6 +105,7 @@ struct KernelArgs {
   const int2* focus_tiles;  // focus tile order: (tile row, tile col), grouped raster;
                             // pass 2: optional explicit tile list (else the raster)
   int group_rows;           // cohesion raster group height (tile rows)
+  PeerBufs peers;           // PEERS kernels: pass-1 counts go to every rank's W
 };
 
 constexpr int kGroupRows = 16;  // tile rows per raster group (L2 reuse of the panels)
@@ -430,7 +440,7 @@ __device__ __forceinline__ WorkSplit make_split(const KernelArgs& a, int C, int 
 // the last warp to finish with it (shared-memory arrival counter), so no
 // block-wide barrier sits in the main loop.
 template <int PASS, bool A_NU, bool B_NU, bool T_NU, bool ZERO_DIAG, bool FAST, bool SPLIT = false,
-          int TILE = kTile, bool LIST = false>
+          int TILE = kTile, bool LIST = false, bool PEERS = false>
 __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE))
     pald_tile_kernel(const __grid_constant__ CUtensorMap tm_d,
                      const __grid_constant__ CUtensorMap tm_dnu,
@@ -588,7 +598,13 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE))
         for (int j = 0; j < TT; ++j) {
           const int c = c0 + row_off<TILE>(tx, j);
           const float v = (j & 1) ? acc[i][j >> 1].y : acc[i][j >> 1].x;
-          if (c < n) atomicAdd(args.w + (size_t)r * ld + c, v);  // RED.ADD.F32, exact
+          if constexpr (PEERS) {  // fused exchange: the partial count to every rank
+            if (c < n && v != 0.f)
+              for (int q = 0; q < args.peers.count; ++q)
+                atomicAdd(args.peers.ptr[q] + (size_t)r * ld + c, v);
+          } else {
+            if (c < n) atomicAdd(args.w + (size_t)r * ld + c, v);  // RED.ADD.F32, exact
+          }
         }
       }
     } else {

@@ -69,6 +69,7 @@ struct SymArgs {
   const uint32_t* tile_flags; // [nb]: every k of every pair of this tile is marked
   int n, ld, nb, nch;
   int tile_begin, tile_end;   // share of the tile-pair list
+  PeerBufs peers;             // PEERS: every C entry is stored to every rank's C
 };
 
 // Full-avalanche mix (murmur3 finalizer): the bucket takes the low bits and
@@ -324,13 +325,24 @@ __device__ __forceinline__ void sym_step_tri_sel(const float* __restrict__ sa,
   }
 }
 
+// C store of the pair kernel: the local buffer, or (PEERS) every rank's
+// buffer over NVLink, so that no collective is needed after pass 2.
+template <bool PEERS>
+__device__ __forceinline__ void store_c4(const SymArgs& a, size_t off, float4 v) {
+  if constexpr (PEERS) {
+    for (int q = 0; q < a.peers.count; ++q) *reinterpret_cast<float4*>(a.peers.ptr[q] + off) = v;
+  } else {
+    *reinterpret_cast<float4*>(a.c + off) = v;
+  }
+}
+
 // Persistent pass-2 kernel over the tile pairs [tile_begin, tile_end) of the
 // grouped upper-triangular order (P <= Q). CTA g takes pairs
 // tile_begin + g, + G, ...; each pair streams all k chunks through a
 // 3-stage TMA/mbarrier pipeline (four 32 x 128 boxes per stage) and writes
 // C[P rows][Q cols] and, for P < Q, C[Q rows][P cols]. Pairwise Strict
 // (TRI = false) or triplet cohesion on the fast (scaled fp32) layout.
-template <bool TRI>
+template <bool TRI, bool PEERS = false>
 __global__ void __launch_bounds__(kThreads, 1)
     pald_sym_cohesion_kernel(const __grid_constant__ CUtensorMap tm_d,
                              const __grid_constant__ CUtensorMap tm_dnu,
@@ -468,14 +480,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             acc[i][j >> 1].x = 0.f;
         }
       }
-      float* crow = args.c + (size_t)r * ld;
+      const size_t rowo = (size_t)r * ld;
       const int ca = c0 + tx * 4, cb = c0 + 64 + tx * 4;
       if (ca < n)
-        *reinterpret_cast<float4*>(crow + ca) =
-            make_float4(acc[i][0].x, acc[i][0].y, acc[i][1].x, acc[i][1].y);
+        store_c4<PEERS>(args, rowo + ca, make_float4(acc[i][0].x, acc[i][0].y, acc[i][1].x, acc[i][1].y));
       if (cb < n)
-        *reinterpret_cast<float4*>(crow + cb) =
-            make_float4(acc[i][2].x, acc[i][2].y, acc[i][3].x, acc[i][3].y);
+        store_c4<PEERS>(args, rowo + cb, make_float4(acc[i][2].x, acc[i][2].y, acc[i][3].x, acc[i][3].y));
     }
     // ---- C[c][r] (rows of Q, columns of P); the diagonal pair already
     // wrote every entry of its tile above.
@@ -484,23 +494,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; j < 8; ++j) {
         const int c = c0 + row_off<kTile>(tx, j);
         if (c >= n) continue;
-        float* crow = args.c + (size_t)c * ld;
+        const size_t rowo = (size_t)c * ld;
         const int ra = r0 + ty * 4, rb = r0 + 64 + ty * 4;
         const int jp = j >> 1;
         if ((j & 1) == 0) {
           if (ra < n)
-            *reinterpret_cast<float4*>(crow + ra) =
-                make_float4(act[0][jp].x, act[1][jp].x, act[2][jp].x, act[3][jp].x);
+            store_c4<PEERS>(args, rowo + ra, make_float4(act[0][jp].x, act[1][jp].x, act[2][jp].x, act[3][jp].x));
           if (rb < n)
-            *reinterpret_cast<float4*>(crow + rb) =
-                make_float4(act[4][jp].x, act[5][jp].x, act[6][jp].x, act[7][jp].x);
+            store_c4<PEERS>(args, rowo + rb, make_float4(act[4][jp].x, act[5][jp].x, act[6][jp].x, act[7][jp].x));
         } else {
           if (ra < n)
-            *reinterpret_cast<float4*>(crow + ra) =
-                make_float4(act[0][jp].y, act[1][jp].y, act[2][jp].y, act[3][jp].y);
+            store_c4<PEERS>(args, rowo + ra, make_float4(act[0][jp].y, act[1][jp].y, act[2][jp].y, act[3][jp].y));
           if (rb < n)
-            *reinterpret_cast<float4*>(crow + rb) =
-                make_float4(act[4][jp].y, act[5][jp].y, act[6][jp].y, act[7][jp].y);
+            store_c4<PEERS>(args, rowo + rb, make_float4(act[4][jp].y, act[5][jp].y, act[6][jp].y, act[7][jp].y));
         }
       }
     }

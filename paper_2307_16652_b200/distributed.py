@@ -16,7 +16,18 @@ Work decomposition:
     complete in-order sum on exactly one rank (bit-identical to 1 GPU) and
     0 on the others, so one SUM all-reduce of C assembles it exactly.
 The exchange steps are real data dependencies (W between the passes, C at
-the end); nothing else crosses ranks. ``cohesion_row_split`` / the row-band
+the end); nothing else crosses ranks.
+
+Fused mode (``fused=True``, the default for N > 1 when the engine supports
+it): the two all-reduces are replaced by the kernels themselves writing over
+NVLink into every rank's buffers (CUDA IPC mappings, include/pald_gpu.h):
+pass-1 partial counts are added into every rank's W and the pair kernel
+stores each C entry into every rank's C. The host orders the ranks with a
+barrier after load (all W zeroed), after pass 1 (all counts in) and after
+pass 2 (all of C written). If a rank cannot map its peers, every rank
+falls back to the collectives; if the pair kernel does not run for the
+loaded D (tie-heavy input, InclusiveSplit, exact path), pass 2 of that step
+uses cohesion_share + the all-reduce. ``cohesion_row_split`` / the row-band
 all-gather remain for engines without cohesion_share.
 """
 from __future__ import annotations
@@ -61,12 +72,18 @@ class ShardedRunner:
     interface -- the CPU tests use a gloo-backed stand-in).
     """
 
-    def __init__(self, engine, group=None):
+    def __init__(self, engine, group=None, fused: bool | None = None):
         self.engine = engine
         self.group = group
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.plan = make_shard_plan(engine.n, engine.tile, self.rank, self.world)
+        self.fused = False
+        self._fused_c = False  # this step's pass 2 ran fused
+        if fused is None:
+            fused = self.world > 1 and hasattr(engine, "attach_peers")
+        if fused and self.world > 1:
+            self.fused = self._attach_peers()
         ld = engine.ld
         self._even = all(r1 - r0 == self.plan.band_rows
                          for r0, r1 in cohesion_row_split(engine.n, engine.tile, self.world))
@@ -76,10 +93,58 @@ class ShardedRunner:
             self._send = torch.zeros(self.plan.band_rows * ld, dtype=torch.float32, device=dev)
             self._recv = torch.empty(self.world * self.plan.band_rows * ld, dtype=torch.float32, device=dev)
 
+    def _attach_peers(self) -> bool:
+        """Map every rank's W and C into this process; all ranks agree on
+        the outcome (any failure -> collectives everywhere)."""
+        ok = 1
+        try:
+            mine = self.engine.export_buffers()
+        except Exception:
+            mine, ok = (b"", b""), 0
+        handles = [None] * self.world
+        dist.all_gather_object(handles, mine, group=self.group)
+        if ok and all(h[0] for h in handles):
+            try:
+                self.engine.attach_peers(self.rank, [h[0] for h in handles], [h[1] for h in handles])
+            except Exception:
+                ok = 0
+        else:
+            ok = 0
+        flag = torch.tensor([ok], dtype=torch.int32, device=self._flag_device())
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
+        if int(flag.item()) == 0:
+            if ok:
+                self.engine.detach_peers()
+            return False
+        return True
+
+    def _flag_device(self):
+        backend = dist.get_backend(self.group)
+        return self.engine.C.device if backend == "nccl" else "cpu"
+
+    def _sync_barrier(self) -> None:
+        torch.cuda.current_stream().synchronize()
+        dist.barrier(group=self.group)
+
+    def load(self, D, stream=None) -> None:
+        self.engine.load(D, stream)
+        if self.fused:
+            self._sync_barrier()  # every rank's W zeroed before any rank adds into it
+
+    def focus(self, stream=None) -> None:
+        """This rank's share of pass 1 (counts into W, or into every W)."""
+        if self.fused:
+            self.engine.focus_counts_peers(*self.plan.focus_share, stream=stream)
+        else:
+            self.engine.focus_counts(*self.plan.focus_share, stream=stream)
+
     def exchange_focus(self) -> None:
         """SUM the integer focus counts over ranks, then finish locally."""
         if self.world > 1:
-            dist.all_reduce(self.engine.full_W(), op=dist.ReduceOp.SUM, group=self.group)
+            if self.fused:
+                self._sync_barrier()  # all ranks' counts are in every W
+            else:
+                dist.all_reduce(self.engine.full_W(), op=dist.ReduceOp.SUM, group=self.group)
         self.engine.focus_finish()
 
     def reduce_cohesion(self) -> None:
@@ -110,23 +175,33 @@ class ShardedRunner:
     def cohesion(self, stream=None) -> None:
         """This rank's share of pass 2."""
         e = self.engine
+        self._fused_c = False
+        if self.fused:
+            self._fused_c = e.cohesion_share_peers(self.rank, self.world, stream=stream)
+            if self._fused_c:
+                return
         if getattr(e, "cohesion_share", None) is not None:
             e.cohesion_share(self.rank, self.world, stream=stream)
         else:
             e.cohesion(*self.plan.cohesion_rows, stream=stream)
 
     def assemble_cohesion(self) -> None:
-        """Full C on every rank: SUM all-reduce of the shares (or the
-        row-band all-gather for engines without cohesion_share)."""
-        if getattr(self.engine, "cohesion_share", None) is not None:
+        """Full C on every rank: a barrier after the fused pass 2, else the
+        SUM all-reduce of the shares (or the row-band all-gather for engines
+        without cohesion_share)."""
+        if self.world == 1:
+            return
+        # every rank took the same branch: the pair-kernel choice depends on D only
+        if self._fused_c:
+            self._sync_barrier()
+        elif getattr(self.engine, "cohesion_share", None) is not None:
             self.reduce_cohesion()
         else:
             self.gather_cohesion()
 
     def step(self, D, stream=None) -> None:
-        e, p = self.engine, self.plan
-        e.load(D, stream)
-        e.focus_counts(*p.focus_share, stream=stream)
+        self.load(D, stream)
+        self.focus(stream=stream)
         self.exchange_focus()
         self.cohesion(stream=stream)
         self.assemble_cohesion()

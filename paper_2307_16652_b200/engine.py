@@ -150,6 +150,39 @@ class Engine:
         _raise_for(self.lib.pald_gpu_plan_cohesion_share(self._plan, part, parts,
                                                          self._stream(stream)))
 
+    # -- fused multi-GPU exchange over peer memory (include/pald_gpu.h) --
+    def export_buffers(self) -> tuple[bytes, bytes]:
+        """CUDA IPC handles of this plan's W and C (64 bytes each)."""
+        w, c = _lib.IpcHandle(), _lib.IpcHandle()
+        _raise_for(self.lib.pald_gpu_plan_export_buffers(self._plan, C.byref(w), C.byref(c)))
+        return bytes(w.bytes), bytes(c.bytes)
+
+    def attach_peers(self, rank: int, w_handles: list[bytes], c_handles: list[bytes]) -> None:
+        world = len(w_handles)
+        arr_t = _lib.IpcHandle * world
+        wa, ca = arr_t(), arr_t()
+        for q in range(world):
+            C.memmove(wa[q].bytes, w_handles[q], 64)
+            C.memmove(ca[q].bytes, c_handles[q], 64)
+        _raise_for(self.lib.pald_gpu_plan_attach_peers(self._plan, world, rank, wa, ca))
+
+    def detach_peers(self) -> None:
+        _raise_for(self.lib.pald_gpu_plan_detach_peers(self._plan))
+
+    def focus_counts_peers(self, part: int, parts: int, stream=None) -> None:
+        """Pass 1 share with its counts added into every attached rank's W."""
+        _raise_for(self.lib.pald_gpu_plan_focus_counts_peers(self._plan, part, parts,
+                                                             self._stream(stream)))
+
+    def cohesion_share_peers(self, part: int, parts: int, stream=None) -> bool:
+        """Pass 2 share stored into every attached rank's C; False when the
+        pair kernel does not run for this D (caller falls back)."""
+        rc = self.lib.pald_gpu_plan_cohesion_share_peers(self._plan, part, parts, self._stream(stream))
+        if rc == _lib.ERR_UNSUPPORTED:
+            return False
+        _raise_for(rc)
+        return True
+
     def info(self) -> dict:
         """Pass-2 kernel of the last cohesion call and the tie statistics."""
         i = _lib.PlanInfo()

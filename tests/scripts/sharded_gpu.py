@@ -22,6 +22,7 @@ from paper_2307_16652_b200.engine import Engine  # noqa: E402
 def main():
     n, alg = int(sys.argv[1]), sys.argv[2]
     kind = sys.argv[3] if len(sys.argv) > 3 else "ties"
+    mode = sys.argv[4] if len(sys.argv) > 4 else "collectives"
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
     torch.cuda.set_device(0)
@@ -29,7 +30,9 @@ def main():
     ref = Engine(n, alg)
     ref.run(D)
     eng = Engine(n, alg)
-    runner = ShardedRunner(eng)
+    runner = ShardedRunner(eng, fused=(mode == "fused"))
+    if mode == "fused":
+        assert runner.fused, "peer mapping failed"
     for _ in range(2):  # repeated steps reuse the plan
         runner.step(D)
     torch.cuda.synchronize()
@@ -38,7 +41,8 @@ def main():
     flags = torch.tensor([int(ok_u), int(ok_c)], dtype=torch.int32)
     dist.all_reduce(flags, op=dist.ReduceOp.MIN)
     if rank == 0:
-        print("shares", runner.plan.focus_share, "kernel", eng.info()["cohesion_kernel"], "ok", flags.tolist())
+        print("shares", runner.plan.focus_share, "kernel", eng.info()["cohesion_kernel"], "fused", runner.fused,
+              "fused_c", runner._fused_c, "ok", flags.tolist())
     dist.destroy_process_group()
     sys.exit(0 if flags.tolist() == [1, 1] else 1)
 

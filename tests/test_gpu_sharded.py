@@ -22,14 +22,25 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("world,n,alg,kind", [
-    (2, 700, "pairwise", "ties"), (3, 513, "triplet", "ties"), (2, 300, "triplet", "ties"),
-    (2, 700, "pairwise", "rand"), (3, 1000, "pairwise", "rand"),
+@pytest.mark.parametrize("world,n,alg,kind,mode", [
+    (2, 700, "pairwise", "ties", "collectives"), (3, 513, "triplet", "ties", "collectives"),
+    (2, 300, "triplet", "ties", "collectives"), (2, 700, "pairwise", "rand", "collectives"),
+    (3, 1000, "pairwise", "rand", "collectives"),
+    (2, 700, "pairwise", "rand", "fused"), (3, 1000, "pairwise", "rand", "fused"),
+    (2, 700, "pairwise", "ties", "fused"), (3, 513, "triplet", "rand", "fused"),
 ])
-def test_sharded_real_engine(world, n, alg, kind):
+def test_sharded_real_engine(world, n, alg, kind, mode):
+    """mode "fused": pass-1 counts and pass-2 entries written into every
+    rank's buffers through CUDA IPC mappings (the ranks' processes share
+    cuda:0 here; on a node they are NVLink peers). No kernel waits on another
+    rank: the ranks are ordered by host barriers between the kernels."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr=127.0.0.1", f"--master-port={_port()}", str(SCRIPT), str(n), alg, kind]
+           "--master-addr=127.0.0.1", f"--master-port={_port()}", str(SCRIPT), str(n), alg, kind, mode]
     env = dict(os.environ, PALD_GPU_SYM="2")
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     assert "ok [1, 1]" in out.stdout
+    if mode == "fused":
+        assert "fused True" in out.stdout
+        if kind == "rand":
+            assert "fused_c True" in out.stdout
