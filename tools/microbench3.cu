@@ -7,7 +7,7 @@
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); exit(1);} } while (0)
 __device__ unsigned long long g_cyc[4096];
 
-template <int TM, int TN, bool SYM, int NSET = 0>
+template <int TM, int TN, bool SYM, int NSET = 0, int PRED = 0>
 __global__ void __launch_bounds__(128 * 128 / (TM * TN), 1) tile_kernel(float* out, int reps, const float* thr_in) {
   constexpr int NT = 128 * 128 / (TM * TN), BK = 16;
   __shared__ __align__(16) float sA[BK][128];
@@ -60,6 +60,17 @@ __global__ void __launch_bounds__(128 * 128 / (TM * TN), 1) tile_kernel(float* o
 #pragma unroll
         for (int p = 0; p < TN / 2; ++p) {
           const float m0 = fminf(a[i], b[2 * p]), m1 = fminf(a[i], b[2 * p + 1]);
+          if (PRED) {
+            const bool p0 = m0 > thr[i][p].x, p1 = m1 > thr[i][p].y;
+            if (PRED == 1) {
+              if (p0) { acc[i][p].x += w[i]; act[i][p].x += v[2 * p]; }
+              if (p1) { acc[i][p].y += w[i]; act[i][p].y += v[2 * p + 1]; }
+            } else {
+              acc[i][p].x += p0 ? w[i] : 0.f; act[i][p].x += p0 ? v[2 * p] : 0.f;
+              acc[i][p].y += p1 ? w[i] : 0.f; act[i][p].y += p1 ? v[2 * p + 1] : 0.f;
+            }
+            continue;
+          }
           float k0, k1;
           if (p < NSET) {
             k0 = (m0 > thr[i][p].x) ? 1.f : 0.f;
@@ -87,7 +98,7 @@ __global__ void __launch_bounds__(128 * 128 / (TM * TN), 1) tile_kernel(float* o
   if (threadIdx.x == 0) g_cyc[blockIdx.x] = t1 - t0;
 }
 
-template <int TM, int TN, bool SYM, int NSET = 0>
+template <int TM, int TN, bool SYM, int NSET = 0, int PRED = 0>
 void run(const char* name, float* out, const float* thr, int nsm) {
   constexpr int NT = 128 * 128 / (TM * TN);
   const int reps = 1024;
@@ -95,7 +106,7 @@ void run(const char* name, float* out, const float* thr, int nsm) {
   float ms = 0;
   for (int rep = 0; rep < 3; ++rep) {
     cudaEventRecord(e0);
-    tile_kernel<TM, TN, SYM, NSET><<<nsm, NT>>>(out, reps, thr);
+    tile_kernel<TM, TN, SYM, NSET, PRED><<<nsm, NT>>>(out, reps, thr);
     cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
     CK(cudaGetLastError());
     cudaEventElapsedTime(&ms, e0, e1);
@@ -120,5 +131,7 @@ int main() {
   run<8, 8, true, 2>("cohesion_8x8_sym_fset2", out, thr, nsm);
   run<8, 8, true, 3>("cohesion_8x8_sym_fset3", out, thr, nsm);
   run<8, 8, true, 4>("cohesion_8x8_sym_fset4", out, thr, nsm);
+  run<8, 8, true, 0, 1>("cohesion_8x8_sym_pred_branch", out, thr, nsm);
+  run<8, 8, true, 0, 2>("cohesion_8x8_sym_pred_select", out, thr, nsm);
   return 0;
 }
