@@ -78,3 +78,13 @@ def test_argument_validation_before_device_work():
     assert lib.pald_gpu_cohesion_f32(d, 1, C.byref(o), u, c, None) == _lib.ERR_VALIDATION
     o.struct_size = 7
     assert lib.pald_gpu_cohesion_f32(d, 3, C.byref(o), u, c, None) == _lib.ERR_VALIDATION
+
+
+def test_build_tracks_every_csrc_file():
+    """A stale library must rebuild when any kernel header changes (the
+    pair-kernel header once escaped the staleness check)."""
+    from paper_2307_16652_b200 import _build
+
+    names = {p.name for p in _build.deps()}
+    for f in ("pald_gpu.cu", "pald_kernels.cuh", "pald_sym.cuh", "pald_internal.h", "pald_gpu.h"):
+        assert f in names, f
