@@ -53,6 +53,9 @@ constexpr int kTile = 128;      // pair-tile edge (rows and columns)
 #define PALD_KUNROLL 2
 #endif
 constexpr int kKUnroll = PALD_KUNROLL;
+#ifndef PALD_K_ORDER  // k-step instruction order: 0 rows outer, 1 column pairs outer
+#define PALD_K_ORDER 0
+#endif
 #ifndef PALD_COH_ACC  // cohesion accumulate: 0 = packed FFMA2 (default), 1 = scalar FFMA
 #define PALD_COH_ACC 0
 #endif
@@ -197,10 +200,17 @@ __device__ __forceinline__ void k_step(const float* __restrict__ sa, const float
     lds_vec<TILE>(sb + kk * TILE, tx, b);
     if (PASS == 1) lds_vec<TILE>(sw + kk * TILE, ty, w);
   }
+#if PALD_K_ORDER == 1
+#pragma unroll
+  for (int jp = 0; jp < TT / 2; ++jp) {
+#pragma unroll
+    for (int i = 0; i < TT; ++i) {
+#else
 #pragma unroll
   for (int i = 0; i < TT; ++i) {
 #pragma unroll
     for (int jp = 0; jp < TT / 2; ++jp) {
+#endif
       if (FAST) {
         const float m0 = fminf(a[i], b[2 * jp]);
         const float m1 = fminf(a[i], b[2 * jp + 1]);

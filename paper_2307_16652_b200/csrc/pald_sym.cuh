@@ -44,6 +44,9 @@ namespace pald_gpu {
 #ifndef PALD_SYM_UNROLL  // unroll of the shared k loop (scheduling knob)
 #define PALD_SYM_UNROLL 2
 #endif
+#ifndef PALD_SYM_ORDER  // shared-step instruction order: 0 row-major, 1 per-row batches, 2 column-pair outer
+#define PALD_SYM_ORDER 2
+#endif
 #ifndef PALD_SYM_SCALAR_DIRECT  // 1: C[r][c] accumulated with scalar FFMA
 #define PALD_SYM_SCALAR_DIRECT 0
 #endif
@@ -227,10 +230,37 @@ __device__ __forceinline__ void sym_step(const float* __restrict__ sa, const flo
     v[0] = v0.x; v[1] = v0.y; v[2] = v0.z; v[3] = v0.w;
     v[4] = v1.x; v[5] = v1.y; v[6] = v1.z; v[7] = v1.w;
   }
+#if PALD_SYM_ORDER == 1
+  // per row: the 8 mins, the 8 compares, then the two accumulate groups
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    float m[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) m[j] = fminf(a[i], b[j]);
+    float2 kv[4];
+#pragma unroll
+    for (int jp = 0; jp < 4; ++jp)
+      kv[jp] = make_float2(__saturatef(__fmaf_rn(m[2 * jp], kCmpScale, thr[i][jp].x)),
+                           __saturatef(__fmaf_rn(m[2 * jp + 1], kCmpScale, thr[i][jp].y)));
+#pragma unroll
+    for (int jp = 0; jp < 4; ++jp) acc[i][jp] = __ffma2_rn(kv[jp], make_float2(w[i], w[i]), acc[i][jp]);
+#pragma unroll
+    for (int jp = 0; jp < 4; ++jp)
+      act[i][jp] = __ffma2_rn(kv[jp], make_float2(v[2 * jp], v[2 * jp + 1]), act[i][jp]);
+  }
+  return;
+#endif
+#if PALD_SYM_ORDER == 2
+#pragma unroll
+  for (int jp = 0; jp < 4; ++jp) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+#else
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
 #pragma unroll
     for (int jp = 0; jp < 4; ++jp) {
+#endif
       const float m0 = fminf(a[i], b[2 * jp]);
       const float m1 = fminf(a[i], b[2 * jp + 1]);
       const float2 kv = make_float2(__saturatef(__fmaf_rn(m0, kCmpScale, thr[i][jp].x)),

@@ -7,7 +7,7 @@
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); exit(1);} } while (0)
 __device__ unsigned long long g_cyc[4096];
 
-template <int TM, int TN, bool SYM, int NSET = 0, int PRED = 0>
+template <int TM, int TN, bool SYM, int NSET = 0, int PRED = 0, int ORD = 0>
 __global__ void __launch_bounds__(128 * 128 / (TM * TN), 1) tile_kernel(float* out, int reps, const float* thr_in) {
   constexpr int NT = 128 * 128 / (TM * TN), BK = 16;
   __shared__ __align__(16) float sA[BK][128];
@@ -55,6 +55,38 @@ __global__ void __launch_bounds__(128 * 128 / (TM * TN), 1) tile_kernel(float* o
           v[h * 4 + 0] = vv.x; v[h * 4 + 1] = vv.y; v[h * 4 + 2] = vv.z; v[h * 4 + 3] = vv.w;
         }
       }
+      if (ORD == 1) {  // per row: all mins, then compares, then direct, then transposed
+#pragma unroll
+        for (int i = 0; i < TM; ++i) {
+          float m[TN];
+#pragma unroll
+          for (int j = 0; j < TN; ++j) m[j] = fminf(a[i], b[j]);
+          float2 kv[TN / 2];
+#pragma unroll
+          for (int p = 0; p < TN / 2; ++p)
+            kv[p] = make_float2(__saturatef(__fmaf_rn(m[2 * p], 0x1p20f, thr[i][p].x)),
+                                __saturatef(__fmaf_rn(m[2 * p + 1], 0x1p20f, thr[i][p].y)));
+#pragma unroll
+          for (int p = 0; p < TN / 2; ++p) acc[i][p] = __ffma2_rn(kv[p], make_float2(w[i], w[i]), acc[i][p]);
+#pragma unroll
+          for (int p = 0; p < TN / 2; ++p)
+            act[i][p] = __ffma2_rn(kv[p], make_float2(v[2 * p], v[2 * p + 1]), act[i][p]);
+        }
+        continue;
+      }
+      if (ORD == 2) {  // column-pair outer, rows inner
+#pragma unroll
+        for (int p = 0; p < TN / 2; ++p)
+#pragma unroll
+          for (int i = 0; i < TM; ++i) {
+            const float m0 = fminf(a[i], b[2 * p]), m1 = fminf(a[i], b[2 * p + 1]);
+            const float2 kv = make_float2(__saturatef(__fmaf_rn(m0, 0x1p20f, thr[i][p].x)),
+                                          __saturatef(__fmaf_rn(m1, 0x1p20f, thr[i][p].y)));
+            acc[i][p] = __ffma2_rn(kv, make_float2(w[i], w[i]), acc[i][p]);
+            act[i][p] = __ffma2_rn(kv, make_float2(v[2 * p], v[2 * p + 1]), act[i][p]);
+          }
+        continue;
+      }
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
@@ -98,7 +130,7 @@ __global__ void __launch_bounds__(128 * 128 / (TM * TN), 1) tile_kernel(float* o
   if (threadIdx.x == 0) g_cyc[blockIdx.x] = t1 - t0;
 }
 
-template <int TM, int TN, bool SYM, int NSET = 0, int PRED = 0>
+template <int TM, int TN, bool SYM, int NSET = 0, int PRED = 0, int ORD = 0>
 void run(const char* name, float* out, const float* thr, int nsm) {
   constexpr int NT = 128 * 128 / (TM * TN);
   const int reps = 1024;
@@ -106,7 +138,7 @@ void run(const char* name, float* out, const float* thr, int nsm) {
   float ms = 0;
   for (int rep = 0; rep < 3; ++rep) {
     cudaEventRecord(e0);
-    tile_kernel<TM, TN, SYM, NSET, PRED><<<nsm, NT>>>(out, reps, thr);
+    tile_kernel<TM, TN, SYM, NSET, PRED, ORD><<<nsm, NT>>>(out, reps, thr);
     cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
     CK(cudaGetLastError());
     cudaEventElapsedTime(&ms, e0, e1);
@@ -132,6 +164,8 @@ int main() {
   run<8, 8, true, 3>("cohesion_8x8_sym_fset3", out, thr, nsm);
   run<8, 8, true, 4>("cohesion_8x8_sym_fset4", out, thr, nsm);
   run<8, 8, true, 0, 1>("cohesion_8x8_sym_pred_branch", out, thr, nsm);
+  run<8, 8, true, 0, 0, 1>("cohesion_8x8_sym_rowbatch", out, thr, nsm);
+  run<8, 8, true, 0, 0, 2>("cohesion_8x8_sym_colouter", out, thr, nsm);
   run<8, 8, true, 0, 2>("cohesion_8x8_sym_pred_select", out, thr, nsm);
   return 0;
 }
