@@ -42,7 +42,7 @@
 namespace pald_gpu {
 
 #ifndef PALD_SYM_UNROLL  // unroll of the shared k loop (scheduling knob)
-#define PALD_SYM_UNROLL 2
+#define PALD_SYM_UNROLL 1
 #endif
 #ifndef PALD_SYM_ORDER  // shared-step instruction order: 0 row-major, 1 per-row batches, 2 column-pair outer
 #define PALD_SYM_ORDER 2
