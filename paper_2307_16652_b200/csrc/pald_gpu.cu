@@ -247,6 +247,7 @@ struct pald_gpu_plan {
   uint32_t* sym_masks = nullptr;         // tie k-masks per (tile pair, 32-wide k chunk)
   uint32_t* sym_tile_flags = nullptr;
   unsigned long long* sym_count = nullptr;
+  unsigned int* round_bar = nullptr;     // round barrier counter of the pair kernel
   int sym_nch = 0;
   double sym_marked = 0;                 // share of (pair, k) steps on the exact step
   int last_kernel = PALD_GPU_KERNEL_NONE;
@@ -295,6 +296,7 @@ struct pald_gpu_plan {
     cudaFree(sym_masks);
     cudaFree(sym_tile_flags);
     cudaFree(sym_count);
+    cudaFree(round_bar);
     cudaSetDevice(prev);
   }
 };
@@ -393,6 +395,7 @@ int plan_alloc(pald_gpu_plan* p) {
     if ((rc = make_map(&p->tm_dnu32, p->dnu, p->n, p->ld, kTile, kSymBK))) return rc;
     if ((rc = make_map(&p->tm_w32, p->w, p->n, p->ld, kTile, kSymBK))) return rc;
     p->sym_nch = (int)((p->n + kSymBK - 1) / kSymBK);
+    PALD_CUDA(cudaMalloc(&p->round_bar, sizeof(unsigned int)));
   }
   if (p->algorithm == PALD_GPU_PAIRWISE && p->policy == PALD_GPU_STRICT) {
     PALD_CUDA(cudaMalloc(&p->sym_masks, sym_mask_words(p) * sizeof(uint32_t)));
@@ -613,7 +616,8 @@ int launch_cohesion_list64(pald_gpu_plan* p, const int2* list, int count, cudaSt
   return launch_tile<1, false, true, false, false, true, false, 64, true>(p->tm_d64, p->tm_dnu64, p->tm_w64, a, grid, s);
 }
 
-int launch_sym(pald_gpu_plan* p, int t0, int t1, cudaStream_t s, bool peers = false) {
+int launch_sym(pald_gpu_plan* p, int t0, int t1, cudaStream_t s, bool peers = false,
+               bool round_sync = true) {
   if (t1 <= t0) return PALD_GPU_OK;
   static bool attr_done[64] = {};
   if (!attr_done[p->device & 63]) {
@@ -621,22 +625,44 @@ int launch_sym(pald_gpu_plan* p, int t0, int t1, cudaStream_t s, bool peers = fa
     PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
     PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
     PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
+    PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
+    PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
+    PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
+    PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
     attr_done[p->device & 63] = true;
   }
-  SymArgs a{p->ds, p->c, p->focus_tiles, p->sym_masks, p->sym_tile_flags,
-            (int)p->n, (int)p->ld, (int)p->nb, p->sym_nch, t0, t1, p->peer_c};
   const int grid = std::min(t1 - t0, p->sms);
+  // Optional round barrier (cooperative launch: all CTAs co-resident, one
+  // per SM). It keeps the CTAs of a round at the same k, which cuts the
+  // kernel's DRAM reads 7x (1.39 -> 0.20 TB at n = 32768, L2 hit 42 -> 85 %)
+  // but costs 4 % of time waiting for each round's slowest CTA; the kernel
+  // is operand-bound, not memory-bound, so it is off by default
+  // (profiles/round_sync_r01.txt).
+  static const int sync_mode = [] {
+    const char* e = getenv("PALD_GPU_ROUND_SYNC");  // 1: round barrier on
+    return e ? atoi(e) : 0;
+  }();
+  const bool sync = round_sync && sync_mode && (t1 - t0) / grid >= 2;
+  if (sync) PALD_CUDA(cudaMemsetAsync(p->round_bar, 0, sizeof(unsigned int), s));
+  SymArgs a{p->ds, p->c, p->focus_tiles, p->sym_masks, p->sym_tile_flags,
+            (int)p->n, (int)p->ld, (int)p->nb, p->sym_nch, t0, t1, p->peer_c,
+            sync ? p->round_bar : nullptr};
   const bool tri = p->algorithm == PALD_GPU_TRIPLET;
-  if (peers) {  // C entries stored straight into every rank's C over NVLink
-    if (tri)
-      pald_sym_cohesion_kernel<true, true><<<grid, kThreads, kSymSmem, s>>>(p->tm_d32, p->tm_dnu32, p->tm_w32, a);
-    else
-      pald_sym_cohesion_kernel<false, true><<<grid, kThreads, kSymSmem, s>>>(p->tm_d32, p->tm_dnu32, p->tm_w32, a);
-  } else if (tri) {
-    pald_sym_cohesion_kernel<true><<<grid, kThreads, kSymSmem, s>>>(p->tm_d32, p->tm_dnu32, p->tm_w32, a);
-  } else {
-    pald_sym_cohesion_kernel<false><<<grid, kThreads, kSymSmem, s>>>(p->tm_d32, p->tm_dnu32, p->tm_w32, a);
-  }
+  auto k = sync ? (peers ? (tri ? pald_sym_cohesion_kernel<true, true, true> : pald_sym_cohesion_kernel<false, true, true>)
+                        : (tri ? pald_sym_cohesion_kernel<true, false, true> : pald_sym_cohesion_kernel<false, false, true>))
+                : (peers ? (tri ? pald_sym_cohesion_kernel<true, true> : pald_sym_cohesion_kernel<false, true>)
+                         : (tri ? pald_sym_cohesion_kernel<true, false> : pald_sym_cohesion_kernel<false, false>));
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSymSmem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = sync ? 1 : 0;
+  PALD_CUDA(cudaLaunchKernelEx(&cfg, k, p->tm_d32, p->tm_dnu32, p->tm_w32, a));
   PALD_CUDA(cudaGetLastError());
   return PALD_GPU_OK;
 }
@@ -1036,7 +1062,8 @@ int pald_gpu_cohesion_f32(const float* D, uint64_t n, const pald_gpu_opts* o, in
       const uint64_t target = pairs * (uint64_t)(band + 1) / kBands;
       if ((uint64_t)t1 < target && g1 < nb) continue;  // extend the band by one more group
       cudaStream_t cs = (band & 1) ? s2 : s;
-      if ((rc = launch_sym(p, t0, t1, cs))) return rc;
+      // (bands run concurrently on two streams: no shared round barrier)
+      if ((rc = launch_sym(p, t0, t1, cs, false, false))) return rc;
       ++p->launches;
       PALD_CUDA(cudaEventRecord(ev[4 + band], cs));
       PALD_CUDA(cudaStreamWaitEvent(sc, ev[4 + band], 0));

@@ -73,6 +73,7 @@ struct SymArgs {
   int n, ld, nb, nch;
   int tile_begin, tile_end;   // share of the tile-pair list
   PeerBufs peers;             // PEERS: every C entry is stored to every rank's C
+  unsigned int* round_bar;    // SYNC kernels: all CTAs start each full round together
 };
 
 // Full-avalanche mix (murmur3 finalizer): the bucket takes the low bits and
@@ -372,7 +373,7 @@ __device__ __forceinline__ void store_c4(const SymArgs& a, size_t off, float4 v)
 // 3-stage TMA/mbarrier pipeline (four 32 x 128 boxes per stage) and writes
 // C[P rows][Q cols] and, for P < Q, C[Q rows][P cols]. Pairwise Strict
 // (TRI = false) or triplet cohesion on the fast (scaled fp32) layout.
-template <bool TRI, bool PEERS = false>
+template <bool TRI, bool PEERS = false, bool SYNC = false>
 __global__ void __launch_bounds__(kThreads, 1)
     pald_sym_cohesion_kernel(const __grid_constant__ CUtensorMap tm_d,
                              const __grid_constant__ CUtensorMap tm_dnu,
@@ -539,6 +540,25 @@ __global__ void __launch_bounds__(kThreads, 1)
             store_c4<PEERS>(args, rowo + rb, make_float4(act[4][jp].y, act[5][jp].y, act[6][jp].y, act[7][jp].y));
         }
       }
+    }
+    // Round barrier (cooperative launch): the CTAs of one round work on
+    // pairs that share row and column panels chunk by chunk; starting every
+    // full round together keeps them at the same k so that those panels
+    // are read from DRAM once per round, not once per CTA.
+    if (SYNC && ri + 1 < (args.tile_end - args.tile_begin) / G) {
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        atomicAdd(args.round_bar, 1u);
+        const unsigned int target = (unsigned int)(ri + 1) * (unsigned int)G;
+        while (true) {
+          unsigned int v;
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(args.round_bar) : "memory");
+          if (v >= target) break;
+          __nanosleep(200);
+        }
+      }
+      __syncthreads();
     }
   }
 }
