@@ -32,3 +32,13 @@ def test_pair_kernel_matches_one_sided(kind, n, alg):
         assert share == 1.0  # whole tiles marked
     elif kind == "grid" and alg == "pairwise":
         assert 0.0 < share < 0.5  # marked k mixed with shared steps
+
+
+def test_pair_kernel_size_sweep():
+    """Seeded sweep of sizes (ragged, below and above one wave of pairs,
+    with and without the 64-wide tail tiles), both algorithms."""
+    env = dict(os.environ, PALD_GPU_SYM="2")
+    script = Path(__file__).resolve().parent / "scripts" / "pair_sweep.py"
+    out = subprocess.run([sys.executable, str(script), "7"], env=env, capture_output=True, text=True,
+                         timeout=900)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-3000:]
