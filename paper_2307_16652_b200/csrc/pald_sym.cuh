@@ -19,11 +19,11 @@
 //     (tie_scan_kernel) marks every third point k that can meet such a tie
 //     in a tile pair (one 32-bit mask per (tile pair, 32-wide k chunk)); the
 //     marked k steps take the per-element exact step (two mins, the nu() of
-//     each output), all others the shared step. k in {r, c} needs no flag: the min then contains d_rr = 0 or
-//     d_cc = 0 and both indicators are 0 (T > 0: the fast path requires
-//     positive off-diagonal distances), unless the nu'd zero is compared
-//     with T = 0, which is itself a duplicate of column c (d_rc = d_cc = 0)
-//     and flagged.
+//     each output), all others the shared step. k in {r, c} needs no mark:
+//     the min then contains d_rr = 0 or d_cc = 0 and both indicators are 0
+//     (T > 0: the fast path requires positive off-diagonal distances),
+//     unless the nu'd zero is compared with T = 0, which is itself a
+//     duplicate of column c (d_rc = d_cc = 0) and marked.
 //   * triplet (A' = nu(d_kr) iff k < c, B' = nu(d_kc) iff k < r; for the
 //     transposed output nu(d_kc) iff k < r and nu(d_kr) iff k < c): the
 //     same two transformed values, so the shared indicator is exact with
@@ -33,8 +33,10 @@
 //
 // Every C entry is still one fp32 sum over k ascending of the same terms as
 // the one-sided kernel (bit-identical to the reference); only the number of
-// FMNMX / FFMA.SAT instructions per output halves (tools/microbench3.cu:
-// 49 vs 36 output combos per SM-cycle).
+// FMNMX / FFMA.SAT instructions per output halves: 4.75 instead of 7
+// register-operand reads per output combo, the resource that bounds these
+// loops (tools/microbench3.cu: 50 vs 36 output combos
+// per SM-cycle).
 #pragma once
 
 #include "pald_kernels.cuh"
