@@ -28,6 +28,7 @@ def _port():
     (3, 1000, "pairwise", "rand", "collectives"),
     (2, 700, "pairwise", "rand", "fused"), (3, 1000, "pairwise", "rand", "fused"),
     (2, 700, "pairwise", "ties", "fused"), (3, 513, "triplet", "rand", "fused"),
+    (4, 1500, "pairwise", "rand", "fused"),
 ])
 def test_sharded_real_engine(world, n, alg, kind, mode):
     """mode "fused": pass-1 counts and pass-2 entries written into every
