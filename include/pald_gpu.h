@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define PALD_GPU_ABI_VERSION 2
+#define PALD_GPU_ABI_VERSION 3
 
 /* Algorithm variant: blocked_pairwise / parallel_pairwise (blocked.hpp:368,
  * parallel.hpp:159) vs blocked_triplet / parallel_triplet (blocked.hpp:424,
@@ -186,6 +186,7 @@ typedef struct pald_gpu_plan_info {
   int32_t pair_kernel_ready;  /* 1: tie scan done, the pair kernel may run */
   double exact_step_share;    /* share of (pair, k) steps on the exact step */
   uint64_t launches;
+  int32_t rank_codes;         /* 1: pass 1 runs on per-row rank codes (ABI v3) */
 } pald_gpu_plan_info;
 int pald_gpu_plan_get_info(const pald_gpu_plan* plan, pald_gpu_plan_info* out);
 

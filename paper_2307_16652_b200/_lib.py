@@ -96,6 +96,7 @@ class PlanInfo(C.Structure):
         ("pair_kernel_ready", C.c_int32),
         ("exact_step_share", C.c_double),
         ("launches", C.c_uint64),
+        ("rank_codes", C.c_int32),
     ]
 
 

@@ -22,6 +22,7 @@
 #include "../../include/pald_gpu.h"
 #include "pald_internal.h"
 #include "pald_kernels.cuh"
+#include "pald_rank.cuh"
 #include "pald_sym.cuh"
 
 using namespace pald_gpu;
@@ -170,14 +171,15 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 int make_map(CUtensorMap* map, const void* base, uint64_t n, uint64_t ld, int box_cols = kTile,
-             int box_rows = kBK) {
+             int box_rows = kBK, CUtensorMapDataType dtype = CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+             int elem_bytes = 4) {
   auto encode = get_encode();
   if (!encode) return set_error(PALD_GPU_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {n, n};
-  cuuint64_t strides[1] = {ld * 4};
+  cuuint64_t strides[1] = {ld * (uint64_t)elem_bytes};
   cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims,
+  CUresult r = encode(map, dtype, 2, const_cast<void*>(base), dims,
                       strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                       CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -186,18 +188,18 @@ int make_map(CUtensorMap* map, const void* base, uint64_t n, uint64_t ld, int bo
 }
 
 template <int PASS, bool A_NU, bool B_NU, bool T_NU, bool ZD, bool FAST, bool SPLIT = false,
-          int TILE = kTile, bool LIST = false, bool PEERS = false>
+          int TILE = kTile, bool LIST = false, bool PEERS = false, bool RANK = false>
 int launch_tile(const CUtensorMap& md, const CUtensorMap& mnu, const CUtensorMap& mw,
                 const KernelArgs& a, int grid, cudaStream_t s) {
-  auto k = pald_tile_kernel<PASS, A_NU, B_NU, T_NU, ZD, FAST, SPLIT, TILE, LIST, PEERS>;
+  auto k = pald_tile_kernel<PASS, A_NU, B_NU, T_NU, ZD, FAST, SPLIT, TILE, LIST, PEERS, RANK>;
   static bool attr_done[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (!attr_done[dev & 63]) {
-    PALD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes(PASS, TILE)));
+    PALD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes(PASS, TILE, RANK)));
     attr_done[dev & 63] = true;
   }
-  k<<<grid, kThreads, smem_bytes(PASS, TILE), s>>>(md, mnu, mw, a);
+  k<<<grid, kThreads, smem_bytes(PASS, TILE, RANK), s>>>(md, mnu, mw, a);
   PALD_CUDA(cudaGetLastError());
   return PALD_GPU_OK;
 }
@@ -248,6 +250,11 @@ struct pald_gpu_plan {
   uint32_t* sym_tile_flags = nullptr;
   unsigned long long* sym_count = nullptr;
   unsigned int* round_bar = nullptr;     // round barrier counter of the pair kernel
+  // Rank-coded pass 1 (pairwise, n <= 32768; pald_rank.cuh): RA / RB panels.
+  uint32_t* rank_a = nullptr;
+  uint16_t* rank_b = nullptr;
+  CUtensorMap tm_ra, tm_rb;
+  bool rank_ready = false;               // RA / RB built for the loaded D
   int sym_nch = 0;
   double sym_marked = 0;                 // share of (pair, k) steps on the exact step
   int last_kernel = PALD_GPU_KERNEL_NONE;
@@ -297,6 +304,8 @@ struct pald_gpu_plan {
     cudaFree(sym_tile_flags);
     cudaFree(sym_count);
     cudaFree(round_bar);
+    cudaFree(rank_a);
+    cudaFree(rank_b);
     cudaSetDevice(prev);
   }
 };
@@ -410,6 +419,60 @@ int plan_alloc(pald_gpu_plan* p) {
 
 int grid_rows(uint64_t n) { return (int)std::min<uint64_t>(n, 148ull * 16); }
 
+// Rank-coded pass 1 (pald_rank.cuh): pairwise focus with 2048 < n <= 32768
+// (below that the code build costs more than the faster pass 1 saves).
+// PALD_GPU_RANK=0 keeps the fp32 / integer-key compare path everywhere, 2
+// forces the rank path for every n <= 32768 (A/B, tests).
+bool rank_wanted(const pald_gpu_plan* p) {
+  static const int m = [] {
+    const char* e = getenv("PALD_GPU_RANK");
+    return e ? atoi(e) : 1;
+  }();
+  if (m == 0 || p->algorithm != PALD_GPU_PAIRWISE || p->n < 2 || p->n > (uint64_t)kRankMaxN) return false;
+  return m == 2 || p->n > 2048;
+}
+
+template <int THREADS, int ITEMS>
+int launch_row_rank(pald_gpu_plan* p, uint16_t* rk, uint16_t* scratch, int end_bit, cudaStream_t s) {
+  using Cfg = RankCfg<THREADS, ITEMS>;
+  auto k = row_rank_kernel<THREADS, ITEMS>;
+  const int n = (int)p->n, smem = Cfg::smem_bytes(n);
+  PALD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int per_sm = 1;
+  PALD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, THREADS, smem));
+  const int grid = std::min(n, p->sms * std::max(1, per_sm));
+  k<<<grid, THREADS, smem, s>>>(p->ds, n, (int)p->ld, end_bit, rk, scratch);
+  PALD_CUDA(cudaGetLastError());
+  return PALD_GPU_OK;
+}
+
+// Builds RA / RB from the plan's layout of D, using W as the Rk scratch
+// (W is zeroed afterwards by the caller).
+int build_rank_codes(pald_gpu_plan* p, cudaStream_t s) {
+  if (!p->rank_a) {
+    PALD_CUDA(cudaMalloc(&p->rank_a, p->n * p->ld * 4));
+    PALD_CUDA(cudaMalloc(&p->rank_b, p->n * p->ld * 2));
+    int rc;
+    if ((rc = make_map(&p->tm_ra, p->rank_a, p->n, p->ld, kTile, kBK, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4))) return rc;
+    if ((rc = make_map(&p->tm_rb, p->rank_b, p->n, p->ld, kTile, kBK, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2))) return rc;
+  }
+  const int n = (int)p->n, ld = (int)p->ld;
+  uint16_t* rk = reinterpret_cast<uint16_t*>(p->w);                  // W[0, n*ld*2 B)
+  uint16_t* scratch = rk + p->n * p->ld;                              // W[n*ld*2 B, ...)
+  const int end_bit = p->exact ? 32 : 30;  // fast path: scaled values < 1.0
+  int rc = n <= 2048   ? launch_row_rank<256, 8>(p, rk, scratch, end_bit, s)
+           : n <= 4096 ? launch_row_rank<256, 16>(p, rk, scratch, end_bit, s)
+           : n <= 8192 ? launch_row_rank<256, 32>(p, rk, scratch, end_bit, s)
+                       : launch_row_rank<512, 32>(p, rk, scratch, end_bit, s);
+  if (rc) return rc;
+  rank_layout_kernel<<<dim3((unsigned)(p->ld / 32), (unsigned)((p->n + 31) / 32)), 256, 0, s>>>(rk, n, ld, p->rank_a,
+                                                                                             p->rank_b);
+  PALD_CUDA(cudaGetLastError());
+  p->launches += 2;
+  p->rank_ready = true;
+  return PALD_GPU_OK;
+}
+
 bool sym_wins(const pald_gpu_plan* p, double marked);
 
 int plan_load_impl(pald_gpu_plan* p, const float* dD, uint64_t ldd, cudaStream_t s) {
@@ -453,6 +516,11 @@ int plan_load_impl(pald_gpu_plan* p, const float* dD, uint64_t ldd, cudaStream_t
                                                        p->dnu);
   PALD_CUDA(cudaGetLastError());
   ++p->launches;
+  p->rank_ready = false;
+  if (rank_wanted(p)) {
+    const int rc = build_rank_codes(p, s);
+    if (rc) return rc;
+  }
   PALD_CUDA(cudaMemsetAsync(p->u, 0, p->n * p->ld * 4, s));
   PALD_CUDA(cudaMemsetAsync(p->w, 0, p->n * p->ld * 4, s));
   p->sym_ready = false;
@@ -534,7 +602,17 @@ int plan_focus_counts_impl(pald_gpu_plan* p, uint64_t part, uint64_t parts, cuda
   const bool tri = p->algorithm == PALD_GPU_TRIPLET;
   const bool split = p->policy == PALD_GPU_INCLUSIVE_SPLIT;
   const CUtensorMap &md = p->tm_d, &mn = p->tm_dnu, &mw = p->tm_w;
-  if (peers) {  // counts RED'd straight into every rank's W over NVLink
+  if (p->rank_ready) {  // rank-coded packed compares (exact for both layouts)
+    KernelArgs ar = a;
+    ar.d = p->rank_a;
+    const CUtensorMap &ra = p->tm_ra, &rb = p->tm_rb;
+    if (peers)
+      rc = split ? launch_tile<0, false, false, true, false, true, false, kTile, false, true, true>(ra, rb, mw, ar, grid, s)
+                 : launch_tile<0, false, false, false, false, true, false, kTile, false, true, true>(ra, rb, mw, ar, grid, s);
+    else
+      rc = split ? launch_tile<0, false, false, true, false, true, false, kTile, false, false, true>(ra, rb, mw, ar, grid, s)
+                 : launch_tile<0, false, false, false, false, true, false, kTile, false, false, true>(ra, rb, mw, ar, grid, s);
+  } else if (peers) {  // counts RED'd straight into every rank's W over NVLink
     if (!p->exact) {
       rc = tri     ? launch_tile<0, true, true, true, false, true, false, kTile, false, true>(md, mn, mw, a, grid, s)
            : split ? launch_tile<0, false, false, true, false, true, false, kTile, false, true>(md, mn, mw, a, grid, s)
@@ -956,6 +1034,7 @@ int pald_gpu_plan_get_info(const pald_gpu_plan* p, pald_gpu_plan_info* out) {
   out->pair_kernel_ready = p->sym_ready ? 1 : 0;
   out->exact_step_share = p->sym_marked;
   out->launches = p->launches;
+  out->rank_codes = p->rank_ready ? 1 : 0;
   return PALD_GPU_OK;
 }
 

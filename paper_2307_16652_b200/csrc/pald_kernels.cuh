@@ -63,7 +63,10 @@ constexpr int kKUnroll = PALD_KUNROLL;
 constexpr int kBK = PALD_BK;    // third-point chunk per pipeline stage
 constexpr int kThreads = 256;   // 8 warps, 16 x 16 threads (8 x 8 outputs each on 128-wide tiles)
 __host__ __device__ constexpr int box_bytes(int tile) { return kBK * tile * 4; }
-__host__ __device__ constexpr int stage_bytes(int pass, int tile) { return (pass == 0 ? 2 : 3) * box_bytes(tile); }
+__host__ __device__ constexpr int stage_bytes(int pass, int tile, bool rank = false) {
+  // rank-coded pass 1: a 4-byte RA box and a 2-byte RB box (pald_rank.cuh)
+  return rank ? box_bytes(tile) + box_bytes(tile) / 2 : (pass == 0 ? 2 : 3) * box_bytes(tile);
+}
 // CTAs per SM: 1 for 128-wide tiles (8 x 8 outputs per thread, ~230
 // registers), 2 for the 64-wide small-n tiles (4 x 4 per thread).
 __host__ __device__ constexpr int ctas_per_sm(int tile) { return tile == 128 ? 1 : 2; }
@@ -72,15 +75,15 @@ __host__ __device__ constexpr int ctas_per_sm(int tile) { return tile == 128 ? 1
 #ifndef PALD_SMEM_BUDGET_KB
 #define PALD_SMEM_BUDGET_KB 200
 #endif
-__host__ __device__ constexpr int stages_for(int pass, int tile) {
-  return stage_bytes(pass, tile) * 4 <= PALD_SMEM_BUDGET_KB * 1024 / ctas_per_sm(tile) ? 4
-         : stage_bytes(pass, tile) * 3 <= PALD_SMEM_BUDGET_KB * 1024 / ctas_per_sm(tile) ? 3 : 2;
+__host__ __device__ constexpr int stages_for(int pass, int tile, bool rank = false) {
+  return stage_bytes(pass, tile, rank) * 4 <= PALD_SMEM_BUDGET_KB * 1024 / ctas_per_sm(tile) ? 4
+         : stage_bytes(pass, tile, rank) * 3 <= PALD_SMEM_BUDGET_KB * 1024 / ctas_per_sm(tile) ? 3 : 2;
 }
 constexpr int kBoxBytes = kBK * kTile * 4;  // one TMA box of a 128-wide panel (32 KB)
 constexpr float kCmpScale = 0x1p125f;       // S of the FFMA.SAT compare
 
-__host__ __device__ constexpr int smem_bytes(int pass, int tile) {
-  return stages_for(pass, tile) * stage_bytes(pass, tile) + 1024;
+__host__ __device__ constexpr int smem_bytes(int pass, int tile, bool rank = false) {
+  return stages_for(pass, tile, rank) * stage_bytes(pass, tile, rank) + 1024;
 }
 
 // Multi-GPU exchange over peer memory: the same buffer (W or C) of every
@@ -342,6 +345,43 @@ __device__ __forceinline__ void k_step_split(const float* __restrict__ sa, const
   }
 }
 
+// One k step of the rank-coded pairwise focus pass (pald_rank.cuh). Per
+// output (r, c) the focus test [d_rk < d_rc] | [d_ck < d_rc] becomes
+// [Rk[r][k] < RR] | [Rk[c][k] < CR] with RR = Rk[r][c], CR = Rk[c][r]
+// (+1 each for InclusiveSplit's <=). Two columns share one 32-bit word in
+// 16-bit lanes: X = (0x8000 | code) - threshold never borrows across lanes
+// and its bit 15 is [code >= threshold], so
+//   F = ~(X1 & X2) & 0x80008000   (focus flags of both columns)
+//   acc += F >> 15                (LEA.HI: the two counts in the two halves)
+// = 4 integer instructions per 2 output combos (vs 5 on the fp32 path).
+// thr[i][jp] holds -RR (.x) and -CR (.y) packed per column pair, acc .x the
+// packed counts.
+template <int TT = 8>
+__device__ __forceinline__ void k_step_rank(const uint32_t* __restrict__ sa, const uint16_t* __restrict__ sb,
+                                            int kk, int ty, int tx, const float2 (&thr)[TT][TT / 2],
+                                            float2 (&acc)[TT][TT / 2]) {
+  const uint4 a0 = reinterpret_cast<const uint4*>(sa + kk * kTile)[ty];
+  const uint4 a1 = reinterpret_cast<const uint4*>(sa + kk * kTile)[16 + ty];
+  const uint2 b0 = reinterpret_cast<const uint2*>(sb + kk * kTile)[tx];
+  const uint2 b1 = reinterpret_cast<const uint2*>(sb + kk * kTile)[16 + tx];
+  const uint32_t a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+  const uint32_t b[4] = {b0.x, b0.y, b1.x, b1.y};
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+#pragma unroll
+    for (int jp = 0; jp < 4; ++jp) {
+      const uint32_t x1 = a[i] + __float_as_uint(thr[i][jp].x);
+      const uint32_t x2 = b[jp] + __float_as_uint(thr[i][jp].y);
+      const uint32_t f = ~(x1 & x2) & 0x80008000u;
+      // hi32(f * 2^17) + acc = (f >> 15) + acc: ptxas emits one LEA.HI (a plain
+      // shift + add compiles to SHF + IADD3, tools/microbench4.cu)
+      uint32_t sum;
+      asm("mad.hi.u32 %0, %1, 0x20000, %2;" : "=r"(sum) : "r"(f), "r"(__float_as_uint(acc[i][jp].x)));
+      acc[i][jp].x = __uint_as_float(sum);
+    }
+  }
+}
+
 // Focus-finish tile index -> (tile row, tile col): upper-triangular tiles in
 // row-major order.
 __device__ __forceinline__ void tri_coords(int t, int nb, int& tr, int& tc) {
@@ -450,7 +490,7 @@ __device__ __forceinline__ WorkSplit make_split(const KernelArgs& a, int C, int 
 // the last warp to finish with it (shared-memory arrival counter), so no
 // block-wide barrier sits in the main loop.
 template <int PASS, bool A_NU, bool B_NU, bool T_NU, bool ZERO_DIAG, bool FAST, bool SPLIT = false,
-          int TILE = kTile, bool LIST = false, bool PEERS = false>
+          int TILE = kTile, bool LIST = false, bool PEERS = false, bool RANK = false>
 __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE))
     pald_tile_kernel(const __grid_constant__ CUtensorMap tm_d,
                      const __grid_constant__ CUtensorMap tm_dnu,
@@ -459,7 +499,8 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE))
   // Align the pipeline buffers to 1 KB with an offset into the same array,
   // so the compiler keeps the shared address space (LDS, not generic LD).
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  constexpr int kStages = stages_for(PASS, TILE);
+  static_assert(!RANK || (PASS == 0 && TILE == kTile), "rank codes: 128-wide pass 1 only");
+  constexpr int kStages = stages_for(PASS, TILE, RANK);
   constexpr int TT = TILE / 16;  // outputs per thread per dimension
   constexpr int BOX = box_bytes(TILE);
   __shared__ uint64_t full_bar[kStages];
@@ -504,7 +545,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE))
   auto run_c0 = [&](int ri) { return ri < ws.full ? 0 : s_rem[ri - ws.full][1]; };
   auto run_c1 = [&](int ri) { return ri < ws.full ? nchunks : s_rem[ri - ws.full][2]; };
 
-  constexpr int SB = stage_bytes(PASS, TILE);
+  constexpr int SB = stage_bytes(PASS, TILE, RANK);
   auto issue = [&](int t, int ch, int s) {
     int tr, tc;
     tile_coords<PASS, LIST>(args, t, tr, tc);
@@ -516,6 +557,11 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE))
     const CUtensorMap* mb = (B_NU && k1 <= r0) ? &tm_dnu : &tm_d;
     uint8_t* st = smem + s * SB;
     mbar_expect_tx(&full_bar[s], SB);
+    if (RANK) {  // tm_d: RA (uint32 codes, rows R), tm_dnu: RB (uint16 codes, columns Q)
+      tma_load_2d(st, &tm_d, r0, k0, &full_bar[s]);
+      tma_load_2d(st + BOX, &tm_dnu, c0, k0, &full_bar[s]);
+      return;
+    }
     tma_load_2d(st, ma, r0, k0, &full_bar[s]);
     tma_load_2d(st + BOX, mb, c0, k0, &full_bar[s]);
     if (PASS == 1) tma_load_2d(st + 2 * BOX, &tm_w, r0, k0, &full_bar[s]);
@@ -551,6 +597,22 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE))
 #pragma unroll
       for (int jp = 0; jp < TT / 2; ++jp) {
         uint32_t t2[2];
+        if constexpr (RANK) {  // args.d = RA: Rk[r][c] = RA[c][r] & 0x7fff
+          uint32_t rr = 0, cr = 0;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = r0 + row_off<TILE>(ty, i), c = c0 + row_off<TILE>(tx, 2 * jp + h);
+            if (r < n && c < n) {
+              const uint32_t t_rc = (__ldg(args.d + (size_t)c * ld + r) & 0x7fffu) + (T_NU ? 1u : 0u);
+              const uint32_t t_cr = (__ldg(args.d + (size_t)r * ld + c) & 0x7fffu) + (T_NU ? 1u : 0u);
+              rr |= t_rc << (16 * h);
+              cr |= t_cr << (16 * h);
+            }
+          }
+          thr[i][jp] = make_float2(__uint_as_float(0u - rr), __uint_as_float(0u - cr));
+          acc[i][jp] = make_float2(0.f, 0.f);
+          continue;
+        }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int r = r0 + row_off<TILE>(ty, i), c = c0 + row_off<TILE>(tx, 2 * jp + h);
@@ -579,7 +641,16 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE))
       const bool a_in = A_NU && (k0 >= c0) && (k0 < c0 + TILE);
       const bool b_in = B_NU && (k0 >= r0) && (k0 < r0 + TILE);
       const int kmax = min(kBK, n - k0);
-      if (PASS == 1 && SPLIT) {
+      if constexpr (RANK) {
+        const uint32_t* ra = reinterpret_cast<const uint32_t*>(st);
+        const uint16_t* rb = reinterpret_cast<const uint16_t*>(st + BOX);
+        if (kmax == kBK) {
+#pragma unroll kKUnroll
+          for (int kk = 0; kk < kBK; ++kk) k_step_rank(ra, rb, kk, ty, tx, thr, acc);
+        } else {
+          for (int kk = 0; kk < kmax; ++kk) k_step_rank(ra, rb, kk, ty, tx, thr, acc);
+        }
+      } else if (PASS == 1 && SPLIT) {
         for (int kk = 0; kk < kmax; ++kk) k_step_split<FAST, TILE>(sa, sb, sw, kk, ty, tx, thr, acc);
       } else if (!a_in && !b_in && kmax == kBK) {
 #pragma unroll kKUnroll
@@ -607,7 +678,13 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE))
 #pragma unroll
         for (int j = 0; j < TT; ++j) {
           const int c = c0 + row_off<TILE>(tx, j);
-          const float v = (j & 1) ? acc[i][j >> 1].y : acc[i][j >> 1].x;
+          float v;
+          if constexpr (RANK) {
+            const uint32_t packed = __float_as_uint(acc[i][j >> 1].x);
+            v = (float)((j & 1) ? (packed >> 16) : (packed & 0xffffu));
+          } else {
+            v = (j & 1) ? acc[i][j >> 1].y : acc[i][j >> 1].x;
+          }
           if constexpr (PEERS) {  // fused exchange: the partial count to every rank
             if (c < n && v != 0.f)
               for (int q = 0; q < args.peers.count; ++q)

@@ -1,0 +1,211 @@
+// pald_rank.cuh -- per-row rank codes of D for the packed pass-1 kernel.
+//
+// Pairwise focus (blocked.hpp:101-122, reference.hpp:31-45) only ever
+// compares two entries of the SAME row of D: [d_xz < d_xy] (row x) and
+// [d_yz < d_xy] (row y). Replacing every entry of row r by its rank in that
+// row,
+//
+//   Rk[r][k] = #{ j : d_rj < d_rk }          (ties share the lowest rank),
+//
+// preserves every such comparison exactly: d_rk < d_rc <=> Rk[r][k] <
+// Rk[r][c], and d_rk <= d_rc <=> Rk[r][k] < Rk[r][c] + 1. Ranks of an
+// n <= 32768 row fit in 15 bits, so the focus kernel can compare two output
+// columns per 32-bit integer instruction (16-bit lanes with a borrow-free
+// flag bit, pald_kernels.cuh k_step_rank). The codes are built once per load:
+//
+//   row_rank_kernel:    one CTA per row; CUB block radix sort of (key,
+//                       index) pairs (rows > 16384: two sorted segments
+//                       merged by merge path), then a max-scan over the
+//                       sorted keys gives each element the position of the
+//                       first element of its tie group; ranks scattered to
+//                       Rk[r][*].
+//   rank_layout_kernel: transposes Rk into the two panels the focus kernel
+//                       streams by TMA: RA[k][r] = (0x8000 | Rk[r][k]) * 0x10001
+//                       (the 16-bit code with its flag bit, broadcast to both
+//                       halves) and RB[k][c] = 0x8000 | Rk[c][k] (uint16).
+//
+// Keys are the plan's layout of D (scaled fp32 bits or the exact path's
+// integer keys 2*bits(d)): both are monotone in d as unsigned integers.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cub/block/block_radix_sort.cuh>
+
+namespace pald_gpu {
+
+constexpr int kRankMaxN = 32768;  // ranks < 2^15: one flag bit per 16-bit lane
+constexpr int kRankRadixBits = 6;   // 5 digit passes over 30-bit fast-path keys, 6 over 32
+
+// Per-row sort configuration: THREADS x ITEMS keys per CUB block radix sort
+// (one "segment"); rows longer than one segment (n > 16384) are sorted as two
+// segments and merged.
+template <int THREADS, int ITEMS>
+struct RankCfg {
+  static constexpr int kSeg = THREADS * ITEMS;
+  using Sort = cub::BlockRadixSort<uint32_t, THREADS, ITEMS, uint16_t, kRankRadixBits>;
+  static constexpr int kTempBytes = (int)((sizeof(typename Sort::TempStorage) + 127) / 128 * 128);
+  // the two-segment merge keeps both sorted key runs in shared memory
+  static constexpr int smem_bytes(int n) { return kTempBytes + (n > kSeg ? 2 * kSeg * 4 : 0); }
+};
+
+// Block-wide exclusive max-scan of one value per thread (tid order).
+template <int THREADS>
+__device__ __forceinline__ uint32_t block_excl_max(uint32_t v, uint32_t* warp_buf) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl = max(incl, u);
+  }
+  if (lane == 31) warp_buf[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = lane < THREADS / 32 ? warp_buf[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w = max(w, u);
+    }
+    if (lane < THREADS / 32) warp_buf[lane] = w;
+  }
+  __syncthreads();
+  uint32_t ex = __shfl_up_sync(0xffffffffu, incl, 1);
+  if (lane == 0) ex = 0u;
+  if (warp > 0) ex = max(ex, warp_buf[warp - 1]);
+  __syncthreads();  // warp_buf reused by the caller's next scan
+  return ex;
+}
+
+// Rk (uint16, n x ld, row-major) of the layout keys ds (n x ld). Rank of a
+// sorted position = the last tie-group start at or before it (a max-scan of
+// the positions where the key changes). idx_scratch: 2 * kSeg uint16 per
+// CTA (two-segment rows only).
+template <int THREADS, int ITEMS>
+__global__ void __launch_bounds__(THREADS)
+    row_rank_kernel(const uint32_t* __restrict__ ds, int n, int ld, int end_bit, uint16_t* __restrict__ rk,
+                    uint16_t* __restrict__ idx_scratch) {
+  using Cfg = RankCfg<THREADS, ITEMS>;
+  constexpr int S = Cfg::kSeg;
+  extern __shared__ __align__(128) uint8_t rank_smem[];
+  auto& temp = *reinterpret_cast<typename Cfg::Sort::TempStorage*>(rank_smem);
+  uint32_t* sk = reinterpret_cast<uint32_t*>(rank_smem + Cfg::kTempBytes);  // two-segment rows
+  __shared__ uint32_t warp_buf[THREADS / 32];
+  __shared__ uint32_t last_key[THREADS / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nseg = n > S ? 2 : 1;
+  uint16_t* scr = idx_scratch + (size_t)blockIdx.x * 2 * S;
+
+  for (int r = blockIdx.x; r < n; r += gridDim.x) {
+    const uint32_t* row = ds + (size_t)r * ld;
+    uint16_t* out = rk + (size_t)r * ld;
+    for (int h = 0; h < nseg; ++h) {
+      uint32_t keys[ITEMS];
+      uint16_t vals[ITEMS];
+#pragma unroll
+      for (int e = 0; e < ITEMS; ++e) {  // striped (coalesced) load; order is irrelevant
+        const int i = h * S + e * THREADS + tid;
+        keys[e] = i < n ? __ldg(row + i) : 0xffffffffu;  // never a layout key: sorts last
+        vals[e] = (uint16_t)i;
+      }
+      Cfg::Sort(temp).Sort(keys, vals, 0, end_bit);  // blocked: positions tid*ITEMS + e
+      if (nseg == 1) {
+        // previous key of position tid*ITEMS: the last key of thread tid - 1
+        uint32_t prev = __shfl_up_sync(0xffffffffu, keys[ITEMS - 1], 1);
+        if (lane == 31) last_key[warp] = keys[ITEMS - 1];
+        __syncthreads();
+        if (lane == 0) prev = warp > 0 ? last_key[warp - 1] : ~keys[0];
+        uint32_t m = 0, pk = prev;
+#pragma unroll
+        for (int e = 0; e < ITEMS; ++e) {
+          if (keys[e] != pk) m = (uint32_t)(tid * ITEMS + e);
+          pk = keys[e];
+        }
+        uint32_t run = block_excl_max<THREADS>(m, warp_buf);
+        pk = prev;
+#pragma unroll
+        for (int e = 0; e < ITEMS; ++e) {
+          if (keys[e] != pk) run = (uint32_t)(tid * ITEMS + e);
+          pk = keys[e];
+          if (vals[e] < n) out[vals[e]] = (uint16_t)run;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < ITEMS; ++e) {
+          sk[h * S + tid * ITEMS + e] = keys[e];
+          scr[h * S + tid * ITEMS + e] = vals[e];
+        }
+      }
+      __syncthreads();  // TempStorage / last_key reuse
+    }
+    if (nseg == 1) continue;
+    // Two sorted runs A = sk[0, S), B = sk[S, 2S): thread tid emits merged
+    // positions [d, d + 2*ITEMS) (merge path; A first on equal keys).
+    const uint32_t* A = sk;
+    const uint32_t* B = sk + S;
+    const int d = tid * 2 * ITEMS;
+    int lo = max(0, d - S), hi = min(d, S);
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (A[mid] <= B[d - mid - 1]) lo = mid + 1; else hi = mid;
+    }
+    const int i0 = lo, j0 = d - lo;
+    uint32_t prev;  // merged key at position d - 1
+    if (d == 0) prev = (A[0] <= B[0] ? A[0] : B[0]) ^ 1u;  // differs from the first merged key
+    else prev = max(i0 > 0 ? A[i0 - 1] : 0u, j0 > 0 ? B[j0 - 1] : 0u);
+    uint32_t m = 0;
+    {
+      int i = i0, j = j0;
+      uint32_t pk = prev;
+      for (int q = 0; q < 2 * ITEMS; ++q) {
+        const bool ta = j >= S || (i < S && A[i] <= B[j]);
+        const uint32_t k = ta ? A[i] : B[j];
+        if (ta) ++i; else ++j;
+        if (k != pk) m = (uint32_t)(d + q);
+        pk = k;
+      }
+    }
+    uint32_t run = block_excl_max<THREADS>(m, warp_buf);
+    {
+      int i = i0, j = j0;
+      uint32_t pk = prev;
+      for (int q = 0; q < 2 * ITEMS; ++q) {
+        const bool ta = j >= S || (i < S && A[i] <= B[j]);
+        const uint32_t k = ta ? A[i] : B[j];
+        const int v = ta ? scr[i] : scr[S + j];
+        if (ta) ++i; else ++j;
+        if (k != pk) run = (uint32_t)(d + q);
+        pk = k;
+        if (v < n) out[v] = (uint16_t)run;
+      }
+    }
+    __syncthreads();  // sk reused by the next row
+  }
+}
+
+// RA[k][r] = (0x8000 | Rk[r][k]) * 0x10001, RB[k][r] = 0x8000 | Rk[r][k] for
+// k < n, r < ld; padding rows/columns (r >= n) get code 0.
+__global__ void __launch_bounds__(256)
+    rank_layout_kernel(const uint16_t* __restrict__ rk, int n, int ld, uint32_t* __restrict__ ra,
+                       uint16_t* __restrict__ rb) {
+  __shared__ uint16_t t[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  const int r0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+  for (int yy = ty; yy < 32; yy += 8) {
+    const int r = r0 + yy, k = k0 + tx;
+    t[yy][tx] = (r < n && k < n) ? rk[(size_t)r * ld + k] : (uint16_t)0;
+  }
+  __syncthreads();
+  for (int yy = ty; yy < 32; yy += 8) {
+    const int k = k0 + yy, r = r0 + tx;
+    if (k < n && r < ld) {
+      const uint32_t v = 0x8000u | t[tx][yy];
+      ra[(size_t)k * ld + r] = v * 0x10001u;
+      rb[(size_t)k * ld + r] = (uint16_t)v;
+    }
+  }
+}
+
+}  // namespace pald_gpu

@@ -190,7 +190,8 @@ class Engine:
         _raise_for(self.lib.pald_gpu_plan_get_info(self._plan, C.byref(i)))
         return {"cohesion_kernel": _lib.KERNEL_NAMES.get(i.cohesion_kernel, str(i.cohesion_kernel)),
                 "exact_path": bool(i.exact_path), "pair_kernel_ready": bool(i.pair_kernel_ready),
-                "exact_step_share": i.exact_step_share, "launches": int(i.launches)}
+                "exact_step_share": i.exact_step_share, "launches": int(i.launches),
+                "rank_codes": bool(i.rank_codes)}
 
     def run(self, D: torch.Tensor, stream=None) -> None:
         self.load(D, stream)

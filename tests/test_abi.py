@@ -51,7 +51,7 @@ def test_abi_version_and_opts_layout():
     from paper_2307_16652_b200 import _lib
 
     lib = _lib.load()
-    assert lib.pald_gpu_abi_version() == 2
+    assert lib.pald_gpu_abi_version() == 3
     o = _lib.make_opts()
     assert o.struct_size == C.sizeof(_lib.Opts) == 48
     assert o.block == o.block_focus == o.block_cohesion == 128 and o.device == -1

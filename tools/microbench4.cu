@@ -1,0 +1,158 @@
+// Focus (pass 1) inner loop: fp32 FMNMX + FFMA.SAT + FADD2 (current) vs
+// per-row rank codes packed two columns per 32-bit word:
+//   X1 = A_bc - RR, X2 = B - CR  (16-bit lanes, bit 15 = "not less")
+//   F  = ~(X1 & X2) & 0x80008000 (focus flags), acc += F >> 15.
+// Output: output (r, c, k) combos per SM-cycle.
+#include <cstdio>
+#include <cstdlib>
+#include <cstdint>
+#include <cuda_runtime.h>
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); exit(1);} } while (0)
+__device__ unsigned long long g_cyc[4096];
+
+__device__ __forceinline__ uint32_t madhi(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm volatile("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t vmin2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("min.u16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+
+// MODE 0: fp32 baseline. 1: rank, acc += F>>15 (compiler). 2: rank, mad.hi.
+// 3: rank with min.u16x2 + mask. 4: rank, add via IMAD forced (mad.lo with
+// register one) for X1.
+template <int MODE, int ORD>
+__global__ void __launch_bounds__(256, 1) kern(uint32_t* out, int reps, const uint32_t* cin) {
+  constexpr int BK = 16;
+  __shared__ __align__(16) uint32_t sA[BK][128];
+  __shared__ __align__(16) uint32_t sB[BK][128];
+  for (int i = threadIdx.x; i < BK * 128; i += 256) {
+    const uint32_t ra = (i * 2654435761u) & 0x7fff, rb = (i * 2246822519u) & 0x7fff;
+    if (MODE == 0) {
+      (&sA[0][0])[i] = __float_as_uint(ra * 1e-4f);
+      (&sB[0][0])[i] = __float_as_uint(rb * 1e-4f);
+    } else {
+      (&sA[0][0])[i] = (0x8000u | ra) * 0x10001u;
+      (&sB[0][0])[i] = (0x8000u | rb) | ((0x8000u | ((rb * 7) & 0x7fff)) << 16);
+    }
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ty = (warp >> 1) * 4 + (lane >> 3), tx = (warp & 1) * 8 + (lane & 7);
+  uint32_t acc[8][4], c1[8][4], c2[8][4];
+  float2 facc[8][4], thr[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      acc[i][p] = 0;
+      c1[i][p] = cin[(i * 4 + p) * 512 + threadIdx.x];
+      c2[i][p] = cin[(i * 4 + p + 32) * 512 + threadIdx.x];
+      facc[i][p] = make_float2(0.f, 0.f);
+      thr[i][p] = make_float2(__uint_as_float(c1[i][p]), __uint_as_float(c2[i][p]));
+    }
+  const uint32_t one = cin[64 * 512];
+  unsigned long long t0 = clock64();
+  for (int r = 0; r < reps; ++r) {
+#pragma unroll 2
+    for (int k = 0; k < BK; ++k) {
+      uint32_t a[8], b[8];
+      const uint4 a0 = *reinterpret_cast<const uint4*>(&sA[k][ty * 4]);
+      const uint4 a1 = *reinterpret_cast<const uint4*>(&sA[k][64 + ty * 4]);
+      a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w;
+      a[4] = a1.x; a[5] = a1.y; a[6] = a1.z; a[7] = a1.w;
+      if (MODE == 0) {
+        const uint4 b0 = *reinterpret_cast<const uint4*>(&sB[k][tx * 4]);
+        const uint4 b1 = *reinterpret_cast<const uint4*>(&sB[k][64 + tx * 4]);
+        b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w;
+        b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int p = 0; p < 4; ++p) {
+            const float m0 = fminf(__uint_as_float(a[i]), __uint_as_float(b[2 * p]));
+            const float m1 = fminf(__uint_as_float(a[i]), __uint_as_float(b[2 * p + 1]));
+            const float k0 = __saturatef(__fmaf_rn(m0, -0x1p125f, thr[i][p].x));
+            const float k1 = __saturatef(__fmaf_rn(m1, -0x1p125f, thr[i][p].y));
+            facc[i][p] = __fadd2_rn(facc[i][p], make_float2(k0, k1));
+          }
+      } else {
+        // B: 8 columns as 4 packed pairs (16-bit)
+        const uint4 b0 = *reinterpret_cast<const uint4*>(&sB[k][tx * 4]);
+        b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w;
+        auto body = [&](int i, int p) {
+          uint32_t x1, x2, f;
+          if (MODE == 4) asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(x1) : "r"(a[i]), "r"(one), "r"(c1[i][p]));
+          else x1 = a[i] + c1[i][p];
+          x2 = b[p] + c2[i][p];
+          if (MODE == 3) {
+            f = vmin2(x1, x2);
+            acc[i][p] = madhi(~f & 0x80008000u, 0x20000u, acc[i][p]);
+            return;
+          }
+          f = ~(x1 & x2) & 0x80008000u;
+          if (MODE == 1) acc[i][p] += f >> 15;
+          else acc[i][p] = madhi(f, 0x20000u, acc[i][p]);
+        };
+        if (ORD == 0) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int p = 0; p < 4; ++p) body(i, p);
+        } else {
+#pragma unroll
+          for (int p = 0; p < 4; ++p)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) body(i, p);
+        }
+      }
+    }
+  }
+  unsigned long long t1 = clock64();
+  uint32_t s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int p = 0; p < 4; ++p) s += acc[i][p] + __float_as_uint(facc[i][p].x + facc[i][p].y);
+  out[blockIdx.x * 1024 + threadIdx.x] = s;
+  if (threadIdx.x == 0) g_cyc[blockIdx.x] = t1 - t0;
+}
+
+template <int MODE, int ORD>
+void run(const char* name, uint32_t* out, const uint32_t* cin, int nsm) {
+  const int reps = 1024;
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  float ms = 0;
+  for (int rep = 0; rep < 3; ++rep) {
+    cudaEventRecord(e0);
+    kern<MODE, ORD><<<nsm, 256>>>(out, reps, cin);
+    cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
+    CK(cudaGetLastError());
+    cudaEventElapsedTime(&ms, e0, e1);
+  }
+  static unsigned long long h[4096];
+  CK(cudaMemcpyFromSymbol(h, g_cyc, sizeof(unsigned long long) * nsm));
+  double cyc = 0; for (int i = 0; i < nsm; ++i) cyc += h[i]; cyc /= nsm;
+  const double combos = 128.0 * 128 * 16 * reps;
+  printf("{\"bench\": \"%s\", \"output_combos_per_sm_cycle\": %.2f, \"ms\": %.3f, \"mhz_est\": %.0f}\n", name, combos / cyc, ms, cyc / (ms * 1e3));
+}
+
+int main() {
+  cudaDeviceProp prop; CK(cudaGetDeviceProperties(&prop, 0));
+  const int nsm = prop.multiProcessorCount;
+  uint32_t* out; CK(cudaMalloc(&out, sizeof(uint32_t) * 4096 * 1024));
+  uint32_t* cin; CK(cudaMalloc(&cin, sizeof(uint32_t) * 65 * 512));
+  CK(cudaMemset(cin, 0, sizeof(uint32_t) * 65 * 512));
+  uint32_t one = 1; CK(cudaMemcpy(cin + 64 * 512, &one, 4, cudaMemcpyHostToDevice));
+  run<0, 0>("focus_fp32", out, cin, nsm);
+  run<1, 0>("focus_rank_shift", out, cin, nsm);
+  run<2, 0>("focus_rank_madhi", out, cin, nsm);
+  run<3, 0>("focus_rank_vmin", out, cin, nsm);
+  run<4, 0>("focus_rank_madhi_imadx1", out, cin, nsm);
+  run<1, 1>("focus_rank_shift_colouter", out, cin, nsm);
+  run<2, 1>("focus_rank_madhi_colouter", out, cin, nsm);
+  return 0;
+}

@@ -38,11 +38,12 @@ def main():
         f = statistics.median(e[1].elapsed_time(e[2]) for e in ev) / 1e3
         c = statistics.median(e[2].elapsed_time(e[3]) for e in ev) / 1e3
         t = statistics.median(e[0].elapsed_time(e[3]) for e in ev) / 1e3
+        ld_ms = statistics.median(e[0].elapsed_time(e[1]) for e in ev)
         nb = eng.tiles_per_dim
         fcombos = nb * (nb + 1) / 2 * 128 * 128 * n
         ccombos = nb * nb * 128 * 128 * n
         cyc = 148 * mhz * 1e6
-        print(f"{cfg.name}:{alg} n={n} step {t*1e3:.2f} ms  focus {f*1e3:.2f} ms "
+        print(f"{cfg.name}:{alg} n={n} step {t*1e3:.2f} ms  load {ld_ms:.2f} ms  focus {f*1e3:.2f} ms "
               f"({fcombos/f/cyc:.1f} combos/SM-cyc)  cohesion {c*1e3:.2f} ms ({ccombos/c/cyc:.1f})  "
               f"triplets/s {n**3/t:.3e} exact={eng.exact_path}", flush=True)
         if a.check and alg == "pairwise":
