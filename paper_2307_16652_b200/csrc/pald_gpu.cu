@@ -253,6 +253,9 @@ struct pald_gpu_plan {
   // Rank-coded pass 1 (pairwise, n <= 32768; pald_rank.cuh): RA / RB panels.
   uint32_t* rank_a = nullptr;
   uint16_t* rank_b = nullptr;
+  uint32_t* rank_scratch = nullptr;      // per-CTA scratch of the rank kernels
+  int* rank_fail = nullptr;              // [count, rows...] declined by the bins kernel
+  size_t rank_scratch_words = 0;
   CUtensorMap tm_ra, tm_rb;
   bool rank_ready = false;               // RA / RB built for the loaded D
   int sym_nch = 0;
@@ -306,6 +309,8 @@ struct pald_gpu_plan {
     cudaFree(round_bar);
     cudaFree(rank_a);
     cudaFree(rank_b);
+    cudaFree(rank_scratch);
+    cudaFree(rank_fail);
     cudaSetDevice(prev);
   }
 };
@@ -432,8 +437,20 @@ bool rank_wanted(const pald_gpu_plan* p) {
   return m == 2 || p->n > 2048;
 }
 
+int ensure_rank_scratch(pald_gpu_plan* p, size_t words) {
+  if (words <= p->rank_scratch_words) return PALD_GPU_OK;
+  cudaFree(p->rank_scratch);
+  p->rank_scratch = nullptr;
+  p->rank_scratch_words = 0;
+  PALD_CUDA(cudaMalloc(&p->rank_scratch, words * 4));
+  p->rank_scratch_words = words;
+  return PALD_GPU_OK;
+}
+
+// Sort path of the rank codes over all rows (rows == nullptr) or over the
+// rows listed by the bins kernel (count on the device).
 template <int THREADS, int ITEMS>
-int launch_row_rank(pald_gpu_plan* p, uint16_t* rk, uint16_t* scratch, int end_bit, cudaStream_t s) {
+int launch_row_rank(pald_gpu_plan* p, uint16_t* rk, int end_bit, const int* rows, const int* count, cudaStream_t s) {
   using Cfg = RankCfg<THREADS, ITEMS>;
   auto k = row_rank_kernel<THREADS, ITEMS>;
   const int n = (int)p->n, smem = Cfg::smem_bytes(n);
@@ -441,8 +458,11 @@ int launch_row_rank(pald_gpu_plan* p, uint16_t* rk, uint16_t* scratch, int end_b
   int per_sm = 1;
   PALD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, THREADS, smem));
   const int grid = std::min(n, p->sms * std::max(1, per_sm));
-  k<<<grid, THREADS, smem, s>>>(p->ds, n, (int)p->ld, end_bit, rk, scratch);
+  int rc = ensure_rank_scratch(p, (size_t)grid * std::max(n, Cfg::kSeg));
+  if (rc) return rc;
+  k<<<grid, THREADS, smem, s>>>(p->ds, n, (int)p->ld, end_bit, rows, count, rk, p->rank_scratch);
   PALD_CUDA(cudaGetLastError());
+  ++p->launches;
   return PALD_GPU_OK;
 }
 
@@ -457,18 +477,36 @@ int build_rank_codes(pald_gpu_plan* p, cudaStream_t s) {
     if ((rc = make_map(&p->tm_rb, p->rank_b, p->n, p->ld, kTile, kBK, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2))) return rc;
   }
   const int n = (int)p->n, ld = (int)p->ld;
-  uint16_t* rk = reinterpret_cast<uint16_t*>(p->w);                  // W[0, n*ld*2 B)
-  uint16_t* scratch = rk + p->n * p->ld;                              // W[n*ld*2 B, ...)
-  const int end_bit = p->exact ? 32 : 30;  // fast path: scaled values < 1.0
-  int rc = n <= 2048   ? launch_row_rank<256, 8>(p, rk, scratch, end_bit, s)
-           : n <= 4096 ? launch_row_rank<256, 16>(p, rk, scratch, end_bit, s)
-           : n <= 8192 ? launch_row_rank<256, 32>(p, rk, scratch, end_bit, s)
-                       : launch_row_rank<512, 32>(p, rk, scratch, end_bit, s);
+  uint16_t* rk = reinterpret_cast<uint16_t*>(p->w);  // W[0, n*ld*2 B)
+  const int end_bit = p->exact ? 32 : 30;            // fast path: scaled values < 1.0
+  const int* rows = nullptr;
+  const int* count = nullptr;
+  int rc;
+  if (!p->exact) {  // value-linear bins (finite fp32 keys); declined rows -> sort path
+    if (!p->rank_fail) PALD_CUDA(cudaMalloc(&p->rank_fail, (p->n + 1) * sizeof(int)));
+    PALD_CUDA(cudaMemsetAsync(p->rank_fail, 0, sizeof(int), s));
+    static bool attr_done[64] = {};
+    if (!attr_done[p->device & 63]) {
+      PALD_CUDA(cudaFuncSetAttribute(row_rank_bins_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kRankBinSmem));
+      attr_done[p->device & 63] = true;
+    }
+    const int grid = (int)std::min<uint64_t>(p->n, (uint64_t)p->sms);
+    row_rank_bins_kernel<<<grid, kRankBinThreads, kRankBinSmem, s>>>(p->ds, n, ld, rk, p->rank_fail + 1,
+                                                                      p->rank_fail);
+    PALD_CUDA(cudaGetLastError());
+    ++p->launches;
+    rows = p->rank_fail + 1;
+    count = p->rank_fail;
+  }
+  rc = n <= 2048   ? launch_row_rank<256, 8>(p, rk, end_bit, rows, count, s)
+       : n <= 4096 ? launch_row_rank<256, 16>(p, rk, end_bit, rows, count, s)
+       : n <= 8192 ? launch_row_rank<256, 32>(p, rk, end_bit, rows, count, s)
+                   : launch_row_rank<512, 32>(p, rk, end_bit, rows, count, s);
   if (rc) return rc;
   rank_layout_kernel<<<dim3((unsigned)(p->ld / 32), (unsigned)((p->n + 31) / 32)), 256, 0, s>>>(rk, n, ld, p->rank_a,
                                                                                              p->rank_b);
   PALD_CUDA(cudaGetLastError());
-  p->launches += 2;
+  ++p->launches;
   p->rank_ready = true;
   return PALD_GPU_OK;
 }

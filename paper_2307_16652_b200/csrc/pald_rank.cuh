@@ -37,6 +37,10 @@ namespace pald_gpu {
 
 constexpr int kRankMaxN = 32768;  // ranks < 2^15: one flag bit per 16-bit lane
 constexpr int kRankRadixBits = 6;   // 5 digit passes over 30-bit fast-path keys, 6 over 32
+constexpr int kRankBins = 16384;    // value-linear bins of the fast row path
+constexpr int kRankMaxBin = 64;     // larger bins: the row takes the sort path
+// packed u16 counts + cursors, and the keys of multi-key bins
+constexpr int kRankBinSmem = kRankBins * 2 * 2 + kRankMaxN * 4;
 
 // Per-row sort configuration: THREADS x ITEMS keys per CUB block radix sort
 // (one "segment"); rows longer than one segment (n > 16384) are sorted as two
@@ -79,14 +83,157 @@ __device__ __forceinline__ uint32_t block_excl_max(uint32_t v, uint32_t* warp_bu
   return ex;
 }
 
+template <int THREADS>
+__device__ __forceinline__ uint32_t block_reduce_max(uint32_t v, uint32_t* warp_buf) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if (lane == 0) warp_buf[warp] = v;
+  __syncthreads();
+  uint32_t r = 0;
+#pragma unroll
+  for (int w = 0; w < THREADS / 32; ++w) r = max(r, warp_buf[w]);
+  __syncthreads();
+  return r;
+}
+
+// Block-wide exclusive sum of one value per thread (tid order); *total set.
+template <int THREADS>
+__device__ __forceinline__ uint32_t block_excl_sum(uint32_t v, uint32_t* warp_buf, uint32_t* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += u;
+  }
+  if (lane == 31) warp_buf[warp] = incl;
+  __syncthreads();
+  uint32_t before = 0, all = 0;
+#pragma unroll
+  for (int w = 0; w < THREADS / 32; ++w) {
+    const uint32_t x = warp_buf[w];
+    if (w < warp) before += x;
+    all += x;
+  }
+  __syncthreads();
+  *total = all;
+  return before + incl - v;
+}
+
+// Fast path of one row (fp32 layout keys, all finite): counting sort on
+// NB value-linear bins, bin = floor(v * (NB-1)/vmax) (monotone in v), so
+//   rank(x) = #{keys in lower bins} + #{keys < x in x's bin}.
+// Bins hold ~n/NB keys; multi-key bins are resolved by scanning the bin's
+// keys, scattered into shared memory. The row stays in registers (thread t
+// holds elements t + e*THREADS). Returns false (row left to the sort path)
+// when a bin holds more than kRankMaxBin keys.
+template <int THREADS>
+__device__ bool rank_row_bins(const uint32_t* __restrict__ row, int n, uint16_t* __restrict__ out,
+                              uint32_t* hist, uint32_t* curs, uint32_t* kscr, uint32_t* warp_buf) {
+  constexpr int NB = kRankBins, W = NB / 2, PER = W / THREADS, E = kRankMaxN / THREADS;
+  const int tid = threadIdx.x;
+  uint32_t key[E];
+  uint32_t mx = 0;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = e * THREADS + tid;
+    key[e] = i < n ? __ldg(row + i) : 0u;
+    mx = max(mx, key[e]);
+  }
+#pragma unroll
+  for (int q = 0; q < PER; ++q) hist[q * THREADS + tid] = 0u;
+  mx = block_reduce_max<THREADS>(mx, warp_buf);  // (syncs: hist zeroed)
+  const float scale = (float)(NB - 1) / __uint_as_float(mx);
+  auto bin_of = [&](uint32_t k) { return min(NB - 1, (int)(__uint_as_float(k) * scale)); };
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    if (e * THREADS + tid < n) {
+      const int b = bin_of(key[e]);
+      atomicAdd(&hist[b >> 1], 1u << ((b & 1) * 16));
+    }
+  }
+  __syncthreads();
+  // exclusive scan of the NB counts (thread tid: words [tid*PER, (tid+1)*PER))
+  uint32_t local = 0, cmax = 0;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const uint32_t w = hist[tid * PER + q];
+    local += (w & 0xffffu) + (w >> 16);
+    cmax = max(cmax, max(w & 0xffffu, w >> 16));
+  }
+  uint32_t total;
+  uint32_t run = block_excl_sum<THREADS>(local, warp_buf, &total);
+  cmax = block_reduce_max<THREADS>(cmax, warp_buf);
+  if (cmax > (uint32_t)kRankMaxBin) return false;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const uint32_t w = hist[tid * PER + q];
+    const uint32_t lo = run, hi = run + (w & 0xffffu);
+    run = hi + (w >> 16);
+    const uint32_t pw = lo | (hi << 16);
+    hist[tid * PER + q] = pw;  // bin starts
+    curs[tid * PER + q] = pw;
+  }
+  __syncthreads();
+  auto start = [&](int b) { return (hist[b >> 1] >> ((b & 1) * 16)) & 0xffffu; };
+  auto next = [&](int b) { return b + 1 < NB ? start(b + 1) : (uint32_t)n; };
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    if (e * THREADS + tid < n) {
+      const int b = bin_of(key[e]);
+      if (next(b) - start(b) > 1u) {
+        const uint32_t old = atomicAdd(&curs[b >> 1], 1u << ((b & 1) * 16));
+        kscr[(old >> ((b & 1) * 16)) & 0xffffu] = key[e];
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = e * THREADS + tid;
+    if (i < n) {
+      const int b = bin_of(key[e]);
+      const uint32_t base = start(b), end = next(b);
+      uint32_t cnt = 0;
+      if (end - base > 1u)
+        for (uint32_t q = base; q < end; ++q) cnt += kscr[q] < key[e];
+      out[i] = (uint16_t)(base + cnt);
+    }
+  }
+  __syncthreads();
+  return true;
+}
+
 // Rk (uint16, n x ld, row-major) of the layout keys ds (n x ld). Rank of a
 // sorted position = the last tie-group start at or before it (a max-scan of
 // the positions where the key changes). idx_scratch: 2 * kSeg uint16 per
 // CTA (two-segment rows only).
+constexpr int kRankBinThreads = 1024;
+
+// Fast-layout rows through rank_row_bins; rows it declines are appended to
+// (fail_rows, *fail_count) for row_rank_kernel.
+__global__ void __launch_bounds__(kRankBinThreads, 1)
+    row_rank_bins_kernel(const uint32_t* __restrict__ ds, int n, int ld, uint16_t* __restrict__ rk,
+                         int* __restrict__ fail_rows, int* __restrict__ fail_count) {
+  extern __shared__ __align__(128) uint8_t rank_smem[];
+  __shared__ uint32_t warp_buf[kRankBinThreads / 32];
+  uint32_t* hist = reinterpret_cast<uint32_t*>(rank_smem);
+  uint32_t* kscr = hist + kRankBins;  // after counts and cursors
+  for (int r = blockIdx.x; r < n; r += gridDim.x) {
+    if (!rank_row_bins<kRankBinThreads>(ds + (size_t)r * ld, n, rk + (size_t)r * ld, hist, hist + kRankBins / 2,
+                                        kscr, warp_buf)) {
+      if (threadIdx.x == 0) fail_rows[atomicAdd(fail_count, 1)] = r;
+      __syncthreads();
+    }
+  }
+}
+
+// Sort path: all rows (rows == nullptr) or the listed rows.
 template <int THREADS, int ITEMS>
 __global__ void __launch_bounds__(THREADS)
-    row_rank_kernel(const uint32_t* __restrict__ ds, int n, int ld, int end_bit, uint16_t* __restrict__ rk,
-                    uint16_t* __restrict__ idx_scratch) {
+    row_rank_kernel(const uint32_t* __restrict__ ds, int n, int ld, int end_bit, const int* __restrict__ rows,
+                    const int* __restrict__ row_count, uint16_t* __restrict__ rk, uint32_t* __restrict__ scratch) {
   using Cfg = RankCfg<THREADS, ITEMS>;
   constexpr int S = Cfg::kSeg;
   extern __shared__ __align__(128) uint8_t rank_smem[];
@@ -96,9 +243,13 @@ __global__ void __launch_bounds__(THREADS)
   __shared__ uint32_t last_key[THREADS / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nseg = n > S ? 2 : 1;
-  uint16_t* scr = idx_scratch + (size_t)blockIdx.x * 2 * S;
+  // per-CTA scratch: max(n, S) words (bin keys, or the two-segment indices)
+  uint32_t* kscr = scratch + (size_t)blockIdx.x * max(n, S);
+  uint16_t* scr = reinterpret_cast<uint16_t*>(kscr);
 
-  for (int r = blockIdx.x; r < n; r += gridDim.x) {
+  const int nrows = rows ? *row_count : n;
+  for (int ri = blockIdx.x; ri < nrows; ri += gridDim.x) {
+    const int r = rows ? rows[ri] : ri;
     const uint32_t* row = ds + (size_t)r * ld;
     uint16_t* out = rk + (size_t)r * ld;
     for (int h = 0; h < nseg; ++h) {
