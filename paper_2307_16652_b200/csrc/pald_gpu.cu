@@ -468,7 +468,7 @@ int launch_row_rank(pald_gpu_plan* p, uint16_t* rk, int end_bit, const int* rows
 
 // Builds RA / RB from the plan's layout of D, using W as the Rk scratch
 // (W is zeroed afterwards by the caller).
-int build_rank_codes(pald_gpu_plan* p, cudaStream_t s) {
+int build_rank_codes(pald_gpu_plan* p, cudaStream_t s, bool mark_ties) {
   if (!p->rank_a) {
     PALD_CUDA(cudaMalloc(&p->rank_a, p->n * p->ld * 4));
     PALD_CUDA(cudaMalloc(&p->rank_b, p->n * p->ld * 2));
@@ -491,8 +491,9 @@ int build_rank_codes(pald_gpu_plan* p, cudaStream_t s) {
       attr_done[p->device & 63] = true;
     }
     const int grid = (int)std::min<uint64_t>(p->n, (uint64_t)p->sms);
+    const TieMarks tm{mark_ties ? p->sym_masks : nullptr, (int)p->nb, p->sym_nch};
     row_rank_bins_kernel<<<grid, kRankBinThreads, kRankBinSmem, s>>>(p->ds, n, ld, rk, p->rank_fail + 1,
-                                                                      p->rank_fail);
+                                                                      p->rank_fail, tm);
     PALD_CUDA(cudaGetLastError());
     ++p->launches;
     rows = p->rank_fail + 1;
@@ -555,25 +556,32 @@ int plan_load_impl(pald_gpu_plan* p, const float* dD, uint64_t ldd, cudaStream_t
   PALD_CUDA(cudaGetLastError());
   ++p->launches;
   p->rank_ready = false;
-  if (rank_wanted(p)) {
-    const int rc = build_rank_codes(p, s);
+  p->sym_ready = false;
+  p->sym_marked = 0;
+  // Duplicate scan of the columns of D for the tile-pair cohesion kernel
+  // (pairwise; skipped where the pair kernel cannot win even tie-free).
+  const bool tie_scan = fast && p->sym_masks && sym_enabled() && sym_wins(p, 0.0);
+  const size_t mask_words = tie_scan ? sym_mask_words(p) : 0;
+  if (tie_scan) {
+    PALD_CUDA(cudaMemsetAsync(p->sym_masks, 0, mask_words * sizeof(uint32_t), s));
+    PALD_CUDA(cudaMemsetAsync(p->sym_tile_flags, 0, p->nb * sizeof(uint32_t), s));
+    PALD_CUDA(cudaMemsetAsync(p->sym_count, 0, sizeof(unsigned long long), s));
+  }
+  if (rank_wanted(p)) {  // on the fast layout this also marks the ties (bins kernel)
+    const int rc = build_rank_codes(p, s, tie_scan);
     if (rc) return rc;
   }
   PALD_CUDA(cudaMemsetAsync(p->u, 0, p->n * p->ld * 4, s));
   PALD_CUDA(cudaMemsetAsync(p->w, 0, p->n * p->ld * 4, s));
-  p->sym_ready = false;
-  p->sym_marked = 0;
   // Triplet: the pair kernel's shared indicator is exact without a scan
   // (its per-element chunks, those inside the row or column tile, cost too
   // little to enter the cost model: tools/time_n.py). Pairwise: the scan is
   // skipped where the pair kernel cannot win even tie-free.
   if (fast && p->algorithm == PALD_GPU_TRIPLET && sym_enabled() && sym_wins(p, 0.0)) p->sym_ready = true;
-  if (fast && p->sym_masks && sym_enabled() && sym_wins(p, 0.0)) {
-    // Duplicate scan of the columns of D for the tile-pair cohesion kernel.
-    const size_t words = sym_mask_words(p);
-    PALD_CUDA(cudaMemsetAsync(p->sym_masks, 0, words * sizeof(uint32_t), s));
-    PALD_CUDA(cudaMemsetAsync(p->sym_tile_flags, 0, p->nb * sizeof(uint32_t), s));
-    PALD_CUDA(cudaMemsetAsync(p->sym_count, 0, sizeof(unsigned long long), s));
+  if (tie_scan) {
+    const size_t words = mask_words;
+    // the rank-code bins kernel marked its rows: scan only the rows it declined
+    const bool by_rank = p->rank_ready && !p->exact;
     static bool attr_done[64] = {};
     if (!attr_done[p->device & 63]) {
       PALD_CUDA(cudaFuncSetAttribute(tie_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTieSmem));
@@ -581,7 +589,8 @@ int plan_load_impl(pald_gpu_plan* p, const float* dD, uint64_t ldd, cudaStream_t
     }
     const int passes = (int)((p->n + kTieCap * 3 / 4 - 1) / (kTieCap * 3 / 4));
     tie_scan_kernel<<<(unsigned)std::min<uint64_t>(p->n, (uint64_t)p->sms), kTieThreads, kTieSmem, s>>>(
-        p->ds, n, (int)p->ld, (int)p->nb, p->sym_nch, passes, p->sym_masks, p->sym_tile_flags);
+        p->ds, n, (int)p->ld, (int)p->nb, p->sym_nch, passes, p->sym_masks, p->sym_tile_flags,
+        by_rank ? p->rank_fail + 1 : nullptr, by_rank ? p->rank_fail : nullptr);
     PALD_CUDA(cudaGetLastError());
     tie_count_kernel<<<(unsigned)p->sms * 4, 256, 0, s>>>(p->sym_masks, words, p->sym_count);
     PALD_CUDA(cudaGetLastError());

@@ -33,14 +33,16 @@
 
 #include <cub/block/block_radix_sort.cuh>
 
+#include "pald_sym.cuh"  // tie masks of the tile-pair kernel (pair_index, kSymBK)
+
 namespace pald_gpu {
 
 constexpr int kRankMaxN = 32768;  // ranks < 2^15: one flag bit per 16-bit lane
 constexpr int kRankRadixBits = 6;   // 5 digit passes over 30-bit fast-path keys, 6 over 32
-constexpr int kRankBins = 16384;    // value-linear bins of the fast row path
+constexpr int kRankBins = 8192;     // value-linear bins of the fast row path
 constexpr int kRankMaxBin = 64;     // larger bins: the row takes the sort path
-// packed u16 counts + cursors, and the keys of multi-key bins
-constexpr int kRankBinSmem = kRankBins * 2 * 2 + kRankMaxN * 4;
+// packed u16 counts + cursors, and the keys + indices of multi-key bins
+constexpr int kRankBinSmem = kRankBins * 2 * 2 + kRankMaxN * (4 + 2);
 
 // Per-row sort configuration: THREADS x ITEMS keys per CUB block radix sort
 // (one "segment"); rows longer than one segment (n > 16384) are sorted as two
@@ -128,9 +130,21 @@ __device__ __forceinline__ uint32_t block_excl_sum(uint32_t v, uint32_t* warp_bu
 // keys, scattered into shared memory. The row stays in registers (thread t
 // holds elements t + e*THREADS). Returns false (row left to the sort path)
 // when a bin holds more than kRankMaxBin keys.
+//
+// Equal keys meet in one bin, so the bin scan also yields every duplicate
+// pair (a, b) of row j (= column j of the symmetric D): with tie masks
+// given, it marks third point k = b in tile pair {tile(j), tile(a)}
+// (element a's scan) and k = a in {tile(j), tile(b)} (element b's scan),
+// the marks of tie_scan_kernel (pald_sym.cuh) for this row.
+struct TieMarks {
+  uint32_t* masks;  // nullptr: no marking
+  int nb, nch;
+};
+
 template <int THREADS>
-__device__ bool rank_row_bins(const uint32_t* __restrict__ row, int n, uint16_t* __restrict__ out,
-                              uint32_t* hist, uint32_t* curs, uint32_t* kscr, uint32_t* warp_buf) {
+__device__ bool rank_row_bins(const uint32_t* __restrict__ row, int j, int n, uint16_t* __restrict__ out,
+                              uint32_t* hist, uint32_t* curs, uint32_t* kscr, uint16_t* kidx, uint32_t* warp_buf,
+                              const TieMarks& tm) {
   constexpr int NB = kRankBins, W = NB / 2, PER = W / THREADS, E = kRankMaxN / THREADS;
   const int tid = threadIdx.x;
   uint32_t key[E];
@@ -184,7 +198,9 @@ __device__ bool rank_row_bins(const uint32_t* __restrict__ row, int n, uint16_t*
       const int b = bin_of(key[e]);
       if (next(b) - start(b) > 1u) {
         const uint32_t old = atomicAdd(&curs[b >> 1], 1u << ((b & 1) * 16));
-        kscr[(old >> ((b & 1) * 16)) & 0xffffu] = key[e];
+        const uint32_t slot = (old >> ((b & 1) * 16)) & 0xffffu;
+        kscr[slot] = key[e];
+        kidx[slot] = (uint16_t)(e * THREADS + tid);
       }
     }
   }
@@ -196,8 +212,17 @@ __device__ bool rank_row_bins(const uint32_t* __restrict__ row, int n, uint16_t*
       const int b = bin_of(key[e]);
       const uint32_t base = start(b), end = next(b);
       uint32_t cnt = 0;
-      if (end - base > 1u)
-        for (uint32_t q = base; q < end; ++q) cnt += kscr[q] < key[e];
+      if (end - base > 1u) {
+        for (uint32_t q = base; q < end; ++q) {
+          const uint32_t kq = kscr[q];
+          cnt += kq < key[e];
+          if (kq == key[e] && tm.masks && kidx[q] != i) {
+            const int k = kidx[q], tj = j / kTile, ti = i / kTile;
+            atomicOr(&tm.masks[pair_index(min(tj, ti), max(tj, ti), tm.nb) * tm.nch + k / kSymBK],
+                     1u << (k % kSymBK));
+          }
+        }
+      }
       out[i] = (uint16_t)(base + cnt);
     }
   }
@@ -215,14 +240,15 @@ constexpr int kRankBinThreads = 1024;
 // (fail_rows, *fail_count) for row_rank_kernel.
 __global__ void __launch_bounds__(kRankBinThreads, 1)
     row_rank_bins_kernel(const uint32_t* __restrict__ ds, int n, int ld, uint16_t* __restrict__ rk,
-                         int* __restrict__ fail_rows, int* __restrict__ fail_count) {
+                         int* __restrict__ fail_rows, int* __restrict__ fail_count, TieMarks tm) {
   extern __shared__ __align__(128) uint8_t rank_smem[];
   __shared__ uint32_t warp_buf[kRankBinThreads / 32];
   uint32_t* hist = reinterpret_cast<uint32_t*>(rank_smem);
   uint32_t* kscr = hist + kRankBins;  // after counts and cursors
+  uint16_t* kidx = reinterpret_cast<uint16_t*>(kscr + kRankMaxN);
   for (int r = blockIdx.x; r < n; r += gridDim.x) {
-    if (!rank_row_bins<kRankBinThreads>(ds + (size_t)r * ld, n, rk + (size_t)r * ld, hist, hist + kRankBins / 2,
-                                        kscr, warp_buf)) {
+    if (!rank_row_bins<kRankBinThreads>(ds + (size_t)r * ld, r, n, rk + (size_t)r * ld, hist, hist + kRankBins / 2,
+                                        kscr, kidx, warp_buf, tm)) {
       if (threadIdx.x == 0) fail_rows[atomicAdd(fail_count, 1)] = r;
       __syncthreads();
     }

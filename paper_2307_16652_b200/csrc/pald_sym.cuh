@@ -99,7 +99,8 @@ __host__ __device__ __forceinline__ size_t pair_index(int P, int Q, int nb) {
 // column are bucketed in shared memory in turn and compared within buckets.
 __global__ void __launch_bounds__(kTieThreads)
     tie_scan_kernel(const uint32_t* __restrict__ d, int n, int ld, int nb, int nch, int passes,
-                    uint32_t* __restrict__ masks, uint32_t* __restrict__ tile_flags) {
+                    uint32_t* __restrict__ masks, uint32_t* __restrict__ tile_flags,
+                    const int* __restrict__ rows = nullptr, const int* __restrict__ row_count = nullptr) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint32_t* keys = reinterpret_cast<uint32_t*>(smem_raw);
   uint32_t* idx = keys + kTieCap;
@@ -108,7 +109,11 @@ __global__ void __launch_bounds__(kTieThreads)
   __shared__ uint32_t warp_sums[kTieThreads / 32];
   __shared__ int overflow;
   const int tid = threadIdx.x;
-  for (int j = blockIdx.x; j < n; j += gridDim.x) {
+  // all columns, or only the listed ones (rows the rank-code build left
+  // unmarked: pald_rank.cuh)
+  const int ncols = rows ? *row_count : n;
+  for (int jj = blockIdx.x; jj < ncols; jj += gridDim.x) {
+    const int j = rows ? rows[jj] : jj;
     const uint32_t* row = d + (size_t)j * ld;
     const int tj = j / kTile;
     for (int pass = 0; pass < passes; ++pass) {

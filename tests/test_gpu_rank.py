@@ -52,3 +52,21 @@ def test_rank_path_segments_sampled_rows(oracle, n, kind):
     ur, cr = oracle.pairwise_rows_f32(d, rows)
     assert np.array_equal(e.U[rows.tolist()].cpu().numpy(), ur)
     assert np.array_equal(e.C[rows.tolist()].cpu().numpy().view(np.uint32), cr.view(np.uint32))
+
+
+def test_bins_tie_marks_equal_tie_scan():
+    """The rank-code bins kernel marks the duplicate pairs of its rows for the
+    pair kernel instead of tie_scan_kernel: same marked share (a few
+    duplicates per column, no overflowing hash bucket) and, with the pair
+    kernel forced, C equal to the one-sided kernel bit for bit."""
+    script = Path(__file__).resolve().parent / "scripts" / "sym_vs_onesided.py"
+    shares = {}
+    for rank in ("0", "1"):
+        env = dict(os.environ, PALD_GPU_SYM="2", PALD_GPU_RANK=rank)
+        out = subprocess.run([sys.executable, str(script), "grid", "13001", "pairwise"], env=env,
+                             capture_output=True, text=True, timeout=900)
+        assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-3000:]
+        assert "same True" in out.stdout
+        shares[rank] = float(out.stdout.split("exact_step_share")[1].split()[0])
+    assert 0.0 < shares["1"] < 0.5
+    assert shares["0"] == shares["1"]
