@@ -31,6 +31,32 @@ def main():
             u_ref, c_ref = o.pairwise_f32(d, policy=0 if policy == "strict" else 1)
             assert np.array_equal(e.U.cpu().numpy(), u_ref), (seed, n, kind, policy)
             assert np.array_equal(e.C.cpu().numpy().view(np.uint32), c_ref.view(np.uint32)), (seed, n, kind, policy)
+    # fp32 conversions of valid double inputs with off-diagonal 0 and inf
+    # (test_gpu_parity.py::test_valid_double_inputs_that_degenerate_in_fp32):
+    # exact (integer-key) layout, ranks from the sort path
+    for extreme in ("underflow", "overflow", "both"):
+        n = 97
+        rng = np.random.default_rng(5)
+        d = np.zeros((n, n))
+        iu = np.triu_indices(n, 1)
+        v = rng.uniform(0.5, 2.0, iu[0].size)
+        pick = rng.random(iu[0].size)
+        if extreme in ("underflow", "both"):
+            v[pick < 0.1] = 1e-50 * (1 + pick[pick < 0.1])
+        if extreme in ("overflow", "both"):
+            v[pick > 0.9] = 1e300 * (1 + pick[pick > 0.9])
+        d[iu] = v
+        d[(iu[1], iu[0])] = v
+        d32 = d.astype(np.float32)
+        D = torch.from_numpy(d32).cuda()
+        for policy in ("strict", "split"):
+            e = Engine(n, "pairwise", policy=policy)
+            e.run(D)
+            torch.cuda.synchronize()
+            assert e.info()["rank_codes"] and e.exact_path
+            u_ref, c_ref = o.pairwise_f32(d32, policy=0 if policy == "strict" else 1)
+            assert np.array_equal(e.U.cpu().numpy(), u_ref), (extreme, policy)
+            assert np.array_equal(e.C.cpu().numpy(), c_ref, equal_nan=True), (extreme, policy)
     print("ok")
 
 
