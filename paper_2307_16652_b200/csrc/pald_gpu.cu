@@ -424,8 +424,9 @@ int plan_alloc(pald_gpu_plan* p) {
 
 int grid_rows(uint64_t n) { return (int)std::min<uint64_t>(n, 148ull * 16); }
 
-// Rank-coded pass 1 (pald_rank.cuh): pairwise focus with 2048 < n <= 32768
-// (below that the code build costs more than the faster pass 1 saves).
+// Rank-coded pass 1 (pald_rank.cuh): pairwise and triplet focus with
+// 2048 < n <= 32768 (below that the code build costs more than the faster
+// pass 1 saves).
 // PALD_GPU_RANK=0 keeps the fp32 / integer-key compare path everywhere, 2
 // forces the rank path for every n <= 32768 (A/B, tests).
 bool rank_wanted(const pald_gpu_plan* p) {
@@ -433,7 +434,8 @@ bool rank_wanted(const pald_gpu_plan* p) {
     const char* e = getenv("PALD_GPU_RANK");
     return e ? atoi(e) : 1;
   }();
-  if (m == 0 || p->algorithm != PALD_GPU_PAIRWISE || p->n < 2 || p->n > (uint64_t)kRankMaxN) return false;
+  if (m == 0 || p->n < 2 || p->n > (uint64_t)kRankMaxN) return false;
+  if (p->algorithm == PALD_GPU_TRIPLET && p->policy != PALD_GPU_STRICT) return false;
   return m == 2 || p->n > 2048;
 }
 
@@ -444,6 +446,21 @@ int ensure_rank_scratch(pald_gpu_plan* p, size_t words) {
   p->rank_scratch_words = 0;
   PALD_CUDA(cudaMalloc(&p->rank_scratch, words * 4));
   p->rank_scratch_words = words;
+  return PALD_GPU_OK;
+}
+
+// Bins path of the rank codes (fast layout): THREADS x E keys per row.
+template <int THREADS, int E>
+int launch_rank_bins(pald_gpu_plan* p, uint16_t* rk, const TieMarks& tm, cudaStream_t s) {
+  auto k = row_rank_bins_kernel<THREADS, E>;
+  const int n = (int)p->n, smem = rank_bin_smem(THREADS * E);
+  PALD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int per_sm = 1;
+  PALD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, THREADS, smem));
+  const int grid = std::min(n, p->sms * std::max(1, per_sm));
+  k<<<grid, THREADS, smem, s>>>(p->ds, n, (int)p->ld, rk, p->rank_fail + 1, p->rank_fail, tm);
+  PALD_CUDA(cudaGetLastError());
+  ++p->launches;
   return PALD_GPU_OK;
 }
 
@@ -485,17 +502,12 @@ int build_rank_codes(pald_gpu_plan* p, cudaStream_t s, bool mark_ties) {
   if (!p->exact) {  // value-linear bins (finite fp32 keys); declined rows -> sort path
     if (!p->rank_fail) PALD_CUDA(cudaMalloc(&p->rank_fail, (p->n + 1) * sizeof(int)));
     PALD_CUDA(cudaMemsetAsync(p->rank_fail, 0, sizeof(int), s));
-    static bool attr_done[64] = {};
-    if (!attr_done[p->device & 63]) {
-      PALD_CUDA(cudaFuncSetAttribute(row_rank_bins_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kRankBinSmem));
-      attr_done[p->device & 63] = true;
-    }
-    const int grid = (int)std::min<uint64_t>(p->n, (uint64_t)p->sms);
     const TieMarks tm{mark_ties ? p->sym_masks : nullptr, (int)p->nb, p->sym_nch};
-    row_rank_bins_kernel<<<grid, kRankBinThreads, kRankBinSmem, s>>>(p->ds, n, ld, rk, p->rank_fail + 1,
-                                                                      p->rank_fail, tm);
-    PALD_CUDA(cudaGetLastError());
-    ++p->launches;
+    rc = n <= 4096    ? launch_rank_bins<256, 16>(p, rk, tm, s)
+         : n <= 8192  ? launch_rank_bins<512, 16>(p, rk, tm, s)
+         : n <= 16384 ? launch_rank_bins<1024, 16>(p, rk, tm, s)
+                      : launch_rank_bins<1024, 32>(p, rk, tm, s);
+    if (rc) return rc;
     rows = p->rank_fail + 1;
     count = p->rank_fail;
   }
@@ -654,11 +666,13 @@ int plan_focus_counts_impl(pald_gpu_plan* p, uint64_t part, uint64_t parts, cuda
     ar.d = p->rank_a;
     const CUtensorMap &ra = p->tm_ra, &rb = p->tm_rb;
     if (peers)
-      rc = split ? launch_tile<0, false, false, true, false, true, false, kTile, false, true, true>(ra, rb, mw, ar, grid, s)
-                 : launch_tile<0, false, false, false, false, true, false, kTile, false, true, true>(ra, rb, mw, ar, grid, s);
+      rc = tri     ? launch_tile<0, true, true, true, false, true, false, kTile, false, true, true>(ra, rb, mw, ar, grid, s)
+           : split ? launch_tile<0, false, false, true, false, true, false, kTile, false, true, true>(ra, rb, mw, ar, grid, s)
+                   : launch_tile<0, false, false, false, false, true, false, kTile, false, true, true>(ra, rb, mw, ar, grid, s);
     else
-      rc = split ? launch_tile<0, false, false, true, false, true, false, kTile, false, false, true>(ra, rb, mw, ar, grid, s)
-                 : launch_tile<0, false, false, false, false, true, false, kTile, false, false, true>(ra, rb, mw, ar, grid, s);
+      rc = tri     ? launch_tile<0, true, true, true, false, true, false, kTile, false, false, true>(ra, rb, mw, ar, grid, s)
+           : split ? launch_tile<0, false, false, true, false, true, false, kTile, false, false, true>(ra, rb, mw, ar, grid, s)
+                   : launch_tile<0, false, false, false, false, true, false, kTile, false, false, true>(ra, rb, mw, ar, grid, s);
   } else if (peers) {  // counts RED'd straight into every rank's W over NVLink
     if (!p->exact) {
       rc = tri     ? launch_tile<0, true, true, true, false, true, false, kTile, false, true>(md, mn, mw, a, grid, s)

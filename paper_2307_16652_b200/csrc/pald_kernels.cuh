@@ -382,6 +382,44 @@ __device__ __forceinline__ void k_step_rank(const uint32_t* __restrict__ sa, con
   }
 }
 
+// Rank-coded k step with per-element strictness (triplet focus, chunks
+// inside the row or column tile): output (r, c), third point z = kg. With
+// T' = nu(d_rc), [nu(A) < T'] = [A < T] (strict) and [A < T'] = [A <= T], so
+// the A test is strict iff z < c (A' = nu(A)) and <= otherwise; the B test
+// strict iff z < r (reference.hpp:171-180). thr holds the strict thresholds
+// for the per-element side(s); a <= test subtracts one more from its lane.
+template <int TT = 8>
+__device__ __forceinline__ void k_step_rank_sel(const uint32_t* __restrict__ sa, const uint16_t* __restrict__ sb,
+                                                int kk, int kg, int ty, int tx, int r0, int c0, bool a_in, bool b_in,
+                                                const float2 (&thr)[TT][TT / 2], float2 (&acc)[TT][TT / 2]) {
+  const uint4 a0 = reinterpret_cast<const uint4*>(sa + kk * kTile)[ty];
+  const uint4 a1 = reinterpret_cast<const uint4*>(sa + kk * kTile)[16 + ty];
+  const uint2 b0 = reinterpret_cast<const uint2*>(sb + kk * kTile)[tx];
+  const uint2 b1 = reinterpret_cast<const uint2*>(sb + kk * kTile)[16 + tx];
+  const uint32_t a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+  const uint32_t b[4] = {b0.x, b0.y, b1.x, b1.y};
+  uint32_t ma[4], mb[8];
+#pragma unroll
+  for (int jp = 0; jp < 4; ++jp)
+    ma[jp] = a_in ? ((kg >= c0 + row_off<kTile>(tx, 2 * jp) ? 1u : 0u) |
+                     (kg >= c0 + row_off<kTile>(tx, 2 * jp + 1) ? 0x10000u : 0u))
+                  : 0u;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) mb[i] = (b_in && kg >= r0 + row_off<kTile>(ty, i)) ? 0x10001u : 0u;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+#pragma unroll
+    for (int jp = 0; jp < 4; ++jp) {
+      const uint32_t x1 = a[i] + __float_as_uint(thr[i][jp].x) - ma[jp];
+      const uint32_t x2 = b[jp] + __float_as_uint(thr[i][jp].y) - mb[i];
+      const uint32_t f = ~(x1 & x2) & 0x80008000u;
+      uint32_t sum;
+      asm("mad.hi.u32 %0, %1, 0x20000, %2;" : "=r"(sum) : "r"(f), "r"(__float_as_uint(acc[i][jp].x)));
+      acc[i][jp].x = __uint_as_float(sum);
+    }
+  }
+}
+
 // Focus-finish tile index -> (tile row, tile col): upper-triangular tiles in
 // row-major order.
 __device__ __forceinline__ void tri_coords(int t, int nb, int& tr, int& tc) {
@@ -598,13 +636,16 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE))
       for (int jp = 0; jp < TT / 2; ++jp) {
         uint32_t t2[2];
         if constexpr (RANK) {  // args.d = RA: Rk[r][c] = RA[c][r] & 0x7fff
+          // pairwise: T_NU (InclusiveSplit) tests <= everywhere; triplet
+          // (A_NU, B_NU): strict base thresholds, <= chosen per chunk below
+          constexpr uint32_t plus = (T_NU && !A_NU) ? 1u : 0u;
           uint32_t rr = 0, cr = 0;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int r = r0 + row_off<TILE>(ty, i), c = c0 + row_off<TILE>(tx, 2 * jp + h);
             if (r < n && c < n) {
-              const uint32_t t_rc = (__ldg(args.d + (size_t)c * ld + r) & 0x7fffu) + (T_NU ? 1u : 0u);
-              const uint32_t t_cr = (__ldg(args.d + (size_t)r * ld + c) & 0x7fffu) + (T_NU ? 1u : 0u);
+              const uint32_t t_rc = (__ldg(args.d + (size_t)c * ld + r) & 0x7fffu) + plus;
+              const uint32_t t_cr = (__ldg(args.d + (size_t)r * ld + c) & 0x7fffu) + plus;
               rr |= t_rc << (16 * h);
               cr |= t_cr << (16 * h);
             }
@@ -630,6 +671,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE))
       }
     }
 
+    int le_a = 0, le_b = 0;  // rank-coded triplet: thresholds currently shifted for <=
     for (int ch = ch_begin; ch < ch_end; ++ch, ++p) {
       const int s = p % kStages;
       mbar_wait(&full_bar[s], (p / kStages) & 1);
@@ -644,7 +686,24 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE))
       if constexpr (RANK) {
         const uint32_t* ra = reinterpret_cast<const uint32_t*>(st);
         const uint16_t* rb = reinterpret_cast<const uint16_t*>(st + BOX);
-        if (kmax == kBK) {
+        if constexpr (A_NU) {  // triplet: strictness by the chunk's place (see k_step_rank_sel)
+          const int k1 = k0 + kBK;
+          const int want_a = (!a_in && k1 > c0) ? 1 : 0, want_b = (!b_in && k1 > r0) ? 1 : 0;
+          if (want_a != le_a || want_b != le_b) {
+            const uint32_t da = (uint32_t)(le_a - want_a) * 0x10001u, db = (uint32_t)(le_b - want_b) * 0x10001u;
+#pragma unroll
+            for (int i = 0; i < TT; ++i)
+#pragma unroll
+              for (int jp = 0; jp < TT / 2; ++jp)
+                thr[i][jp] = make_float2(__uint_as_float(__float_as_uint(thr[i][jp].x) + da),
+                                         __uint_as_float(__float_as_uint(thr[i][jp].y) + db));
+            le_a = want_a;
+            le_b = want_b;
+          }
+        }
+        if (a_in || b_in) {
+          for (int kk = 0; kk < kmax; ++kk) k_step_rank_sel(ra, rb, kk, k0 + kk, ty, tx, r0, c0, a_in, b_in, thr, acc);
+        } else if (kmax == kBK) {
 #pragma unroll kKUnroll
           for (int kk = 0; kk < kBK; ++kk) k_step_rank(ra, rb, kk, ty, tx, thr, acc);
         } else {

@@ -42,7 +42,7 @@ constexpr int kRankRadixBits = 6;   // 5 digit passes over 30-bit fast-path keys
 constexpr int kRankBins = 8192;     // value-linear bins of the fast row path
 constexpr int kRankMaxBin = 64;     // larger bins: the row takes the sort path
 // packed u16 counts + cursors, and the keys + indices of multi-key bins
-constexpr int kRankBinSmem = kRankBins * 2 * 2 + kRankMaxN * (4 + 2);
+__host__ __device__ constexpr int rank_bin_smem(int keys) { return kRankBins * 2 * 2 + keys * (4 + 2); }
 
 // Per-row sort configuration: THREADS x ITEMS keys per CUB block radix sort
 // (one "segment"); rows longer than one segment (n > 16384) are sorted as two
@@ -141,11 +141,11 @@ struct TieMarks {
   int nb, nch;
 };
 
-template <int THREADS>
+template <int THREADS, int E>
 __device__ bool rank_row_bins(const uint32_t* __restrict__ row, int j, int n, uint16_t* __restrict__ out,
                               uint32_t* hist, uint32_t* curs, uint32_t* kscr, uint16_t* kidx, uint32_t* warp_buf,
                               const TieMarks& tm) {
-  constexpr int NB = kRankBins, W = NB / 2, PER = W / THREADS, E = kRankMaxN / THREADS;
+  constexpr int NB = kRankBins, W = NB / 2, PER = W / THREADS;  // E * THREADS >= n keys
   const int tid = threadIdx.x;
   uint32_t key[E];
   uint32_t mx = 0;
@@ -234,21 +234,21 @@ __device__ bool rank_row_bins(const uint32_t* __restrict__ row, int j, int n, ui
 // sorted position = the last tie-group start at or before it (a max-scan of
 // the positions where the key changes). idx_scratch: 2 * kSeg uint16 per
 // CTA (two-segment rows only).
-constexpr int kRankBinThreads = 1024;
-
-// Fast-layout rows through rank_row_bins; rows it declines are appended to
+// Fast-layout rows through rank_row_bins (THREADS threads, E keys each, per
+// row; several rows per SM for small n); rows it declines are appended to
 // (fail_rows, *fail_count) for row_rank_kernel.
-__global__ void __launch_bounds__(kRankBinThreads, 1)
+template <int THREADS, int E>
+__global__ void __launch_bounds__(THREADS)
     row_rank_bins_kernel(const uint32_t* __restrict__ ds, int n, int ld, uint16_t* __restrict__ rk,
                          int* __restrict__ fail_rows, int* __restrict__ fail_count, TieMarks tm) {
   extern __shared__ __align__(128) uint8_t rank_smem[];
-  __shared__ uint32_t warp_buf[kRankBinThreads / 32];
+  __shared__ uint32_t warp_buf[THREADS / 32];
   uint32_t* hist = reinterpret_cast<uint32_t*>(rank_smem);
   uint32_t* kscr = hist + kRankBins;  // after counts and cursors
-  uint16_t* kidx = reinterpret_cast<uint16_t*>(kscr + kRankMaxN);
+  uint16_t* kidx = reinterpret_cast<uint16_t*>(kscr + E * THREADS);
   for (int r = blockIdx.x; r < n; r += gridDim.x) {
-    if (!rank_row_bins<kRankBinThreads>(ds + (size_t)r * ld, r, n, rk + (size_t)r * ld, hist, hist + kRankBins / 2,
-                                        kscr, kidx, warp_buf, tm)) {
+    if (!rank_row_bins<THREADS, E>(ds + (size_t)r * ld, r, n, rk + (size_t)r * ld, hist, hist + kRankBins / 2,
+                                   kscr, kidx, warp_buf, tm)) {
       if (threadIdx.x == 0) fail_rows[atomicAdd(fail_count, 1)] = r;
       __syncthreads();
     }

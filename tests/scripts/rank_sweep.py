@@ -2,7 +2,8 @@
 forced (the launcher reads it once per process): the randomized case sweep of
 test_gpu_parity.py (ragged sizes, uniform / integer / grid-point ties, wide
 ranges; fast and exact layouts) through the pairwise kernels, strict and
-InclusiveSplit, U and C bit-exact against the oracle."""
+InclusiveSplit, U and C bit-exact against the oracle, and the triplet
+kernels (U exact, C within 1e-5 of the fp64 oracle)."""
 import sys
 from pathlib import Path
 
@@ -13,6 +14,7 @@ ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 
+from helpers import max_rel_diff  # noqa: E402
 from oracle.oracle import Oracle  # noqa: E402
 from paper_2307_16652_b200.engine import Engine  # noqa: E402
 from test_gpu_parity import _random_case  # noqa: E402
@@ -31,6 +33,12 @@ def main():
             u_ref, c_ref = o.pairwise_f32(d, policy=0 if policy == "strict" else 1)
             assert np.array_equal(e.U.cpu().numpy(), u_ref), (seed, n, kind, policy)
             assert np.array_equal(e.C.cpu().numpy().view(np.uint32), c_ref.view(np.uint32)), (seed, n, kind, policy)
+        e = Engine(n, "triplet", force_exact=bool(seed % 2))
+        e.run(D)
+        torch.cuda.synchronize()
+        u_ref, c_ref = o.triplet_f64(d)
+        assert np.array_equal(e.U.cpu().numpy(), u_ref), (seed, n, kind, "triplet")
+        assert max_rel_diff(e.C.cpu().numpy(), c_ref) <= 1e-5, (seed, n, kind, "triplet")
     # fp32 conversions of valid double inputs with off-diagonal 0 and inf
     # (test_gpu_parity.py::test_valid_double_inputs_that_degenerate_in_fp32):
     # exact (integer-key) layout, ranks from the sort path
