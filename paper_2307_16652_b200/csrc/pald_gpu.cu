@@ -275,6 +275,13 @@ struct pald_gpu_plan {
   int2* tail64 = nullptr;        // 64-wide one-sided tiles of the last partial pair round
   int tail64_count = 0;
   int sym_main_pairs = 0;        // pairs of the full-range pair launch (rest: tail64)
+  // Triplet pass 2 with the last partial round of pairs split along k
+  // (pald_sym.cuh SPLIT items + sym_combine_kernel); built on first use.
+  int4* split_items = nullptr;
+  int4* split_pairs = nullptr;
+  float* split_partial = nullptr;
+  int split_item_count = -1;     // -1: not built; 0: no split
+  int split_pair_count = 0;
   uint64_t launches = 0;
 
   void close_peers() {
@@ -311,6 +318,9 @@ struct pald_gpu_plan {
     cudaFree(rank_b);
     cudaFree(rank_scratch);
     cudaFree(rank_fail);
+    cudaFree(split_items);
+    cudaFree(split_pairs);
+    cudaFree(split_partial);
     cudaSetDevice(prev);
   }
 };
@@ -339,6 +349,14 @@ int sym_mode() {
   return m;
 }
 bool sym_enabled() { return sym_mode() != 0; }
+// PALD_GPU_SPLIT=0 keeps the triplet pass 2 on whole pairs (A/B, tests).
+bool split_enabled() {
+  static const int m = [] {
+    const char* e = getenv("PALD_GPU_SPLIT");
+    return e ? atoi(e) : 1;
+  }();
+  return m != 0;
+}
 
 size_t sym_mask_words(const pald_gpu_plan* p) { return p->nb * (p->nb + 1) / 2 * p->sym_nch; }
 
@@ -806,6 +824,74 @@ int launch_sym(pald_gpu_plan* p, int t0, int t1, cudaStream_t s, bool peers = fa
   return PALD_GPU_OK;
 }
 
+// Triplet C is compared with a tolerance (the reference's own fp32 triplet C
+// depends on its block size), so the pairs of the last partial round of the
+// full-range pair launch can be split along k into f parts whose partial
+// tiles are summed in a fixed order: ceil(L f / G) / f rounds instead of 1.
+int build_split(pald_gpu_plan* p) {
+  p->split_item_count = 0;
+  const std::vector<int2>& order = p->pair_order;
+  const int G = p->sms, pairs = (int)order.size(), L = pairs % G;
+  if (pairs <= G || L == 0) return PALD_GPU_OK;
+  int best_f = 1;
+  double best = 1.0;
+  for (int f = 2; f <= 8 && f <= p->sym_nch; ++f) {
+    const double cost = std::ceil((double)L * f / G) / f;
+    if (cost < best - 1e-9) {
+      best = cost;
+      best_f = f;
+    }
+  }
+  if (best > 0.9) return PALD_GPU_OK;
+  const int f = best_f, nch = p->sym_nch;
+  std::vector<int4> items;
+  std::vector<int4> sp;
+  for (int i = 0; i < pairs - L; ++i) items.push_back(make_int4(order[i].x, order[i].y, nch << 16, -1));
+  for (int j = 0; j < L; ++j) {
+    const int2 pr = order[pairs - L + j];
+    sp.push_back(make_int4(pr.x, pr.y, j * f, f));
+    for (int q = 0; q < f; ++q) {
+      const int cb = nch * q / f, ce = nch * (q + 1) / f;
+      items.push_back(make_int4(pr.x, pr.y, cb | (ce << 16), j * f + q));
+    }
+  }
+  PALD_CUDA(cudaMalloc(&p->split_items, items.size() * sizeof(int4)));
+  PALD_CUDA(cudaMemcpy(p->split_items, items.data(), items.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  PALD_CUDA(cudaMalloc(&p->split_pairs, sp.size() * sizeof(int4)));
+  PALD_CUDA(cudaMemcpy(p->split_pairs, sp.data(), sp.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  PALD_CUDA(cudaMalloc(&p->split_partial, (size_t)L * f * 2 * kTile * kTile * sizeof(float)));
+  p->split_item_count = (int)items.size();
+  p->split_pair_count = L;
+  return PALD_GPU_OK;
+}
+
+// Full-range triplet pass 2 through the split items; false if no split.
+int launch_sym_split(pald_gpu_plan* p, cudaStream_t s, bool* used) {
+  *used = false;
+  if (p->split_item_count < 0) {
+    const int rc = build_split(p);
+    if (rc) return rc;
+  }
+  if (p->split_item_count == 0) return PALD_GPU_OK;
+  static bool attr_done[64] = {};
+  auto k = pald_sym_cohesion_kernel<true, false, false, true>;
+  if (!attr_done[p->device & 63]) {
+    PALD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
+    attr_done[p->device & 63] = true;
+  }
+  SymArgs a{p->ds, p->c, p->focus_tiles, p->sym_masks, p->sym_tile_flags, (int)p->n, (int)p->ld, (int)p->nb,
+            p->sym_nch, 0, p->split_item_count, p->peer_c, nullptr, p->split_items, p->split_partial};
+  const int grid = std::min(p->split_item_count, p->sms);
+  k<<<grid, kThreads, kSymSmem, s>>>(p->tm_d32, p->tm_dnu32, p->tm_w32, a);
+  PALD_CUDA(cudaGetLastError());
+  sym_combine_kernel<<<dim3((unsigned)p->split_pair_count, 2, kTile / 8), 256, 0, s>>>(
+      p->split_pairs, p->split_partial, p->c, (int)p->n, (int)p->ld);
+  PALD_CUDA(cudaGetLastError());
+  p->launches += 2;
+  *used = true;
+  return PALD_GPU_OK;
+}
+
 // Rounds-based cost model (in one-sided 128-tile times): a pair does twice
 // the outputs at ~1.44x the time of a one-sided tile (tools/microbench3.cu),
 // its exact k steps ~2.45x slower than shared ones (measured on all-tied
@@ -833,6 +919,15 @@ int plan_cohesion_impl(pald_gpu_plan* p, uint64_t row0, uint64_t row1, cudaStrea
   // identical: every C entry is the same in-order sum either way.
   const uint64_t tiles128 = ((row1 - row0 + kTile - 1) / kTile) * p->nb;
   if (row0 == 0 && row1 == p->n && p->sym_ready && sym_preferred(p)) {
+    if (p->algorithm == PALD_GPU_TRIPLET && split_enabled()) {
+      bool used = false;
+      const int rc = launch_sym_split(p, s, &used);
+      if (rc) return rc;
+      if (used) {
+        p->last_kernel = PALD_GPU_KERNEL_PAIRS;
+        return PALD_GPU_OK;
+      }
+    }
     int rc = launch_sym(p, 0, p->sym_main_pairs, s);
     if (rc == PALD_GPU_OK) {
       ++p->launches;

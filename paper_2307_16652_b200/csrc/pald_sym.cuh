@@ -76,6 +76,11 @@ struct SymArgs {
   int tile_begin, tile_end;   // share of the tile-pair list
   PeerBufs peers;             // PEERS: every C entry is stored to every rank's C
   unsigned int* round_bar;    // SYNC kernels: all CTAs start each full round together
+  // SPLIT kernels (triplet): work items (tile row, tile col, chunk_begin |
+  // chunk_end << 16, slot) replace whole pairs; slot >= 0 items write their
+  // partial tiles to partial[slot] (2 x 128 x 128 floats) for sym_combine_kernel.
+  const int4* items;
+  float* partial;
 };
 
 // Full-avalanche mix (murmur3 finalizer): the bucket takes the low bits and
@@ -380,7 +385,7 @@ __device__ __forceinline__ void store_c4(const SymArgs& a, size_t off, float4 v)
 // 3-stage TMA/mbarrier pipeline (four 32 x 128 boxes per stage) and writes
 // C[P rows][Q cols] and, for P < Q, C[Q rows][P cols]. Pairwise Strict
 // (TRI = false) or triplet cohesion on the fast (scaled fp32) layout.
-template <bool TRI, bool PEERS = false, bool SYNC = false>
+template <bool TRI, bool PEERS = false, bool SYNC = false, bool SPLIT = false>
 __global__ void __launch_bounds__(kThreads, 1)
     pald_sym_cohesion_kernel(const __grid_constant__ CUtensorMap tm_d,
                              const __grid_constant__ CUtensorMap tm_dnu,
@@ -395,7 +400,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int G = gridDim.x, g = blockIdx.x;
   const int first = args.tile_begin + g;
   const int R = first < args.tile_end ? (args.tile_end - 1 - first) / G + 1 : 0;
-  const int P = R * nch;
+  // item ri of this CTA: tile pair and chunk range [cb, ce) (whole pairs
+  // unless SPLIT)
+  auto item = [&](int ri, int2& tp, int& cb, int& ce, int& slot) {
+    if constexpr (SPLIT) {
+      const int4 it = args.items[first + ri * G];
+      tp = make_int2(it.x, it.y);
+      cb = it.z & 0xffff;
+      ce = it.z >> 16;
+      slot = it.w;
+    } else {
+      tp = args.tiles[first + ri * G];
+      cb = 0;
+      ce = nch;
+      slot = -1;
+    }
+  };
+  int P = R * nch;
+  if constexpr (SPLIT) {
+    P = 0;
+    for (int ri = 0; ri < R; ++ri) {
+      int2 tp;
+      int cb, ce, sl;
+      item(ri, tp, cb, ce, sl);
+      P += ce - cb;
+    }
+  }
   if (P <= 0) return;
   if (tid == 0) {
     for (int s = 0; s < kSymStages; ++s) {
@@ -407,7 +437,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
 
   auto issue = [&](int ri, int ch, int s) {
-    const int2 tp = args.tiles[first + ri * G];
+    int2 tp;
+    int cb_, ce_, sl_;
+    item(ri, tp, cb_, ce_, sl_);
     const int r0 = tp.x * kTile, c0 = tp.y * kTile, k0 = ch * kSymBK;
     uint8_t* st = smem + s * kSymStageBytes;
     const int k1 = min(k0 + kSymBK, n);
@@ -420,11 +452,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_load_2d(st + 2 * kSymBox, &tm_w, r0, k0, &full_bar[s]);
     tma_load_2d(st + 3 * kSymBox, &tm_w, c0, k0, &full_bar[s]);
   };
-  int pr_ri = 0, pr_ch = 0;
+  int pr_ri = 0, pr_ch = 0, pr_end = nch;
+  if constexpr (SPLIT) {
+    int2 tp;
+    int sl;
+    item(0, tp, pr_ch, pr_end, sl);
+  }
   auto pr_advance = [&]() {
-    if (++pr_ch == nch) {
-      pr_ch = 0;
+    if (++pr_ch == pr_end) {
       ++pr_ri;
+      if constexpr (SPLIT) {
+        if (pr_ri < R) {
+          int2 tp;
+          int sl;
+          item(pr_ri, tp, pr_ch, pr_end, sl);
+        }
+      } else {
+        pr_ch = 0;
+      }
     }
   };
   for (int p = 0; p < kSymStages && p < P; ++p) {
@@ -438,7 +483,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   int p = 0;
   for (int ri = 0; ri < R; ++ri) {
-    const int2 tp = args.tiles[first + ri * G];
+    int2 tp;
+    int ch_b, ch_e, slot;
+    item(ri, tp, ch_b, ch_e, slot);
     const int r0 = tp.x * kTile, c0 = tp.y * kTile;
     const bool diag = tp.x == tp.y;
     const uint32_t* mk = TRI ? nullptr : args.masks + pair_index(tp.x, tp.y, args.nb) * nch;
@@ -461,7 +508,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         act[i][jp] = make_float2(0.f, 0.f);
       }
     }
-    for (int ch = 0; ch < nch; ++ch, ++p) {
+    for (int ch = ch_b; ch < ch_e; ++ch, ++p) {
       const int s = p % kSymStages;
       mbar_wait(&full_bar[s], (p / kSymStages) & 1);
       const uint8_t* st = smem + s * kSymStageBytes;
@@ -502,6 +549,40 @@ __global__ void __launch_bounds__(kThreads, 1)
           issue(pr_ri, pr_ch, s);
         pr_advance();
       }
+    }
+    if (SPLIT && slot >= 0) {  // partial tiles: [0] rows of P x cols of Q, [1] rows of Q x cols of P
+      float* pt = args.partial + (size_t)slot * 2 * kTile * kTile;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int rl = row_off<kTile>(ty, i);
+        if (TRI && diag) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (row_off<kTile>(tx, j) != rl) continue;
+            if (j & 1)
+              acc[i][j >> 1].y = 0.f;
+            else
+              acc[i][j >> 1].x = 0.f;
+          }
+        }
+        *reinterpret_cast<float4*>(pt + rl * kTile + tx * 4) =
+            make_float4(acc[i][0].x, acc[i][0].y, acc[i][1].x, acc[i][1].y);
+        *reinterpret_cast<float4*>(pt + rl * kTile + 64 + tx * 4) =
+            make_float4(acc[i][2].x, acc[i][2].y, acc[i][3].x, acc[i][3].y);
+      }
+      if (!diag) {
+        float* pq = pt + kTile * kTile;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int cl = row_off<kTile>(tx, j), jp = j >> 1;
+          float v[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[i] = (j & 1) ? act[i][jp].y : act[i][jp].x;
+          *reinterpret_cast<float4*>(pq + cl * kTile + ty * 4) = make_float4(v[0], v[1], v[2], v[3]);
+          *reinterpret_cast<float4*>(pq + cl * kTile + 64 + ty * 4) = make_float4(v[4], v[5], v[6], v[7]);
+        }
+      }
+      continue;
     }
     // ---- flush: C[r][c] (rows of P, columns of Q) ------------------------
 #pragma unroll
@@ -567,6 +648,37 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __syncthreads();
     }
+  }
+}
+
+// Sum of the split items' partial tiles, in slot order (deterministic), into
+// C. One CTA per (split pair, tile half, 8 rows): pairs[q] = (tile row,
+// tile col, first slot, parts).
+__global__ void __launch_bounds__(256)
+    sym_combine_kernel(const int4* __restrict__ pairs, const float* __restrict__ partial, float* __restrict__ c,
+                       int n, int ld) {
+  const int q = blockIdx.x, half = blockIdx.y;
+  const int4 pr = pairs[q];
+  if (half == 1 && pr.x == pr.y) return;  // diagonal pair: one tile
+  const int rl = blockIdx.z * 8 + (threadIdx.x >> 5), cl = (threadIdx.x & 31) * 4;
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int t = 0; t < pr.w; ++t) {
+    const float4 v = *reinterpret_cast<const float4*>(partial + ((size_t)(pr.z + t) * 2 + half) * kTile * kTile +
+                                                      rl * kTile + cl);
+    s.x += v.x;
+    s.y += v.y;
+    s.z += v.z;
+    s.w += v.w;
+  }
+  const int row = (half ? pr.y : pr.x) * kTile + rl, col = (half ? pr.x : pr.y) * kTile + cl;
+  if (row >= n) return;
+  float* dst = c + (size_t)row * ld + col;
+  if (col + 3 < n) {
+    *reinterpret_cast<float4*>(dst) = s;
+  } else {
+    if (col < n) dst[0] = s.x;
+    if (col + 1 < n) dst[1] = s.y;
+    if (col + 2 < n) dst[2] = s.z;
   }
 }
 
