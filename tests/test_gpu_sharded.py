@@ -1,7 +1,8 @@
 """The multi-rank path with the real GPU engine (torchrun, gloo, ranks
 sharing cuda:0): results bit-identical to one process. Tied integer data
 takes the one-sided kernel's row bands; random data with PALD_GPU_SYM=2
-the pair kernel's tile-pair shares."""
+the pair kernel's tile-pair shares. PALD_GPU_SPLIT=0 keeps the
+single-process triplet reference on whole pairs (the shares never split)."""
 import os
 import socket
 import subprocess
@@ -29,6 +30,9 @@ def _port():
     (2, 700, "pairwise", "rand", "fused"), (3, 1000, "pairwise", "rand", "fused"),
     (2, 700, "pairwise", "ties", "fused"), (3, 513, "triplet", "rand", "fused"),
     (4, 1500, "pairwise", "rand", "fused"),
+    # n > 2048: pass 1 on rank codes (built on every rank), shares of its units
+    (2, 2500, "pairwise", "rand", "collectives"), (3, 2500, "pairwise", "rand", "fused"),
+    (2, 2500, "triplet", "rand", "fused"),
 ])
 def test_sharded_real_engine(world, n, alg, kind, mode):
     """mode "fused": pass-1 counts and pass-2 entries written into every
@@ -37,7 +41,7 @@ def test_sharded_real_engine(world, n, alg, kind, mode):
     rank: the ranks are ordered by host barriers between the kernels."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", f"--master-port={_port()}", str(SCRIPT), str(n), alg, kind, mode]
-    env = dict(os.environ, PALD_GPU_SYM="2")
+    env = dict(os.environ, PALD_GPU_SYM="2", PALD_GPU_SPLIT="0")
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     assert "ok [1, 1]" in out.stdout
