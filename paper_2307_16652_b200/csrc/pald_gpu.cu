@@ -520,7 +520,7 @@ int build_rank_codes(pald_gpu_plan* p, cudaStream_t s, bool mark_ties) {
   if (!p->exact) {  // value-linear bins (finite fp32 keys); declined rows -> sort path
     if (!p->rank_fail) PALD_CUDA(cudaMalloc(&p->rank_fail, (p->n + 1) * sizeof(int)));
     PALD_CUDA(cudaMemsetAsync(p->rank_fail, 0, sizeof(int), s));
-    const TieMarks tm{mark_ties ? p->sym_masks : nullptr, (int)p->nb, p->sym_nch};
+    const TieMarks tm{mark_ties ? p->sym_masks : nullptr, p->sym_tile_flags, (int)p->nb, p->sym_nch};
     rc = n <= 4096    ? launch_rank_bins<256, 16>(p, rk, tm, s)
          : n <= 8192  ? launch_rank_bins<512, 16>(p, rk, tm, s)
          : n <= 16384 ? launch_rank_bins<1024, 16>(p, rk, tm, s)

@@ -39,10 +39,11 @@ namespace pald_gpu {
 
 constexpr int kRankMaxN = 32768;  // ranks < 2^15: one flag bit per 16-bit lane
 constexpr int kRankRadixBits = 6;   // 5 digit passes over 30-bit fast-path keys, 6 over 32
-constexpr int kRankBins = 8192;     // value-linear bins of the fast row path
+constexpr int kRankBins = 16384;    // value-linear bins of the fast row path
 constexpr int kRankMaxBin = 64;     // larger bins: the row takes the sort path
-// packed u16 counts + cursors, and the keys + indices of multi-key bins
-__host__ __device__ constexpr int rank_bin_smem(int keys) { return kRankBins * 2 * 2 + keys * (4 + 2); }
+// packed u16 counts + cursors, and the keys of multi-key bins (their
+// indices, read only on a tie, go to a per-CTA global scratch)
+__host__ __device__ constexpr int rank_bin_smem(int keys) { return kRankBins * 2 * 2 + keys * 4; }
 
 // Per-row sort configuration: THREADS x ITEMS keys per CUB block radix sort
 // (one "segment"); rows longer than one segment (n > 16384) are sorted as two
@@ -131,20 +132,24 @@ __device__ __forceinline__ uint32_t block_excl_sum(uint32_t v, uint32_t* warp_bu
 // holds elements t + e*THREADS). Returns false (row left to the sort path)
 // when a bin holds more than kRankMaxBin keys.
 //
-// Equal keys meet in one bin, so the bin scan also yields every duplicate
-// pair (a, b) of row j (= column j of the symmetric D): with tie masks
-// given, it marks third point k = b in tile pair {tile(j), tile(a)}
-// (element a's scan) and k = a in {tile(j), tile(b)} (element b's scan),
-// the marks of tie_scan_kernel (pald_sym.cuh) for this row.
+// Equal keys meet in one bin, so the bin scan also finds every key of row j
+// (= column j of the symmetric D) that occurs more than once. With tie masks
+// given, those keys and their indices are collected (kTieList entries per
+// row; more flag the whole tile, like tie_scan_kernel's overflow), and for
+// every duplicate pair (a, b) third point k = b is marked in tile pair
+// {tile(j), tile(a)} and k = a in {tile(j), tile(b)}: the marks of
+// tie_scan_kernel (pald_sym.cuh) for this row.
 struct TieMarks {
-  uint32_t* masks;  // nullptr: no marking
+  uint32_t* masks;       // nullptr: no marking
+  uint32_t* tile_flags;  // [nb]: the whole tile marked
   int nb, nch;
 };
+constexpr int kTieList = 1024;
 
 template <int THREADS, int E>
 __device__ bool rank_row_bins(const uint32_t* __restrict__ row, int j, int n, uint16_t* __restrict__ out,
-                              uint32_t* hist, uint32_t* curs, uint32_t* kscr, uint16_t* kidx, uint32_t* warp_buf,
-                              const TieMarks& tm) {
+                              uint32_t* hist, uint32_t* curs, uint32_t* kscr, uint2* tie_list, uint32_t* tie_count,
+                              uint32_t* warp_buf, const TieMarks& tm) {
   constexpr int NB = kRankBins, W = NB / 2, PER = W / THREADS;  // E * THREADS >= n keys
   const int tid = threadIdx.x;
   uint32_t key[E];
@@ -200,7 +205,6 @@ __device__ bool rank_row_bins(const uint32_t* __restrict__ row, int j, int n, ui
         const uint32_t old = atomicAdd(&curs[b >> 1], 1u << ((b & 1) * 16));
         const uint32_t slot = (old >> ((b & 1) * 16)) & 0xffffu;
         kscr[slot] = key[e];
-        kidx[slot] = (uint16_t)(e * THREADS + tid);
       }
     }
   }
@@ -211,20 +215,40 @@ __device__ bool rank_row_bins(const uint32_t* __restrict__ row, int j, int n, ui
     if (i < n) {
       const int b = bin_of(key[e]);
       const uint32_t base = start(b), end = next(b);
-      uint32_t cnt = 0;
+      uint32_t cnt = 0, eq = 0;
       if (end - base > 1u) {
         for (uint32_t q = base; q < end; ++q) {
           const uint32_t kq = kscr[q];
           cnt += kq < key[e];
-          if (kq == key[e] && tm.masks && kidx[q] != i) {
-            const int k = kidx[q], tj = j / kTile, ti = i / kTile;
-            atomicOr(&tm.masks[pair_index(min(tj, ti), max(tj, ti), tm.nb) * tm.nch + k / kSymBK],
-                     1u << (k % kSymBK));
-          }
+          eq += kq == key[e];
         }
       }
       out[i] = (uint16_t)(base + cnt);
+      if (eq > 1u && tm.masks) {  // a duplicated value: collect (key, index)
+        const uint32_t o = atomicAdd(tie_count, 1u);
+        if (o < (uint32_t)kTieList) tie_list[o] = make_uint2(key[e], (uint32_t)i);
+      }
     }
+  }
+  __syncthreads();
+  if (tm.masks) {
+    const uint32_t m = *tie_count;
+    const int tj = j / kTile;
+    if (m > (uint32_t)kTieList) {
+      if (tid == 0) atomicOr(&tm.tile_flags[tj], 1u);
+    } else {
+      for (uint32_t a = tid; a < m; a += THREADS) {
+        const uint2 ea = tie_list[a];
+        const int ta = (int)ea.y / kTile;
+        uint32_t* mrow = tm.masks + pair_index(min(tj, ta), max(tj, ta), tm.nb) * tm.nch;
+        for (uint32_t b = 0; b < m; ++b) {
+          const uint2 eb = tie_list[b];
+          if (b != a && eb.x == ea.x) atomicOr(&mrow[eb.y / kSymBK], 1u << (eb.y % kSymBK));
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) *tie_count = 0u;
   }
   __syncthreads();
   return true;
@@ -245,10 +269,13 @@ __global__ void __launch_bounds__(THREADS)
   __shared__ uint32_t warp_buf[THREADS / 32];
   uint32_t* hist = reinterpret_cast<uint32_t*>(rank_smem);
   uint32_t* kscr = hist + kRankBins;  // after counts and cursors
-  uint16_t* kidx = reinterpret_cast<uint16_t*>(kscr + E * THREADS);
+  __shared__ uint2 tie_list[kTieList];
+  __shared__ uint32_t tie_count;
+  if (threadIdx.x == 0) tie_count = 0u;
+  __syncthreads();
   for (int r = blockIdx.x; r < n; r += gridDim.x) {
     if (!rank_row_bins<THREADS, E>(ds + (size_t)r * ld, r, n, rk + (size_t)r * ld, hist, hist + kRankBins / 2,
-                                   kscr, kidx, warp_buf, tm)) {
+                                   kscr, tie_list, &tie_count, warp_buf, tm)) {
       if (threadIdx.x == 0) fail_rows[atomicAdd(fail_count, 1)] = r;
       __syncthreads();
     }
