@@ -64,9 +64,11 @@ struct Stats {
 };
 
 __global__ void stats_kernel(const float* __restrict__ d, uint64_t ldd, int n, int check_sym,
-                             Stats* out) {
+                             Stats* out, int r_begin, int r_end) {
   uint32_t mn = 0xffffffffu, mx = 0u, flags = 0u;
-  for (int r = blockIdx.x; r < n; r += gridDim.x) {
+  // rows [r_begin, r_end); symmetry is checked against the rows above
+  // (c < r), so a banded H2D can check each band as it arrives
+  for (int r = r_begin + blockIdx.x; r < r_end; r += gridDim.x) {
     const float* row = d + (size_t)r * ldd;
     for (int c = threadIdx.x; c < n; c += blockDim.x) {
       const float v = row[c];
@@ -83,7 +85,7 @@ __global__ void stats_kernel(const float* __restrict__ d, uint64_t ldd, int n, i
         mn = min(mn, bits);
         mx = max(mx, bits);
       }
-      if (check_sym && r < c) {
+      if (check_sym && c < r) {
         const float t = d[(size_t)c * ldd + r];
         if (__float_as_uint(t) != bits) flags |= 32u;
       }
@@ -255,6 +257,9 @@ struct pald_gpu_plan {
   uint16_t* rank_b = nullptr;
   uint32_t* rank_scratch = nullptr;      // per-CTA scratch of the rank kernels
   int* rank_fail = nullptr;              // [count, rows...] declined by the bins kernel
+  int2* band_tiles = nullptr;            // pass-1 tiles by the band of their column tile (host API)
+  std::vector<long long> band_units;     // unit offsets of the bands in band_tiles
+  size_t rank_fail_ints = 0;
   size_t rank_scratch_words = 0;
   CUtensorMap tm_ra, tm_rb;
   bool rank_ready = false;               // RA / RB built for the loaded D
@@ -318,6 +323,7 @@ struct pald_gpu_plan {
     cudaFree(rank_b);
     cudaFree(rank_scratch);
     cudaFree(rank_fail);
+    cudaFree(band_tiles);
     cudaFree(split_items);
     cudaFree(split_pairs);
     cudaFree(split_partial);
@@ -467,25 +473,53 @@ int ensure_rank_scratch(pald_gpu_plan* p, size_t words) {
   return PALD_GPU_OK;
 }
 
-// Bins path of the rank codes (fast layout): THREADS x E keys per row.
+// Source keys of the rank codes: the plan's layout of D (scaled fp32 bits
+// or exact-path keys 2*bits), or the raw fp32 D with the sign bit masked
+// (the banded host path, before the range check; positive floats order as
+// their bits, and scaling by 2^p is exact, so the ranks are the same).
+struct RankSrc {
+  const uint32_t* keys;
+  uint32_t mask;
+  int end_bit;  // CUB sort: significant key bits
+  bool bins;    // value-linear bins apply (finite fp32 keys, or raw fp32)
+};
+
+RankSrc rank_src_layout(const pald_gpu_plan* p) {
+  return {p->ds, 0xffffffffu, p->exact ? 32 : 30, !p->exact};  // fast layout: scaled values < 1.0
+}
+
+// Bins path of the rank codes: THREADS x E keys per row, rows [r0, r1);
+// declined rows appended to (fail_rows, *fail_count).
 template <int THREADS, int E>
-int launch_rank_bins(pald_gpu_plan* p, uint16_t* rk, const TieMarks& tm, cudaStream_t s) {
+int launch_rank_bins(pald_gpu_plan* p, const RankSrc& src, uint16_t* rk, const TieMarks& tm, int r0, int r1,
+                     int* fail_rows, int* fail_count, cudaStream_t s) {
   auto k = row_rank_bins_kernel<THREADS, E>;
   const int n = (int)p->n, smem = rank_bin_smem(THREADS * E);
   PALD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int per_sm = 1;
   PALD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, THREADS, smem));
-  const int grid = std::min(n, p->sms * std::max(1, per_sm));
-  k<<<grid, THREADS, smem, s>>>(p->ds, n, (int)p->ld, rk, p->rank_fail + 1, p->rank_fail, tm);
+  const int grid = std::min(r1 - r0, p->sms * std::max(1, per_sm));
+  if (grid <= 0) return PALD_GPU_OK;
+  k<<<grid, THREADS, smem, s>>>(src.keys, n, (int)p->ld, rk, fail_rows, fail_count, tm, r0, r1, src.mask);
   PALD_CUDA(cudaGetLastError());
   ++p->launches;
   return PALD_GPU_OK;
 }
 
+int launch_rank_bins_n(pald_gpu_plan* p, const RankSrc& src, uint16_t* rk, const TieMarks& tm, int r0, int r1,
+                       int* fail_rows, int* fail_count, cudaStream_t s) {
+  const int n = (int)p->n;
+  return n <= 4096    ? launch_rank_bins<256, 16>(p, src, rk, tm, r0, r1, fail_rows, fail_count, s)
+         : n <= 8192  ? launch_rank_bins<512, 16>(p, src, rk, tm, r0, r1, fail_rows, fail_count, s)
+         : n <= 16384 ? launch_rank_bins<1024, 16>(p, src, rk, tm, r0, r1, fail_rows, fail_count, s)
+                      : launch_rank_bins<1024, 32>(p, src, rk, tm, r0, r1, fail_rows, fail_count, s);
+}
+
 // Sort path of the rank codes over all rows (rows == nullptr) or over the
 // rows listed by the bins kernel (count on the device).
 template <int THREADS, int ITEMS>
-int launch_row_rank(pald_gpu_plan* p, uint16_t* rk, int end_bit, const int* rows, const int* count, cudaStream_t s) {
+int launch_row_rank(pald_gpu_plan* p, const RankSrc& src, uint16_t* rk, const int* rows, const int* count,
+                    cudaStream_t s) {
   using Cfg = RankCfg<THREADS, ITEMS>;
   auto k = row_rank_kernel<THREADS, ITEMS>;
   const int n = (int)p->n, smem = Cfg::smem_bytes(n);
@@ -495,15 +529,34 @@ int launch_row_rank(pald_gpu_plan* p, uint16_t* rk, int end_bit, const int* rows
   const int grid = std::min(n, p->sms * std::max(1, per_sm));
   int rc = ensure_rank_scratch(p, (size_t)grid * std::max(n, Cfg::kSeg));
   if (rc) return rc;
-  k<<<grid, THREADS, smem, s>>>(p->ds, n, (int)p->ld, end_bit, rows, count, rk, p->rank_scratch);
+  k<<<grid, THREADS, smem, s>>>(src.keys, n, (int)p->ld, src.end_bit, rows, count, rk, p->rank_scratch, src.mask);
   PALD_CUDA(cudaGetLastError());
   ++p->launches;
   return PALD_GPU_OK;
 }
 
-// Builds RA / RB from the plan's layout of D, using W as the Rk scratch
-// (W is zeroed afterwards by the caller).
-int build_rank_codes(pald_gpu_plan* p, cudaStream_t s, bool mark_ties) {
+int launch_row_rank_n(pald_gpu_plan* p, const RankSrc& src, uint16_t* rk, const int* rows, const int* count,
+                      cudaStream_t s) {
+  const int n = (int)p->n;
+  return n <= 2048   ? launch_row_rank<256, 8>(p, src, rk, rows, count, s)
+         : n <= 4096 ? launch_row_rank<256, 16>(p, src, rk, rows, count, s)
+         : n <= 8192 ? launch_row_rank<256, 32>(p, src, rk, rows, count, s)
+                     : launch_row_rank<512, 32>(p, src, rk, rows, count, s);
+}
+
+// RA / RB columns [r0, r1) (r1 = n: through the padding columns up to ld).
+int launch_rank_layout(pald_gpu_plan* p, const uint16_t* rk, int r0, int r1, cudaStream_t s) {
+  const int n = (int)p->n, ld = (int)p->ld;
+  const int rc1 = r1 >= n ? ld : r1;
+  if (rc1 <= r0) return PALD_GPU_OK;
+  rank_layout_kernel<<<dim3((unsigned)((rc1 - r0 + 31) / 32), (unsigned)((p->n + 31) / 32)), 256, 0, s>>>(
+      rk, n, ld, p->rank_a, p->rank_b, r0);
+  PALD_CUDA(cudaGetLastError());
+  ++p->launches;
+  return PALD_GPU_OK;
+}
+
+int ensure_rank_buffers(pald_gpu_plan* p, size_t fail_ints) {
   if (!p->rank_a) {
     PALD_CUDA(cudaMalloc(&p->rank_a, p->n * p->ld * 4));
     PALD_CUDA(cudaMalloc(&p->rank_b, p->n * p->ld * 2));
@@ -511,38 +564,58 @@ int build_rank_codes(pald_gpu_plan* p, cudaStream_t s, bool mark_ties) {
     if ((rc = make_map(&p->tm_ra, p->rank_a, p->n, p->ld, kTile, kBK, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4))) return rc;
     if ((rc = make_map(&p->tm_rb, p->rank_b, p->n, p->ld, kTile, kBK, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2))) return rc;
   }
-  const int n = (int)p->n, ld = (int)p->ld;
+  if (fail_ints > p->rank_fail_ints) {
+    cudaFree(p->rank_fail);
+    p->rank_fail = nullptr;
+    p->rank_fail_ints = 0;
+    PALD_CUDA(cudaMalloc(&p->rank_fail, fail_ints * sizeof(int)));
+    p->rank_fail_ints = fail_ints;
+  }
+  return PALD_GPU_OK;
+}
+
+// Builds RA / RB from the plan's layout of D, using W as the Rk scratch
+// (W is zeroed afterwards by the caller).
+int build_rank_codes(pald_gpu_plan* p, cudaStream_t s, bool mark_ties) {
+  int rc = ensure_rank_buffers(p, p->n + 1);
+  if (rc) return rc;
+  const int n = (int)p->n;
   uint16_t* rk = reinterpret_cast<uint16_t*>(p->w);  // W[0, n*ld*2 B)
-  const int end_bit = p->exact ? 32 : 30;            // fast path: scaled values < 1.0
+  const RankSrc src = rank_src_layout(p);
   const int* rows = nullptr;
   const int* count = nullptr;
-  int rc;
-  if (!p->exact) {  // value-linear bins (finite fp32 keys); declined rows -> sort path
-    if (!p->rank_fail) PALD_CUDA(cudaMalloc(&p->rank_fail, (p->n + 1) * sizeof(int)));
+  if (src.bins) {  // value-linear bins; declined rows -> sort path
     PALD_CUDA(cudaMemsetAsync(p->rank_fail, 0, sizeof(int), s));
     const TieMarks tm{mark_ties ? p->sym_masks : nullptr, p->sym_tile_flags, (int)p->nb, p->sym_nch};
-    rc = n <= 4096    ? launch_rank_bins<256, 16>(p, rk, tm, s)
-         : n <= 8192  ? launch_rank_bins<512, 16>(p, rk, tm, s)
-         : n <= 16384 ? launch_rank_bins<1024, 16>(p, rk, tm, s)
-                      : launch_rank_bins<1024, 32>(p, rk, tm, s);
-    if (rc) return rc;
+    if ((rc = launch_rank_bins_n(p, src, rk, tm, 0, n, p->rank_fail + 1, p->rank_fail, s))) return rc;
     rows = p->rank_fail + 1;
     count = p->rank_fail;
   }
-  rc = n <= 2048   ? launch_row_rank<256, 8>(p, rk, end_bit, rows, count, s)
-       : n <= 4096 ? launch_row_rank<256, 16>(p, rk, end_bit, rows, count, s)
-       : n <= 8192 ? launch_row_rank<256, 32>(p, rk, end_bit, rows, count, s)
-                   : launch_row_rank<512, 32>(p, rk, end_bit, rows, count, s);
-  if (rc) return rc;
-  rank_layout_kernel<<<dim3((unsigned)(p->ld / 32), (unsigned)((p->n + 31) / 32)), 256, 0, s>>>(rk, n, ld, p->rank_a,
-                                                                                             p->rank_b);
-  PALD_CUDA(cudaGetLastError());
-  ++p->launches;
+  if ((rc = launch_row_rank_n(p, src, rk, rows, count, s))) return rc;
+  if ((rc = launch_rank_layout(p, rk, 0, n, s))) return rc;
   p->rank_ready = true;
   return PALD_GPU_OK;
 }
 
 bool sym_wins(const pald_gpu_plan* p, double marked);
+
+// Duplicate scan of the columns (all, or the listed rows) of keys (n x ld).
+int launch_tie_scan(pald_gpu_plan* p, const uint32_t* keys, const int* rows, const int* count, cudaStream_t s) {
+  static bool attr_done[64] = {};
+  if (!attr_done[p->device & 63]) {
+    PALD_CUDA(cudaFuncSetAttribute(tie_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTieSmem));
+    attr_done[p->device & 63] = true;
+  }
+  const int passes = (int)((p->n + kTieCap * 3 / 4 - 1) / (kTieCap * 3 / 4));
+  tie_scan_kernel<<<(unsigned)std::min<uint64_t>(p->n, (uint64_t)p->sms), kTieThreads, kTieSmem, s>>>(
+      keys, (int)p->n, (int)p->ld, (int)p->nb, p->sym_nch, passes, p->sym_masks, p->sym_tile_flags, rows, count);
+  PALD_CUDA(cudaGetLastError());
+  ++p->launches;
+  return PALD_GPU_OK;
+}
+
+int check_stats(const pald_gpu_plan* p, const Stats& st, bool validate, bool* fast_out, int* p2_out);
+int tie_summary(pald_gpu_plan* p, cudaStream_t s);
 
 int plan_load_impl(pald_gpu_plan* p, const float* dD, uint64_t ldd, cudaStream_t s) {
   const int n = (int)p->n;
@@ -551,35 +624,15 @@ int plan_load_impl(pald_gpu_plan* p, const float* dD, uint64_t ldd, cudaStream_t
   *p->stats_host = init;
   PALD_CUDA(cudaMemcpyAsync(p->stats, p->stats_host, sizeof(Stats), cudaMemcpyHostToDevice, s));
   const bool validate = !(p->flags & PALD_GPU_FLAG_SKIP_VALIDATION);
-  stats_kernel<<<grid_rows(p->n), 256, 0, s>>>(dD, ldd, n, validate ? 1 : 0, p->stats);
+  stats_kernel<<<grid_rows(p->n), 256, 0, s>>>(dD, ldd, n, validate ? 1 : 0, p->stats, 0, n);
   PALD_CUDA(cudaGetLastError());
   ++p->launches;
   PALD_CUDA(cudaMemcpyAsync(p->stats_host, p->stats, sizeof(Stats), cudaMemcpyDeviceToHost, s));
   PALD_CUDA(cudaStreamSynchronize(s));
-  const Stats st = *p->stats_host;
-  if (validate) {
-    if (st.diag_nonzero) return set_error(PALD_GPU_ERR_VALIDATION, "distance matrix diagonal entry is nonzero");
-    if (st.offdiag_not_positive)
-      return set_error(PALD_GPU_ERR_VALIDATION,
-                       "off-diagonal distance must be positive (duplicate points are rejected)");
-    if (st.asymmetric) return set_error(PALD_GPU_ERR_VALIDATION, "distance matrix not symmetric");
-  }
-  // Range check for the FFMA.SAT compare path: scale by 2^p2 so that the
-  // largest value lies in [0.5, 1); all values must stay >= 2^-102.
-  bool fast = !(p->flags & PALD_GPU_FLAG_FORCE_EXACT) && !st.offdiag_zero && !st.has_inf &&
-              !st.has_nan && st.min_pos_bits != 0xffffffffu;
+  bool fast = false;
   int p2 = 0;
-  if (fast) {
-    float vmax, vmin;
-    uint32_t mb = st.max_bits, nbits = st.min_pos_bits;
-    std::memcpy(&vmax, &mb, 4);
-    std::memcpy(&vmin, &nbits, 4);
-    int e = 0;
-    std::frexp(vmax, &e);  // vmax = f * 2^e, f in [0.5, 1)
-    p2 = -e;
-    const double scaled_min = std::ldexp((double)vmin, p2);
-    if (!(scaled_min >= std::ldexp(1.0, -102))) fast = false;
-  }
+  int rc = check_stats(p, *p->stats_host, validate, &fast, &p2);
+  if (rc) return rc;
   p->exact = !fast;
   layout_kernel<<<grid_rows(p->n), 256, 0, s>>>(dD, ldd, n, p->ld, fast ? 1 : 0, p2, p->ds,
                                                        p->dnu);
@@ -609,22 +662,56 @@ int plan_load_impl(pald_gpu_plan* p, const float* dD, uint64_t ldd, cudaStream_t
   // skipped where the pair kernel cannot win even tie-free.
   if (fast && p->algorithm == PALD_GPU_TRIPLET && sym_enabled() && sym_wins(p, 0.0)) p->sym_ready = true;
   if (tie_scan) {
-    const size_t words = mask_words;
     // the rank-code bins kernel marked its rows: scan only the rows it declined
     const bool by_rank = p->rank_ready && !p->exact;
-    static bool attr_done[64] = {};
-    if (!attr_done[p->device & 63]) {
-      PALD_CUDA(cudaFuncSetAttribute(tie_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTieSmem));
-      attr_done[p->device & 63] = true;
-    }
-    const int passes = (int)((p->n + kTieCap * 3 / 4 - 1) / (kTieCap * 3 / 4));
-    tie_scan_kernel<<<(unsigned)std::min<uint64_t>(p->n, (uint64_t)p->sms), kTieThreads, kTieSmem, s>>>(
-        p->ds, n, (int)p->ld, (int)p->nb, p->sym_nch, passes, p->sym_masks, p->sym_tile_flags,
-        by_rank ? p->rank_fail + 1 : nullptr, by_rank ? p->rank_fail : nullptr);
-    PALD_CUDA(cudaGetLastError());
+    if ((rc = launch_tie_scan(p, p->ds, by_rank ? p->rank_fail + 1 : nullptr, by_rank ? p->rank_fail : nullptr, s)))
+      return rc;
+    if ((rc = tie_summary(p, s))) return rc;
+  }
+  p->loaded = true;
+  p->focus_dirty = false;
+  return PALD_GPU_OK;
+}
+
+// Validation errors of the reference (types.hpp:45-65) and the range check
+// of the FFMA.SAT compare path: scale by 2^p2 so that the largest value lies
+// in [0.5, 1); all values must stay >= 2^-102.
+int check_stats(const pald_gpu_plan* p, const Stats& st, bool validate, bool* fast_out, int* p2_out) {
+  if (validate) {
+    if (st.diag_nonzero) return set_error(PALD_GPU_ERR_VALIDATION, "distance matrix diagonal entry is nonzero");
+    if (st.offdiag_not_positive)
+      return set_error(PALD_GPU_ERR_VALIDATION,
+                       "off-diagonal distance must be positive (duplicate points are rejected)");
+    if (st.asymmetric) return set_error(PALD_GPU_ERR_VALIDATION, "distance matrix not symmetric");
+  }
+  bool fast = !(p->flags & PALD_GPU_FLAG_FORCE_EXACT) && !st.offdiag_zero && !st.has_inf &&
+              !st.has_nan && st.min_pos_bits != 0xffffffffu;
+  int p2 = 0;
+  if (fast) {
+    float vmax, vmin;
+    uint32_t mb = st.max_bits, nbits = st.min_pos_bits;
+    std::memcpy(&vmax, &mb, 4);
+    std::memcpy(&vmin, &nbits, 4);
+    int e = 0;
+    std::frexp(vmax, &e);  // vmax = f * 2^e, f in [0.5, 1)
+    p2 = -e;
+    const double scaled_min = std::ldexp((double)vmin, p2);
+    if (!(scaled_min >= std::ldexp(1.0, -102))) fast = false;
+  }
+  *fast_out = fast;
+  *p2_out = p2;
+  return PALD_GPU_OK;
+}
+
+// Marked-step share of the pair kernel's tie masks (cost model input);
+// the pair kernel may run afterwards. Synchronizes s.
+int tie_summary(pald_gpu_plan* p, cudaStream_t s) {
+  {
+    const size_t words = sym_mask_words(p);
+    PALD_CUDA(cudaMemsetAsync(p->sym_count, 0, sizeof(unsigned long long), s));
     tie_count_kernel<<<(unsigned)p->sms * 4, 256, 0, s>>>(p->sym_masks, words, p->sym_count);
     PALD_CUDA(cudaGetLastError());
-    p->launches += 2;
+    ++p->launches;
     unsigned long long marked = 0;
     std::vector<uint32_t> tf(p->nb);
     PALD_CUDA(cudaMemcpyAsync(&marked, p->sym_count, sizeof(marked), cudaMemcpyDeviceToHost, s));
@@ -644,14 +731,15 @@ int plan_load_impl(pald_gpu_plan* p, const float* dD, uint64_t ldd, cudaStream_t
       fprintf(stderr, "[pald_gpu] tie scan: %.4f%% of (pair, k) steps exact, %llu of %llu tiles fully\n",
               100.0 * p->sym_marked, (unsigned long long)flagged_tiles, (unsigned long long)p->nb);
   }
-  p->loaded = true;
-  p->focus_dirty = false;
   return PALD_GPU_OK;
 }
 
 uint64_t focus_units(const pald_gpu_plan* p) {
   return p->nb * (p->nb + 1) / 2 * ((p->n + kBK - 1) / kBK);
 }
+
+int launch_focus_range(pald_gpu_plan* p, long long ub, long long ue, const int2* tile_list, cudaStream_t s,
+                       bool peers);
 
 // Pass 1, share `part` of `parts` equal shares of the work units: integer
 // focus counts accumulated into the W buffer.
@@ -670,10 +758,16 @@ int plan_focus_counts_impl(pald_gpu_plan* p, uint64_t part, uint64_t parts, cuda
   p->focus_dirty = true;
   const uint64_t units = focus_units(p);
   const long long ub = (long long)(units * part / parts), ue = (long long)(units * (part + 1) / parts);
+  return launch_focus_range(p, ub, ue, p->focus_tiles, s, peers);
+}
+
+// Pass-1 work units [ub, ue) of a tile list (unit = tile * nchunks + chunk).
+int launch_focus_range(pald_gpu_plan* p, long long ub, long long ue, const int2* tile_list, cudaStream_t s,
+                       bool peers) {
   if (ue <= ub) return PALD_GPU_OK;
   const long long tiles = (long long)(p->nb * (p->nb + 1) / 2);
   KernelArgs a{p->ds, p->u, p->w, p->c, (int)p->n, (int)p->ld, (int)p->nb, 0, (int)p->nb, tiles, ub, ue,
-               p->focus_tiles, kGroupRows, p->peer_w};
+               tile_list, kGroupRows, p->peer_w};
   const int grid = (int)std::min<long long>(ue - ub, p->sms);
   int rc;
   const bool tri = p->algorithm == PALD_GPU_TRIPLET;
@@ -971,6 +1065,119 @@ int plan_cohesion_share_impl(pald_gpu_plan* p, uint64_t part, uint64_t parts, cu
   // Row bands of whole tile rows (every row costs the same).
   const uint64_t t0 = p->nb * part / parts, t1 = p->nb * (part + 1) / parts;
   return plan_cohesion_impl(p, std::min(p->n, t0 * kTile), std::min(p->n, t1 * kTile), s);
+}
+
+// Host-memory D, banded: the H2D of D runs in bands of 16 tile rows on a
+// copy stream; as each band arrives, its range check (aux stream) and its
+// rows' rank codes, tie marks, RA / RB columns and the pass-1 tiles whose
+// rows AND columns have all arrived (tiles (P, Q), P <= Q, Q in the band)
+// run on the compute stream, so pass 1 overlaps the transfer. Ranks come
+// from the raw fp32 bits (sign masked): same order as the layout keys, no
+// range check needed. The range check, layout and tie statistics finish
+// after the last band; validation errors are reported then (after pass 1).
+bool banded_wanted(const pald_gpu_plan* p) {
+  static const int m = [] {
+    const char* e = getenv("PALD_GPU_BANDED");  // 0: whole H2D, then load + pass 1
+    return e ? atoi(e) : 1;
+  }();
+  return m != 0 && rank_wanted(p) && p->nb > kGroupRows;
+}
+
+int build_band_tiles(pald_gpu_plan* p) {
+  if (p->band_tiles) return PALD_GPU_OK;
+  const int nb = (int)p->nb, nch = (int)((p->n + kBK - 1) / kBK);
+  std::vector<int2> list;
+  p->band_units.assign(1, 0);
+  for (int q0 = 0; q0 < nb; q0 += kGroupRows) {
+    const int q1 = std::min(nb, q0 + kGroupRows);
+    for (int P = 0; P < q1; ++P)
+      for (int Q = std::max(P, q0); Q < q1; ++Q) list.push_back(make_int2(P, Q));
+    p->band_units.push_back((long long)list.size() * nch);
+  }
+  PALD_CUDA(cudaMalloc(&p->band_tiles, list.size() * sizeof(int2)));
+  PALD_CUDA(cudaMemcpy(p->band_tiles, list.data(), list.size() * sizeof(int2), cudaMemcpyHostToDevice));
+  return PALD_GPU_OK;
+}
+
+int load_focus_banded(pald_gpu_plan* p, const float* D, cudaStream_t s, cudaStream_t sc, cudaStream_t sa) {
+  const int n = (int)p->n, ld = (int)p->ld;
+  const int band_rows = kGroupRows * kTile;
+  const int nbands = (n + band_rows - 1) / band_rows;
+  int rc;
+  if ((rc = ensure_rank_buffers(p, (size_t)nbands + p->n))) return rc;
+  if ((rc = build_band_tiles(p))) return rc;
+  const bool validate = !(p->flags & PALD_GPU_FLAG_SKIP_VALIDATION);
+  Stats init{};
+  init.min_pos_bits = 0xffffffffu;
+  *p->stats_host = init;
+  PALD_CUDA(cudaMemcpyAsync(p->stats, p->stats_host, sizeof(Stats), cudaMemcpyHostToDevice, sa));
+  PALD_CUDA(cudaMemsetAsync(p->w, 0, p->n * p->ld * 4, s));  // pass-1 counts
+  PALD_CUDA(cudaMemsetAsync(p->rank_fail, 0, nbands * sizeof(int), s));
+  const bool mark = p->sym_masks && p->algorithm == PALD_GPU_PAIRWISE && p->policy == PALD_GPU_STRICT &&
+                    sym_enabled();
+  if (mark) {
+    PALD_CUDA(cudaMemsetAsync(p->sym_masks, 0, sym_mask_words(p) * sizeof(uint32_t), s));
+    PALD_CUDA(cudaMemsetAsync(p->sym_tile_flags, 0, p->nb * sizeof(uint32_t), s));
+  }
+  p->loaded = false;
+  p->rank_ready = true;  // the pass-1 launches below run on RA / RB
+  p->sym_ready = false;
+  p->sym_marked = 0;
+  p->focus_dirty = true;
+  const uint32_t* raw = reinterpret_cast<const uint32_t*>(p->c);  // D staged in C (free until pass 2)
+  const RankSrc src{raw, 0x7fffffffu, 31, true};
+  uint16_t* rk = reinterpret_cast<uint16_t*>(p->u);  // U is free until the focus finish
+  const TieMarks tm{mark ? p->sym_masks : nullptr, p->sym_tile_flags, (int)p->nb, p->sym_nch};
+  std::vector<cudaEvent_t> ev(nbands);
+  for (auto& e : ev) PALD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  struct EvG {
+    std::vector<cudaEvent_t>& e;
+    ~EvG() {
+      for (auto x : e) cudaEventDestroy(x);
+    }
+  } evg{ev};
+  for (int b = 0; b < nbands; ++b) {
+    const int r0 = b * band_rows, r1 = std::min(n, r0 + band_rows);
+    PALD_CUDA(cudaMemcpy2DAsync(p->c + (size_t)r0 * ld, (size_t)ld * 4, D + (size_t)r0 * n, (size_t)n * 4,
+                                (size_t)n * 4, r1 - r0, cudaMemcpyHostToDevice, sc));
+    PALD_CUDA(cudaEventRecord(ev[b], sc));
+    PALD_CUDA(cudaStreamWaitEvent(sa, ev[b], 0));
+    stats_kernel<<<std::min(r1 - r0, 148 * 16), 256, 0, sa>>>(p->c, (uint64_t)ld, n, validate ? 1 : 0, p->stats, r0,
+                                                               r1);
+    PALD_CUDA(cudaGetLastError());
+    PALD_CUDA(cudaStreamWaitEvent(s, ev[b], 0));
+    int* fail_rows = p->rank_fail + nbands + r0;
+    int* fail_count = p->rank_fail + b;
+    if ((rc = launch_rank_bins_n(p, src, rk, tm, r0, r1, fail_rows, fail_count, s))) return rc;
+    if ((rc = launch_row_rank_n(p, src, rk, fail_rows, fail_count, s))) return rc;
+    if (mark && (rc = launch_tie_scan(p, raw, fail_rows, fail_count, s))) return rc;
+    if ((rc = launch_rank_layout(p, rk, r0, r1, s))) return rc;
+    if ((rc = launch_focus_range(p, p->band_units[b], p->band_units[b + 1], p->band_tiles, s, false))) return rc;
+    p->launches += 1;
+  }
+  PALD_CUDA(cudaMemcpyAsync(p->stats_host, p->stats, sizeof(Stats), cudaMemcpyDeviceToHost, sa));
+  PALD_CUDA(cudaStreamSynchronize(sa));
+  bool fast = false;
+  int p2 = 0;
+  if ((rc = check_stats(p, *p->stats_host, validate, &fast, &p2))) {
+    cudaStreamSynchronize(s);  // no work left behind on the plan
+    p->rank_ready = false;
+    return rc;
+  }
+  p->exact = !fast;
+  // layout for pass 2 on the aux stream, concurrent with the pass-1 tail
+  layout_kernel<<<grid_rows(p->n), 256, 0, sa>>>(p->c, (uint64_t)ld, n, p->ld, fast ? 1 : 0, p2, p->ds, p->dnu);
+  PALD_CUDA(cudaGetLastError());
+  p->launches += 2;  // + the stats bands
+  cudaEvent_t ev_layout;
+  PALD_CUDA(cudaEventCreateWithFlags(&ev_layout, cudaEventDisableTiming));
+  PALD_CUDA(cudaEventRecord(ev_layout, sa));
+  PALD_CUDA(cudaStreamWaitEvent(s, ev_layout, 0));
+  cudaEventDestroy(ev_layout);
+  if (fast && p->algorithm == PALD_GPU_TRIPLET && sym_enabled() && sym_wins(p, 0.0)) p->sym_ready = true;
+  if (mark && fast && sym_wins(p, 0.0) && (rc = tie_summary(p, s))) return rc;
+  p->loaded = true;
+  return PALD_GPU_OK;
 }
 
 // One cached plan per device for the one-shot APIs.
@@ -1278,9 +1485,15 @@ int pald_gpu_cohesion_f32(const float* D, uint64_t n, const pald_gpu_opts* o, in
     }
   } eg{ev, s2};
   PALD_CUDA(cudaEventRecord(ev[0], s));
-  if ((rc = pald_gpu_plan_load_host(p, D, s))) return rc;
-  PALD_CUDA(cudaEventRecord(ev[1], s));
-  if ((rc = plan_focus_impl(p, s))) return rc;
+  if (banded_wanted(p)) {  // H2D in bands overlapped with the rank codes and pass 1
+    PALD_CUDA(cudaEventRecord(ev[1], s));
+    if ((rc = load_focus_banded(p, D, s, sc, s2))) return rc;
+    if ((rc = plan_focus_finish_impl(p, s))) return rc;
+  } else {
+    if ((rc = pald_gpu_plan_load_host(p, D, s))) return rc;
+    PALD_CUDA(cudaEventRecord(ev[1], s));
+    if ((rc = plan_focus_impl(p, s))) return rc;
+  }
   PALD_CUDA(cudaEventRecord(ev[2], s));
   if (U_out) {
     PALD_CUDA(cudaStreamWaitEvent(sc, ev[2], 0));

@@ -147,7 +147,7 @@ struct TieMarks {
 constexpr int kTieList = 1024;
 
 template <int THREADS, int E>
-__device__ bool rank_row_bins(const uint32_t* __restrict__ row, int j, int n, uint16_t* __restrict__ out,
+__device__ bool rank_row_bins(const uint32_t* __restrict__ row, int j, int n, uint32_t key_mask, uint16_t* __restrict__ out,
                               uint32_t* hist, uint32_t* curs, uint32_t* kscr, uint2* tie_list, uint32_t* tie_count,
                               uint32_t* warp_buf, const TieMarks& tm) {
   constexpr int NB = kRankBins, W = NB / 2, PER = W / THREADS;  // E * THREADS >= n keys
@@ -157,7 +157,7 @@ __device__ bool rank_row_bins(const uint32_t* __restrict__ row, int j, int n, ui
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int i = e * THREADS + tid;
-    key[e] = i < n ? __ldg(row + i) : 0u;
+    key[e] = i < n ? (__ldg(row + i) & key_mask) : 0u;
     mx = max(mx, key[e]);
   }
 #pragma unroll
@@ -264,7 +264,8 @@ __device__ bool rank_row_bins(const uint32_t* __restrict__ row, int j, int n, ui
 template <int THREADS, int E>
 __global__ void __launch_bounds__(THREADS)
     row_rank_bins_kernel(const uint32_t* __restrict__ ds, int n, int ld, uint16_t* __restrict__ rk,
-                         int* __restrict__ fail_rows, int* __restrict__ fail_count, TieMarks tm) {
+                         int* __restrict__ fail_rows, int* __restrict__ fail_count, TieMarks tm, int r_begin,
+                         int r_end, uint32_t key_mask) {
   extern __shared__ __align__(128) uint8_t rank_smem[];
   __shared__ uint32_t warp_buf[THREADS / 32];
   uint32_t* hist = reinterpret_cast<uint32_t*>(rank_smem);
@@ -273,8 +274,8 @@ __global__ void __launch_bounds__(THREADS)
   __shared__ uint32_t tie_count;
   if (threadIdx.x == 0) tie_count = 0u;
   __syncthreads();
-  for (int r = blockIdx.x; r < n; r += gridDim.x) {
-    if (!rank_row_bins<THREADS, E>(ds + (size_t)r * ld, r, n, rk + (size_t)r * ld, hist, hist + kRankBins / 2,
+  for (int r = r_begin + blockIdx.x; r < r_end; r += gridDim.x) {
+    if (!rank_row_bins<THREADS, E>(ds + (size_t)r * ld, r, n, key_mask, rk + (size_t)r * ld, hist, hist + kRankBins / 2,
                                    kscr, tie_list, &tie_count, warp_buf, tm)) {
       if (threadIdx.x == 0) fail_rows[atomicAdd(fail_count, 1)] = r;
       __syncthreads();
@@ -286,7 +287,8 @@ __global__ void __launch_bounds__(THREADS)
 template <int THREADS, int ITEMS>
 __global__ void __launch_bounds__(THREADS)
     row_rank_kernel(const uint32_t* __restrict__ ds, int n, int ld, int end_bit, const int* __restrict__ rows,
-                    const int* __restrict__ row_count, uint16_t* __restrict__ rk, uint32_t* __restrict__ scratch) {
+                    const int* __restrict__ row_count, uint16_t* __restrict__ rk, uint32_t* __restrict__ scratch,
+                    uint32_t key_mask) {
   using Cfg = RankCfg<THREADS, ITEMS>;
   constexpr int S = Cfg::kSeg;
   extern __shared__ __align__(128) uint8_t rank_smem[];
@@ -311,7 +313,7 @@ __global__ void __launch_bounds__(THREADS)
 #pragma unroll
       for (int e = 0; e < ITEMS; ++e) {  // striped (coalesced) load; order is irrelevant
         const int i = h * S + e * THREADS + tid;
-        keys[e] = i < n ? __ldg(row + i) : 0xffffffffu;  // never a layout key: sorts last
+        keys[e] = i < n ? (__ldg(row + i) & key_mask) : 0xffffffffu;  // never a key: sorts last
         vals[e] = (uint16_t)i;
       }
       Cfg::Sort(temp).Sort(keys, vals, 0, end_bit);  // blocked: positions tid*ITEMS + e
@@ -390,13 +392,14 @@ __global__ void __launch_bounds__(THREADS)
 }
 
 // RA[k][r] = (0x8000 | Rk[r][k]) * 0x10001, RB[k][r] = 0x8000 | Rk[r][k] for
-// k < n, r < ld; padding rows/columns (r >= n) get code 0.
+// k < n, r in [r_begin, ld) covered by the grid; padding rows/columns
+// (r >= n) get code 0.
 __global__ void __launch_bounds__(256)
     rank_layout_kernel(const uint16_t* __restrict__ rk, int n, int ld, uint32_t* __restrict__ ra,
-                       uint16_t* __restrict__ rb) {
+                       uint16_t* __restrict__ rb, int r_begin) {
   __shared__ uint16_t t[32][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-  const int r0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+  const int r0 = r_begin + blockIdx.x * 32, k0 = blockIdx.y * 32;
   for (int yy = ty; yy < 32; yy += 8) {
     const int r = r0 + yy, k = k0 + tx;
     t[yy][tx] = (r < n && k < n) ? rk[(size_t)r * ld + k] : (uint16_t)0;

@@ -295,3 +295,43 @@ def test_triplet_split_last_round(oracle, n, kind):
     ur, cr = oracle.triplet_rows_f64(d, rows)
     assert np.array_equal(eng.U.cpu().numpy()[rows], ur)
     assert max_rel_diff(c1[rows], cr) <= TOL
+
+
+@pytest.mark.parametrize("mutate", ["asym_low", "asym_high", "neg", "diag", "nan", "zero"])
+def test_host_api_banded_validation(mutate):
+    """The one-shot host API streams D in bands of 2048 rows and checks each
+    band as it arrives (symmetry against the rows above): every invalid
+    input is still rejected, wherever the defect sits, and the next call on
+    the same cached plan is correct."""
+    from paper_2307_16652_b200 import _lib
+    from paper_2307_16652_b200.api import ValidationError, _raise_for
+
+    lib = _lib.load()
+    n = 4200
+    d = random_upper(n, 3)
+    i, j = (4100, 7) if mutate != "asym_high" else (7, 4100)
+    if mutate.startswith("asym"):
+        d[i, j] += 1.0
+    elif mutate == "neg":
+        d[i, j] = d[j, i] = -1.0
+    elif mutate == "diag":
+        d[i, i] = 1.0
+    elif mutate == "nan":
+        d[i, j] = d[j, i] = np.nan
+    else:
+        d[i, j] = d[j, i] = 0.0
+    opts = _lib.make_opts(algorithm=_lib.PAIRWISE)
+    u = np.empty((n, n), np.int32)
+    c = np.empty((n, n), np.float32)
+    with pytest.raises(ValidationError):
+        _raise_for(lib.pald_gpu_cohesion_f32(d.ctypes.data, n, C.byref(opts), u.ctypes.data, c.ctypes.data, None))
+    good = random_upper(n, 4)
+    u2, c2 = run_gpu(good, "pairwise")
+    from paper_2307_16652_b200.engine import Engine
+    import torch
+
+    e = Engine(n, "pairwise")
+    e.run(torch.from_numpy(good).cuda())
+    torch.cuda.synchronize()
+    assert np.array_equal(u2, e.U.cpu().numpy())
+    assert np.array_equal(c2.view(np.uint32), e.C.cpu().numpy().view(np.uint32))
