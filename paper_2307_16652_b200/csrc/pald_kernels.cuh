@@ -53,6 +53,10 @@ constexpr int kTile = 128;      // pair-tile edge (rows and columns)
 #define PALD_KUNROLL 2
 #endif
 constexpr int kKUnroll = PALD_KUNROLL;
+#ifndef PALD_RANK_UNROLL  // unroll of the rank-coded k loop: the bare loop prefers 8
+#define PALD_RANK_UNROLL 2  // (tools/microbench4.cu), the 255-register kernel 2-4 (8: -1.2 %)
+#endif
+constexpr int kRankUnroll = PALD_RANK_UNROLL;
 #ifndef PALD_K_ORDER  // k-step instruction order: 0 rows outer, 1 column pairs outer
 #define PALD_K_ORDER 0
 #endif
@@ -704,7 +708,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE))
         if (a_in || b_in) {
           for (int kk = 0; kk < kmax; ++kk) k_step_rank_sel(ra, rb, kk, k0 + kk, ty, tx, r0, c0, a_in, b_in, thr, acc);
         } else if (kmax == kBK) {
-#pragma unroll kKUnroll
+#pragma unroll kRankUnroll
           for (int kk = 0; kk < kBK; ++kk) k_step_rank(ra, rb, kk, ty, tx, thr, acc);
         } else {
           for (int kk = 0; kk < kmax; ++kk) k_step_rank(ra, rb, kk, ty, tx, thr, acc);

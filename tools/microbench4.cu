@@ -24,7 +24,7 @@ __device__ __forceinline__ uint32_t vmin2(uint32_t a, uint32_t b) {
 // MODE 0: fp32 baseline. 1: rank, acc += F>>15 (compiler). 2: rank, mad.hi.
 // 3: rank with min.u16x2 + mask. 4: rank, add via IMAD forced (mad.lo with
 // register one) for X1.
-template <int MODE, int ORD>
+template <int MODE, int ORD, int UNR = 2>
 __global__ void __launch_bounds__(256, 1) kern(uint32_t* out, int reps, const uint32_t* cin) {
   constexpr int BK = 16;
   __shared__ __align__(16) uint32_t sA[BK][128];
@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(256, 1) kern(uint32_t* out, int reps, const ui
   const uint32_t one = cin[64 * 512];
   unsigned long long t0 = clock64();
   for (int r = 0; r < reps; ++r) {
-#pragma unroll 2
+#pragma unroll UNR
     for (int k = 0; k < BK; ++k) {
       uint32_t a[8], b[8];
       const uint4 a0 = *reinterpret_cast<const uint4*>(&sA[k][ty * 4]);
@@ -121,14 +121,14 @@ __global__ void __launch_bounds__(256, 1) kern(uint32_t* out, int reps, const ui
   if (threadIdx.x == 0) g_cyc[blockIdx.x] = t1 - t0;
 }
 
-template <int MODE, int ORD>
+template <int MODE, int ORD, int UNR = 2>
 void run(const char* name, uint32_t* out, const uint32_t* cin, int nsm) {
   const int reps = 1024;
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   float ms = 0;
   for (int rep = 0; rep < 3; ++rep) {
     cudaEventRecord(e0);
-    kern<MODE, ORD><<<nsm, 256>>>(out, reps, cin);
+    kern<MODE, ORD, UNR><<<nsm, 256>>>(out, reps, cin);
     cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
     CK(cudaGetLastError());
     cudaEventElapsedTime(&ms, e0, e1);
@@ -154,5 +154,9 @@ int main() {
   run<4, 0>("focus_rank_madhi_imadx1", out, cin, nsm);
   run<1, 1>("focus_rank_shift_colouter", out, cin, nsm);
   run<2, 1>("focus_rank_madhi_colouter", out, cin, nsm);
+  run<2, 0, 1>("focus_rank_madhi_unroll1", out, cin, nsm);
+  run<2, 0, 4>("focus_rank_madhi_unroll4", out, cin, nsm);
+  run<2, 0, 8>("focus_rank_madhi_unroll8", out, cin, nsm);
+  run<4, 0, 4>("focus_rank_madhi_imadx1_unroll4", out, cin, nsm);
   return 0;
 }
