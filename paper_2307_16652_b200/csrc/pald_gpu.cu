@@ -768,7 +768,7 @@ int launch_focus_range(pald_gpu_plan* p, long long ub, long long ue, const int2*
   const long long tiles = (long long)(p->nb * (p->nb + 1) / 2);
   KernelArgs a{p->ds, p->u, p->w, p->c, (int)p->n, (int)p->ld, (int)p->nb, 0, (int)p->nb, tiles, ub, ue,
                tile_list, kGroupRows, p->peer_w};
-  const int grid = (int)std::min<long long>(ue - ub, p->sms);
+  const int grid = (int)std::min<long long>(ue - ub, (long long)p->sms * (p->rank_ready ? ctas_per_sm(kTile, true) : 1));
   int rc;
   const bool tri = p->algorithm == PALD_GPU_TRIPLET;
   const bool split = p->policy == PALD_GPU_INCLUSIVE_SPLIT;

@@ -73,15 +73,20 @@ __host__ __device__ constexpr int stage_bytes(int pass, int tile, bool rank = fa
 }
 // CTAs per SM: 1 for 128-wide tiles (8 x 8 outputs per thread, ~230
 // registers), 2 for the 64-wide small-n tiles (4 x 4 per thread).
-__host__ __device__ constexpr int ctas_per_sm(int tile) { return tile == 128 ? 1 : 2; }
+#ifndef PALD_RANK_CTAS  // CTAs per SM of the rank-coded pass 1 (A/B knob; 2 CTAs at 128
+#define PALD_RANK_CTAS 1   // registers with 2 stages: 44.1 vs 48.5 combos/SM-cycle)
+#endif
+__host__ __device__ constexpr int ctas_per_sm(int tile, bool rank = false) {
+  return rank ? PALD_RANK_CTAS : tile == 128 ? 1 : 2;
+}
 // Pipeline depth so that stages x stage_bytes fits the shared memory of
 // ctas_per_sm CTAs (227 KB per SM).
 #ifndef PALD_SMEM_BUDGET_KB
 #define PALD_SMEM_BUDGET_KB 200
 #endif
 __host__ __device__ constexpr int stages_for(int pass, int tile, bool rank = false) {
-  return stage_bytes(pass, tile, rank) * 4 <= PALD_SMEM_BUDGET_KB * 1024 / ctas_per_sm(tile) ? 4
-         : stage_bytes(pass, tile, rank) * 3 <= PALD_SMEM_BUDGET_KB * 1024 / ctas_per_sm(tile) ? 3 : 2;
+  return stage_bytes(pass, tile, rank) * 4 <= PALD_SMEM_BUDGET_KB * 1024 / ctas_per_sm(tile, rank) ? 4
+         : stage_bytes(pass, tile, rank) * 3 <= PALD_SMEM_BUDGET_KB * 1024 / ctas_per_sm(tile, rank) ? 3 : 2;
 }
 constexpr int kBoxBytes = kBK * kTile * 4;  // one TMA box of a 128-wide panel (32 KB)
 constexpr float kCmpScale = 0x1p125f;       // S of the FFMA.SAT compare
@@ -533,7 +538,7 @@ __device__ __forceinline__ WorkSplit make_split(const KernelArgs& a, int C, int 
 // block-wide barrier sits in the main loop.
 template <int PASS, bool A_NU, bool B_NU, bool T_NU, bool ZERO_DIAG, bool FAST, bool SPLIT = false,
           int TILE = kTile, bool LIST = false, bool PEERS = false, bool RANK = false>
-__global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE))
+__global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE, RANK))
     pald_tile_kernel(const __grid_constant__ CUtensorMap tm_d,
                      const __grid_constant__ CUtensorMap tm_dnu,
                      const __grid_constant__ CUtensorMap tm_w, const KernelArgs args) {
