@@ -335,3 +335,42 @@ def test_host_api_banded_validation(mutate):
     torch.cuda.synchronize()
     assert np.array_equal(u2, e.U.cpu().numpy())
     assert np.array_equal(c2.view(np.uint32), e.C.cpu().numpy().view(np.uint32))
+
+
+@pytest.mark.parametrize("case", ["force_exact", "degenerate"])
+def test_host_api_banded_matches_engine_special_layouts(case):
+    """The banded host path ranks the raw fp32 bits (sign masked) before the
+    range check; with the exact (integer-key) layout for pass 2 (forced, or
+    chosen because the fp32 conversion of a valid double input holds 0 and
+    inf off the diagonal, validation done in double) it must still equal the
+    engine's path (layout keys) bit for bit, NaN rows included."""
+    import torch
+
+    from paper_2307_16652_b200 import _lib
+    from paper_2307_16652_b200.api import _raise_for
+    from paper_2307_16652_b200.engine import Engine
+
+    n = 2300
+    rng = np.random.default_rng(9)
+    d = random_upper(n, 9)
+    flags = _lib.FLAG_FORCE_EXACT
+    if case == "degenerate":
+        iu = np.triu_indices(n, 1)
+        pick = rng.random(iu[0].size)
+        v = d[iu].copy()
+        v[pick < 0.01] = 0.0
+        v[pick > 0.99] = np.inf
+        d[iu] = v
+        d[(iu[1], iu[0])] = v
+        flags = _lib.FLAG_SKIP_VALIDATION
+    lib = _lib.load()
+    opts = _lib.make_opts(algorithm=_lib.PAIRWISE, flags=flags)
+    u = np.empty((n, n), np.int32)
+    c = np.empty((n, n), np.float32)
+    _raise_for(lib.pald_gpu_cohesion_f32(d.ctypes.data, n, C.byref(opts), u.ctypes.data, c.ctypes.data, None))
+    e = Engine(n, "pairwise", force_exact=(case == "force_exact"), skip_validation=(case == "degenerate"))
+    e.run(torch.from_numpy(d).cuda())
+    torch.cuda.synchronize()
+    assert e.exact_path
+    assert np.array_equal(u, e.U.cpu().numpy())
+    assert np.array_equal(c, e.C.cpu().numpy(), equal_nan=True)
