@@ -260,6 +260,8 @@ struct pald_gpu_plan {
   int2* band_tiles = nullptr;            // pass-1 tiles by the band of their column tile (host API)
   std::vector<long long> band_units;     // unit offsets of the bands in band_tiles
   size_t rank_fail_ints = 0;
+  cudaStream_t aux = nullptr;            // load: rank codes beside the range check / layout
+  cudaEvent_t ev_in = nullptr, ev_ranks = nullptr;
   size_t rank_scratch_words = 0;
   CUtensorMap tm_ra, tm_rb;
   bool rank_ready = false;               // RA / RB built for the loaded D
@@ -324,6 +326,9 @@ struct pald_gpu_plan {
     cudaFree(rank_scratch);
     cudaFree(rank_fail);
     cudaFree(band_tiles);
+    if (aux) cudaStreamDestroy(aux);
+    if (ev_in) cudaEventDestroy(ev_in);
+    if (ev_ranks) cudaEventDestroy(ev_ranks);
     cudaFree(split_items);
     cudaFree(split_pairs);
     cudaFree(split_partial);
@@ -480,12 +485,16 @@ int ensure_rank_scratch(pald_gpu_plan* p, size_t words) {
 struct RankSrc {
   const uint32_t* keys;
   uint32_t mask;
-  int end_bit;  // CUB sort: significant key bits
-  bool bins;    // value-linear bins apply (finite fp32 keys, or raw fp32)
+  int end_bit;    // CUB sort: significant key bits
+  bool bins;      // value-linear bins apply (finite fp32 keys, or raw fp32)
+  size_t key_ld;  // row stride of keys
 };
 
 RankSrc rank_src_layout(const pald_gpu_plan* p) {
-  return {p->ds, 0xffffffffu, p->exact ? 32 : 30, !p->exact};  // fast layout: scaled values < 1.0
+  return {p->ds, 0xffffffffu, p->exact ? 32 : 30, !p->exact, p->ld};  // fast layout: scaled values < 1.0
+}
+RankSrc rank_src_raw(const float* d, uint64_t ldd) {
+  return {reinterpret_cast<const uint32_t*>(d), 0x7fffffffu, 31, true, ldd};
 }
 
 // Bins path of the rank codes: THREADS x E keys per row, rows [r0, r1);
@@ -500,7 +509,8 @@ int launch_rank_bins(pald_gpu_plan* p, const RankSrc& src, uint16_t* rk, const T
   PALD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, THREADS, smem));
   const int grid = std::min(r1 - r0, p->sms * std::max(1, per_sm));
   if (grid <= 0) return PALD_GPU_OK;
-  k<<<grid, THREADS, smem, s>>>(src.keys, n, (int)p->ld, rk, fail_rows, fail_count, tm, r0, r1, src.mask);
+  k<<<grid, THREADS, smem, s>>>(src.keys, n, (int)p->ld, rk, fail_rows, fail_count, tm, r0, r1, src.mask,
+                                src.key_ld);
   PALD_CUDA(cudaGetLastError());
   ++p->launches;
   return PALD_GPU_OK;
@@ -529,7 +539,8 @@ int launch_row_rank(pald_gpu_plan* p, const RankSrc& src, uint16_t* rk, const in
   const int grid = std::min(n, p->sms * std::max(1, per_sm));
   int rc = ensure_rank_scratch(p, (size_t)grid * std::max(n, Cfg::kSeg));
   if (rc) return rc;
-  k<<<grid, THREADS, smem, s>>>(src.keys, n, (int)p->ld, src.end_bit, rows, count, rk, p->rank_scratch, src.mask);
+  k<<<grid, THREADS, smem, s>>>(src.keys, n, (int)p->ld, src.end_bit, rows, count, rk, p->rank_scratch, src.mask,
+                                src.key_ld);
   PALD_CUDA(cudaGetLastError());
   ++p->launches;
   return PALD_GPU_OK;
@@ -574,14 +585,18 @@ int ensure_rank_buffers(pald_gpu_plan* p, size_t fail_ints) {
   return PALD_GPU_OK;
 }
 
-// Builds RA / RB from the plan's layout of D, using W as the Rk scratch
-// (W is zeroed afterwards by the caller).
-int build_rank_codes(pald_gpu_plan* p, cudaStream_t s, bool mark_ties) {
+// Builds RA / RB from src (n rows), using W as the Rk scratch (W is zeroed
+// afterwards by the caller). With mark_ties, the bins kernel marks the pair
+// kernel's ties of its rows and tie_scan_kernel those of the rows it
+// declined (the masks must be zeroed before).
+int launch_tie_scan(pald_gpu_plan* p, const uint32_t* keys, const int* rows, const int* count, cudaStream_t s,
+                    uint64_t key_ld);
+
+int build_rank_codes(pald_gpu_plan* p, const RankSrc& src, bool mark_ties, cudaStream_t s) {
   int rc = ensure_rank_buffers(p, p->n + 1);
   if (rc) return rc;
   const int n = (int)p->n;
   uint16_t* rk = reinterpret_cast<uint16_t*>(p->w);  // W[0, n*ld*2 B)
-  const RankSrc src = rank_src_layout(p);
   const int* rows = nullptr;
   const int* count = nullptr;
   if (src.bins) {  // value-linear bins; declined rows -> sort path
@@ -592,6 +607,7 @@ int build_rank_codes(pald_gpu_plan* p, cudaStream_t s, bool mark_ties) {
     count = p->rank_fail;
   }
   if ((rc = launch_row_rank_n(p, src, rk, rows, count, s))) return rc;
+  if (mark_ties && (rc = launch_tie_scan(p, src.keys, rows, count, s, src.key_ld))) return rc;
   if ((rc = launch_rank_layout(p, rk, 0, n, s))) return rc;
   p->rank_ready = true;
   return PALD_GPU_OK;
@@ -600,7 +616,8 @@ int build_rank_codes(pald_gpu_plan* p, cudaStream_t s, bool mark_ties) {
 bool sym_wins(const pald_gpu_plan* p, double marked);
 
 // Duplicate scan of the columns (all, or the listed rows) of keys (n x ld).
-int launch_tie_scan(pald_gpu_plan* p, const uint32_t* keys, const int* rows, const int* count, cudaStream_t s) {
+int launch_tie_scan(pald_gpu_plan* p, const uint32_t* keys, const int* rows, const int* count, cudaStream_t s,
+                    uint64_t key_ld) {
   static bool attr_done[64] = {};
   if (!attr_done[p->device & 63]) {
     PALD_CUDA(cudaFuncSetAttribute(tie_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTieSmem));
@@ -608,7 +625,8 @@ int launch_tie_scan(pald_gpu_plan* p, const uint32_t* keys, const int* rows, con
   }
   const int passes = (int)((p->n + kTieCap * 3 / 4 - 1) / (kTieCap * 3 / 4));
   tie_scan_kernel<<<(unsigned)std::min<uint64_t>(p->n, (uint64_t)p->sms), kTieThreads, kTieSmem, s>>>(
-      keys, (int)p->n, (int)p->ld, (int)p->nb, p->sym_nch, passes, p->sym_masks, p->sym_tile_flags, rows, count);
+      keys, (int)p->n, (int)(key_ld ? key_ld : p->ld), (int)p->nb, p->sym_nch, passes, p->sym_masks,
+      p->sym_tile_flags, rows, count);
   PALD_CUDA(cudaGetLastError());
   ++p->launches;
   return PALD_GPU_OK;
@@ -622,6 +640,32 @@ int plan_load_impl(pald_gpu_plan* p, const float* dD, uint64_t ldd, cudaStream_t
   Stats init{};
   init.min_pos_bits = 0xffffffffu;
   *p->stats_host = init;
+  int rc;
+  p->rank_ready = false;
+  p->sym_ready = false;
+  p->sym_marked = 0;
+  // Rank codes (pald_rank.cuh) from the raw fp32 bits of D on the aux
+  // stream, concurrent with the range check and the layout (ranks need no
+  // range check: positive floats order as their bits, and the scaling of the
+  // fast layout is exact). The bins kernel also marks the pair kernel's ties.
+  const bool ranks = rank_wanted(p);
+  const bool mark = ranks && p->sym_masks && p->algorithm == PALD_GPU_PAIRWISE && p->policy == PALD_GPU_STRICT &&
+                    sym_enabled();
+  if (ranks) {
+    if (!p->aux) {
+      PALD_CUDA(cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking));
+      PALD_CUDA(cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming));
+      PALD_CUDA(cudaEventCreateWithFlags(&p->ev_ranks, cudaEventDisableTiming));
+    }
+    PALD_CUDA(cudaEventRecord(p->ev_in, s));  // D is ready in stream order of s
+    PALD_CUDA(cudaStreamWaitEvent(p->aux, p->ev_in, 0));
+    if (mark) {
+      PALD_CUDA(cudaMemsetAsync(p->sym_masks, 0, sym_mask_words(p) * sizeof(uint32_t), p->aux));
+      PALD_CUDA(cudaMemsetAsync(p->sym_tile_flags, 0, p->nb * sizeof(uint32_t), p->aux));
+    }
+    if ((rc = build_rank_codes(p, rank_src_raw(dD, ldd), mark, p->aux))) return rc;
+    PALD_CUDA(cudaEventRecord(p->ev_ranks, p->aux));
+  }
   PALD_CUDA(cudaMemcpyAsync(p->stats, p->stats_host, sizeof(Stats), cudaMemcpyHostToDevice, s));
   const bool validate = !(p->flags & PALD_GPU_FLAG_SKIP_VALIDATION);
   stats_kernel<<<grid_rows(p->n), 256, 0, s>>>(dD, ldd, n, validate ? 1 : 0, p->stats, 0, n);
@@ -631,41 +675,32 @@ int plan_load_impl(pald_gpu_plan* p, const float* dD, uint64_t ldd, cudaStream_t
   PALD_CUDA(cudaStreamSynchronize(s));
   bool fast = false;
   int p2 = 0;
-  int rc = check_stats(p, *p->stats_host, validate, &fast, &p2);
-  if (rc) return rc;
+  if ((rc = check_stats(p, *p->stats_host, validate, &fast, &p2))) {
+    if (ranks) cudaStreamSynchronize(p->aux);  // leave no work behind on the plan
+    p->rank_ready = false;
+    return rc;
+  }
   p->exact = !fast;
   layout_kernel<<<grid_rows(p->n), 256, 0, s>>>(dD, ldd, n, p->ld, fast ? 1 : 0, p2, p->ds,
                                                        p->dnu);
   PALD_CUDA(cudaGetLastError());
   ++p->launches;
-  p->rank_ready = false;
-  p->sym_ready = false;
-  p->sym_marked = 0;
-  // Duplicate scan of the columns of D for the tile-pair cohesion kernel
-  // (pairwise; skipped where the pair kernel cannot win even tie-free).
-  const bool tie_scan = fast && p->sym_masks && sym_enabled() && sym_wins(p, 0.0);
-  const size_t mask_words = tie_scan ? sym_mask_words(p) : 0;
-  if (tie_scan) {
-    PALD_CUDA(cudaMemsetAsync(p->sym_masks, 0, mask_words * sizeof(uint32_t), s));
-    PALD_CUDA(cudaMemsetAsync(p->sym_tile_flags, 0, p->nb * sizeof(uint32_t), s));
-    PALD_CUDA(cudaMemsetAsync(p->sym_count, 0, sizeof(unsigned long long), s));
-  }
-  if (rank_wanted(p)) {  // on the fast layout this also marks the ties (bins kernel)
-    const int rc = build_rank_codes(p, s, tie_scan);
-    if (rc) return rc;
-  }
+  if (ranks) PALD_CUDA(cudaStreamWaitEvent(s, p->ev_ranks, 0));  // W held the rank scratch
   PALD_CUDA(cudaMemsetAsync(p->u, 0, p->n * p->ld * 4, s));
   PALD_CUDA(cudaMemsetAsync(p->w, 0, p->n * p->ld * 4, s));
   // Triplet: the pair kernel's shared indicator is exact without a scan
   // (its per-element chunks, those inside the row or column tile, cost too
-  // little to enter the cost model: tools/time_n.py). Pairwise: the scan is
+  // little to enter the cost model: tools/time_n.py). Pairwise: the
+  // duplicate scan of the columns of D (marks of the tile-pair kernel) is
   // skipped where the pair kernel cannot win even tie-free.
   if (fast && p->algorithm == PALD_GPU_TRIPLET && sym_enabled() && sym_wins(p, 0.0)) p->sym_ready = true;
+  const bool tie_scan = fast && p->sym_masks && sym_enabled() && sym_wins(p, 0.0);
   if (tie_scan) {
-    // the rank-code bins kernel marked its rows: scan only the rows it declined
-    const bool by_rank = p->rank_ready && !p->exact;
-    if ((rc = launch_tie_scan(p, p->ds, by_rank ? p->rank_fail + 1 : nullptr, by_rank ? p->rank_fail : nullptr, s)))
-      return rc;
+    if (!mark) {  // no rank codes: scan every column of the layout
+      PALD_CUDA(cudaMemsetAsync(p->sym_masks, 0, sym_mask_words(p) * sizeof(uint32_t), s));
+      PALD_CUDA(cudaMemsetAsync(p->sym_tile_flags, 0, p->nb * sizeof(uint32_t), s));
+      if ((rc = launch_tie_scan(p, p->ds, nullptr, nullptr, s, 0))) return rc;
+    }
     if ((rc = tie_summary(p, s))) return rc;
   }
   p->loaded = true;
@@ -1125,7 +1160,7 @@ int load_focus_banded(pald_gpu_plan* p, const float* D, cudaStream_t s, cudaStre
   p->sym_marked = 0;
   p->focus_dirty = true;
   const uint32_t* raw = reinterpret_cast<const uint32_t*>(p->c);  // D staged in C (free until pass 2)
-  const RankSrc src{raw, 0x7fffffffu, 31, true};
+  const RankSrc src = rank_src_raw(p->c, p->ld);
   uint16_t* rk = reinterpret_cast<uint16_t*>(p->u);  // U is free until the focus finish
   const TieMarks tm{mark ? p->sym_masks : nullptr, p->sym_tile_flags, (int)p->nb, p->sym_nch};
   std::vector<cudaEvent_t> ev(nbands);
@@ -1150,7 +1185,7 @@ int load_focus_banded(pald_gpu_plan* p, const float* D, cudaStream_t s, cudaStre
     int* fail_count = p->rank_fail + b;
     if ((rc = launch_rank_bins_n(p, src, rk, tm, r0, r1, fail_rows, fail_count, s))) return rc;
     if ((rc = launch_row_rank_n(p, src, rk, fail_rows, fail_count, s))) return rc;
-    if (mark && (rc = launch_tie_scan(p, raw, fail_rows, fail_count, s))) return rc;
+    if (mark && (rc = launch_tie_scan(p, raw, fail_rows, fail_count, s, 0))) return rc;
     if ((rc = launch_rank_layout(p, rk, r0, r1, s))) return rc;
     if ((rc = launch_focus_range(p, p->band_units[b], p->band_units[b + 1], p->band_tiles, s, false))) return rc;
     p->launches += 1;

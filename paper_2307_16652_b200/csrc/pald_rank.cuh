@@ -265,7 +265,7 @@ template <int THREADS, int E>
 __global__ void __launch_bounds__(THREADS)
     row_rank_bins_kernel(const uint32_t* __restrict__ ds, int n, int ld, uint16_t* __restrict__ rk,
                          int* __restrict__ fail_rows, int* __restrict__ fail_count, TieMarks tm, int r_begin,
-                         int r_end, uint32_t key_mask) {
+                         int r_end, uint32_t key_mask, size_t key_ld) {
   extern __shared__ __align__(128) uint8_t rank_smem[];
   __shared__ uint32_t warp_buf[THREADS / 32];
   uint32_t* hist = reinterpret_cast<uint32_t*>(rank_smem);
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(THREADS)
   if (threadIdx.x == 0) tie_count = 0u;
   __syncthreads();
   for (int r = r_begin + blockIdx.x; r < r_end; r += gridDim.x) {
-    if (!rank_row_bins<THREADS, E>(ds + (size_t)r * ld, r, n, key_mask, rk + (size_t)r * ld, hist, hist + kRankBins / 2,
+    if (!rank_row_bins<THREADS, E>(ds + (size_t)r * key_ld, r, n, key_mask, rk + (size_t)r * ld, hist, hist + kRankBins / 2,
                                    kscr, tie_list, &tie_count, warp_buf, tm)) {
       if (threadIdx.x == 0) fail_rows[atomicAdd(fail_count, 1)] = r;
       __syncthreads();
@@ -288,7 +288,7 @@ template <int THREADS, int ITEMS>
 __global__ void __launch_bounds__(THREADS)
     row_rank_kernel(const uint32_t* __restrict__ ds, int n, int ld, int end_bit, const int* __restrict__ rows,
                     const int* __restrict__ row_count, uint16_t* __restrict__ rk, uint32_t* __restrict__ scratch,
-                    uint32_t key_mask) {
+                    uint32_t key_mask, size_t key_ld) {
   using Cfg = RankCfg<THREADS, ITEMS>;
   constexpr int S = Cfg::kSeg;
   extern __shared__ __align__(128) uint8_t rank_smem[];
@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(THREADS)
   const int nrows = rows ? *row_count : n;
   for (int ri = blockIdx.x; ri < nrows; ri += gridDim.x) {
     const int r = rows ? rows[ri] : ri;
-    const uint32_t* row = ds + (size_t)r * ld;
+    const uint32_t* row = ds + (size_t)r * key_ld;
     uint16_t* out = rk + (size_t)r * ld;
     for (int h = 0; h < nseg; ++h) {
       uint32_t keys[ITEMS];
