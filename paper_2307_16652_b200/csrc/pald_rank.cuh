@@ -24,8 +24,9 @@
 //                       (the 16-bit code with its flag bit, broadcast to both
 //                       halves) and RB[k][c] = 0x8000 | Rk[c][k] (uint16).
 //
-// Keys are the plan's layout of D (scaled fp32 bits or the exact path's
-// integer keys 2*bits(d)): both are monotone in d as unsigned integers.
+// Keys are the raw fp32 bits of D with the sign bit masked (the diagonal may
+// be -0.0), or the plan's layout of D (scaled fp32 bits or the exact path's
+// integer keys 2*bits(d)): all are monotone in d as unsigned integers.
 #pragma once
 
 #include <cuda_runtime.h>
