@@ -56,6 +56,7 @@ class Oracle:
             "pald_oracle_triplet_f32in_f64": (None, [_vp, _u64, _vp, _vp]),
             "pald_oracle_row_sums_f32": (None, [_vp, _u64, _vp]),
             "pald_oracle_triplet_rows_f64": (None, [_vp, _u64, _vp, _u64, _vp, _vp]),
+            "pald_oracle_pairwise_rows_f64": (None, [_vp, _u64, _vp, _u64, _vp, _vp]),
         }
         for k, (r, a) in sigs.items():
             f = getattr(lib, k)
@@ -113,6 +114,16 @@ class Oracle:
         u = np.empty((rows.size, n), np.int32)
         c = np.empty((rows.size, n), np.float32)
         self.lib.pald_oracle_pairwise_rows_f32(_ptr(d), n, _ptr(rows), rows.size, _ptr(u), _ptr(c))
+        return u, c
+
+    def pairwise_rows_f64(self, d: np.ndarray, rows) -> tuple[np.ndarray, np.ndarray]:
+        """Rows of the fp64-accumulated pairwise (Strict) result (tolerance oracle)."""
+        d = np.ascontiguousarray(d, np.float32)
+        n = d.shape[0]
+        rows = np.ascontiguousarray(rows, np.int64)
+        u = np.empty((rows.size, n), np.int32)
+        c = np.empty((rows.size, n), np.float64)
+        self.lib.pald_oracle_pairwise_rows_f64(_ptr(d), n, _ptr(rows), rows.size, _ptr(u), _ptr(c))
         return u, c
 
     def triplet_rows_f64(self, d: np.ndarray, rows) -> tuple[np.ndarray, np.ndarray]:

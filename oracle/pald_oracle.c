@@ -241,6 +241,43 @@ void pald_oracle_pairwise_rows_f32(const float* d, uint64_t n, const int64_t* ro
   free(w);
 }
 
+/* Sampled rows of the fp64 pairwise (Strict) oracle below: row x of C
+ * (pairwise_entrywise, reference.hpp:108-145) accumulated in double, O(n^2)
+ * per row; U as in the fp32 rows. For the fp32-vs-fp64 tolerance at sizes
+ * where the O(n^3) oracle is out of reach. */
+void pald_oracle_pairwise_rows_f64(const float* d, uint64_t n, const int64_t* rows, uint64_t nrows,
+                                   int32_t* u_rows, double* c_rows) {
+  double* w = (double*)malloc(sizeof(double) * n);
+  for (uint64_t i = 0; i < nrows; ++i) {
+    const uint64_t x = (uint64_t)rows[i];
+    const float* rx = d + x * n;
+    int32_t* urow = u_rows + i * n;
+    double* crow = c_rows + i * n;
+    for (uint64_t y = 0; y < n; ++y) {
+      if (y == x) { urow[y] = 0; w[y] = 0.0; continue; }
+      const float* ry = d + y * n;
+      const float dxy = rx[y];
+      int32_t cnt = 0;
+      for (uint64_t z = 0; z < n; ++z) cnt += (rx[z] < dxy) | (ry[z] < dxy);
+      urow[y] = cnt;
+      w[y] = 1.0 / (double)cnt;
+    }
+    for (uint64_t z = 0; z < n; ++z) crow[z] = 0.0;
+    for (uint64_t y = 0; y < n; ++y) {
+      if (y == x) continue;
+      const float* ry = d + y * n;
+      const float dxy = rx[y];
+      for (uint64_t z = 0; z < n; ++z) {
+        const float dxz = rx[z], dyz = ry[z];
+        if (!((dxz < dyz ? dxz : dyz) < dxy)) continue;
+        /* support: x for the pair (x, y) iff dxz < dyz; for (y, x) iff !(dyz < dxz) */
+        if (y > x ? (dxz < dyz) : !(dyz < dxz)) crow[z] += w[y];
+      }
+    }
+  }
+  free(w);
+}
+
 /* fp64 pairwise (Strict) on fp32 inputs: the fp64 oracle for tolerances.
  * Comparisons of the same fp32 values are exact in either precision, so U
  * equals the fp32 U; C is accumulated in double. O(n^3). */

@@ -140,6 +140,14 @@ def test_cfg3_pairwise_rows_and_exact_path(oracle):
     U, Cm = e.U.cpu().numpy(), e.C.cpu().numpy()
     check_pairwise_rows(oracle, d, U, Cm, sample_rows(cfg.n, 4))
     check_u_props(U)
+    # the BASELINE tolerance against fp64 accumulation (n = 8192)
+    from helpers import max_rel_diff
+
+    rows = np.array([0, cfg.n // 2, cfg.n - 1])
+    _, c64 = oracle.pairwise_rows_f64(d, rows)
+    assert max_rel_diff(Cm[rows], c64) <= 1e-5
+    rs = np.abs(Cm[rows].astype(np.float64).sum(1) - c64.sum(1)) / c64.sum(1)
+    assert float(rs.max()) <= 1e-5
     del e
     ex = run(D, "pairwise", force_exact=True)
     assert ex.exact_path
@@ -159,6 +167,14 @@ def test_cfg5_pairwise_sampled(oracle):
     ur, cr = oracle.pairwise_rows_f32(d, rows)
     assert np.array_equal(Ur, ur)
     assert np.array_equal(Cr.view(np.uint32), cr.view(np.uint32))
+    # against fp64 accumulation: the reference's (and our identical) fp32 C
+    # drifts by the rounding of 32768-term sums (see the triplet test below)
+    from helpers import max_rel_diff
+
+    _, c64 = oracle.pairwise_rows_f64(d, rows[:2])
+    assert max_rel_diff(Cr[:2], c64) <= 3e-5
+    rs = np.abs(Cr[:2].astype(np.float64).sum(1) - c64.sum(1)) / c64.sum(1)
+    assert float(rs.max()) <= 1e-5
     total = float(e.C.double().sum())
     assert abs(total - n * (n - 1) / 2) / (n * (n - 1) / 2) < 1e-5
     Ut = e.U

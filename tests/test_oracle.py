@@ -149,6 +149,15 @@ def test_rows_oracle_matches_full(oracle):
     assert np.array_equal(cr.view(np.uint32), c[rows].view(np.uint32))
 
 
+def test_pairwise_rows_f64_oracle_matches_full(oracle):
+    for d in (int_upper(70, 6), random_upper(61, 7)):
+        u, c = oracle.pairwise_f64(d)
+        rows = [0, 17, d.shape[0] - 1]
+        ur, cr = oracle.pairwise_rows_f64(d, rows)
+        assert np.array_equal(ur, u[rows])
+        assert np.max(np.abs(cr - c[rows])) < 1e-12
+
+
 def test_triplet_rows_oracle_matches_full(oracle):
     for d in (int_upper(41, 3), random_upper(37, 4)):
         u, c = oracle.triplet_f64(d)
