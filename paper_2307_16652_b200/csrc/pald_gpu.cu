@@ -248,6 +248,7 @@ struct pald_gpu_plan {
   CUtensorMap tm_d, tm_dnu, tm_w;        // 128-wide boxes
   CUtensorMap tm_d64, tm_dnu64, tm_w64;  // 64-wide boxes (small-n cohesion tiles)
   CUtensorMap tm_d32, tm_dnu32, tm_w32;  // 128 x 32 boxes (tile-pair cohesion)
+  CUtensorMap tm_dt32, tm_dnut32, tm_wt32;  // 32-wide boxes (tail tiles)
   uint32_t* sym_masks = nullptr;         // tie k-masks per (tile pair, 32-wide k chunk)
   uint32_t* sym_tile_flags = nullptr;
   unsigned long long* sym_count = nullptr;
@@ -279,8 +280,9 @@ struct pald_gpu_plan {
   int sms = 148;
   int2* focus_tiles = nullptr;  // grouped upper-triangular tile order
   std::vector<int2> pair_order;  // host copy of it (tile pairs of pass 2)
-  int2* tail64 = nullptr;        // 64-wide one-sided tiles of the last partial pair round
+  int2* tail64 = nullptr;        // 64- (or 32-) wide one-sided tiles of the last partial pair round
   int tail64_count = 0;
+  int tail_tile = 64;            // width of the tail tiles
   int sym_main_pairs = 0;        // pairs of the full-range pair launch (rest: tail64)
   // Triplet pass 2 with the last partial round of pairs split along k
   // (pald_sym.cuh SPLIT items + sym_combine_kernel); built on first use.
@@ -371,6 +373,43 @@ bool split_enabled() {
 
 size_t sym_mask_words(const pald_gpu_plan* p) { return p->nb * (p->nb + 1) / 2 * p->sym_nch; }
 
+// Width of the tail tiles of the pair launch (PALD_GPU_TAIL: 0 none, 32, 64;
+// default -1: the cheaper of 32 and 64 by tail_rounds).
+int tail_width() {
+  static const int w = [] {
+    const char* e = getenv("PALD_GPU_TAIL");
+    const int v = e ? atoi(e) : -1;
+    return (v == 0 || v == 32 || v == 64) ? v : -1;
+  }();
+  return w;
+}
+// Time of `count` W-wide tail tiles in pair-round units (64: 0.52 / 1.44 per
+// round of 2 CTAs/SM; 32: 0.29 per round of 4 CTAs/SM, measured on config 3:
+// pass 2 39.87 ms with 64-wide, 39.66 ms with 32-wide tail tiles).
+double tail_rounds_w(const pald_gpu_plan* p, int width, int count) {
+  if (count <= 0) return 0.0;
+  const double sms = p->sms;
+  return width == 32 ? std::ceil(count / (4.0 * sms)) * 0.29 : std::ceil(count / (2.0 * sms)) * 0.52 / 1.44;
+}
+double tail_rounds(const pald_gpu_plan* p, int count) { return tail_rounds_w(p, p->tail_tile, count); }
+
+// The W-wide one-sided tiles covering pairs [first, end) of the pair order:
+// direct tiles (P, Q), then (Q, P).
+std::vector<int2> tail_tiles(const pald_gpu_plan* p, int first, int end, int W) {
+  std::vector<int2> t;
+  const int f = kTile / W, nbw = (int)((p->n + W - 1) / W);
+  for (int i = first; i < end; ++i) {
+    const int P = p->pair_order[i].x, Q = p->pair_order[i].y;
+    for (int h = 0; h < (P == Q ? 1 : 2); ++h) {
+      const int R = h ? Q : P, Cc = h ? P : Q;
+      for (int a = 0; a < f; ++a)
+        for (int b = 0; b < f; ++b)
+          if (f * R + a < nbw && f * Cc + b < nbw) t.push_back(make_int2(f * R + a, f * Cc + b));
+    }
+  }
+  return t;
+}
+
 int plan_alloc(pald_gpu_plan* p) {
   const size_t bytes = p->n * p->ld * 4;
   PALD_CUDA(cudaMalloc(&p->ds, bytes));
@@ -399,25 +438,21 @@ int plan_alloc(pald_gpu_plan* p) {
   {
     // Tail of the full-range pair launch: the last partial round of L < 148
     // pairs keeps L SMs busy for a whole pair time. When it is cheaper, those
-    // pairs run instead as 64-wide one-sided tiles (2 CTAs/SM, ~0.36 of a
-    // pair time per round; identical in-order sums).
+    // pairs run instead as W-wide one-sided tiles (W = 64: 2 CTAs/SM, ~0.36
+    // of a pair time per round; W = 32: 4 CTAs/SM; identical in-order sums).
     const std::vector<int2>& order = p->pair_order;
     const int G = p->sms, pairs = (int)order.size(), L = pairs > G ? pairs % G : 0;
     p->sym_main_pairs = pairs;
-    if (L > 0) {
-      std::vector<int2> t64;
-      const int nb64 = (int)((p->n + 63) / 64);
-      for (int i = pairs - L; i < pairs; ++i) {
-        const int P = order[i].x, Q = order[i].y;
-        for (int h = 0; h < (P == Q ? 1 : 2); ++h) {
-          const int R = h ? Q : P, Cc = h ? P : Q;  // direct tile (P, Q), then (Q, P)
-          for (int a = 0; a < 2; ++a)
-            for (int b = 0; b < 2; ++b)
-              if (2 * R + a < nb64 && 2 * Cc + b < nb64) t64.push_back(make_int2(2 * R + a, 2 * Cc + b));
-        }
-      }
-      const double rounds64 = std::ceil((double)t64.size() / (2.0 * G));
-      if (rounds64 * 0.52 / 1.44 < 1.0) {
+    int W = tail_width();
+    if (W < 0)
+      W = tail_rounds_w(p, 32, (int)tail_tiles(p, pairs - L, pairs, 32).size()) <
+                  tail_rounds_w(p, 64, (int)tail_tiles(p, pairs - L, pairs, 64).size())
+              ? 32
+              : 64;
+    p->tail_tile = W;
+    if (L > 0 && W > 0) {
+      const std::vector<int2> t64 = tail_tiles(p, pairs - L, pairs, W);
+      if (tail_rounds(p, (int)t64.size()) < 1.0) {
         PALD_CUDA(cudaMalloc(&p->tail64, t64.size() * sizeof(int2)));
         PALD_CUDA(cudaMemcpy(p->tail64, t64.data(), t64.size() * sizeof(int2), cudaMemcpyHostToDevice));
         p->tail64_count = (int)t64.size();
@@ -433,6 +468,9 @@ int plan_alloc(pald_gpu_plan* p) {
   if ((rc = make_map(&p->tm_d64, p->ds, p->n, p->ld, 64))) return rc;
   if ((rc = make_map(&p->tm_dnu64, p->dnu, p->n, p->ld, 64))) return rc;
   if ((rc = make_map(&p->tm_w64, p->w, p->n, p->ld, 64))) return rc;
+  if ((rc = make_map(&p->tm_dt32, p->ds, p->n, p->ld, 32))) return rc;
+  if ((rc = make_map(&p->tm_dnut32, p->dnu, p->n, p->ld, 32))) return rc;
+  if ((rc = make_map(&p->tm_wt32, p->w, p->n, p->ld, 32))) return rc;
   if (p->policy == PALD_GPU_STRICT) {
     if ((rc = make_map(&p->tm_d32, p->ds, p->n, p->ld, kTile, kSymBK))) return rc;
     if ((rc = make_map(&p->tm_dnu32, p->dnu, p->n, p->ld, kTile, kSymBK))) return rc;
@@ -452,6 +490,7 @@ int plan_alloc(pald_gpu_plan* p) {
 }
 
 int grid_rows(uint64_t n) { return (int)std::min<uint64_t>(n, 148ull * 16); }
+
 
 // Rank-coded pass 1 (pald_rank.cuh): pairwise and triplet focus with
 // 2048 < n <= 32768 (below that the code build costs more than the faster
@@ -891,15 +930,22 @@ int launch_cohesion(pald_gpu_plan* p, uint64_t row0, uint64_t row1, cudaStream_t
 // Tile-pair cohesion over pairs [t0, t1) of the grouped upper-triangular
 // order; writes both C[P][Q] and C[Q][P] of each pair.
 // One-sided pass 2 over an explicit list of 64-wide tiles.
-int launch_cohesion_list64(pald_gpu_plan* p, const int2* list, int count, cudaStream_t s) {
-  const uint64_t nb64 = (p->n + 63) / 64;
+template <int TILE>
+int launch_cohesion_list(pald_gpu_plan* p, const int2* list, int count, cudaStream_t s) {
+  const uint64_t nbt = (p->n + TILE - 1) / TILE;
   const long long nch = (long long)((p->n + kBK - 1) / kBK);
-  KernelArgs a{p->ds, p->u, p->w, p->c, (int)p->n, (int)p->ld, (int)nb64, 0, (int)nb64, count, 0,
+  KernelArgs a{p->ds, p->u, p->w, p->c, (int)p->n, (int)p->ld, (int)nbt, 0, (int)nbt, count, 0,
                (long long)count * nch, list, kGroupRows};
-  const int grid = std::min(count, p->sms * ctas_per_sm(64));
+  const int grid = std::min(count, p->sms * ctas_per_sm(TILE));
   const bool tri = p->algorithm == PALD_GPU_TRIPLET;
-  if (tri) return launch_tile<1, true, true, false, true, true, false, 64, true>(p->tm_d64, p->tm_dnu64, p->tm_w64, a, grid, s);
-  return launch_tile<1, false, true, false, false, true, false, 64, true>(p->tm_d64, p->tm_dnu64, p->tm_w64, a, grid, s);
+  const CUtensorMap& md = TILE == 64 ? p->tm_d64 : p->tm_dt32;
+  const CUtensorMap& mn = TILE == 64 ? p->tm_dnu64 : p->tm_dnut32;
+  const CUtensorMap& mw = TILE == 64 ? p->tm_w64 : p->tm_wt32;
+  if (tri) return launch_tile<1, true, true, false, true, true, false, TILE, true>(md, mn, mw, a, grid, s);
+  return launch_tile<1, false, true, false, false, true, false, TILE, true>(md, mn, mw, a, grid, s);
+}
+int launch_cohesion_list64(pald_gpu_plan* p, const int2* list, int count, cudaStream_t s) {
+  return p->tail_tile == 32 ? launch_cohesion_list<32>(p, list, count, s) : launch_cohesion_list<64>(p, list, count, s);
 }
 
 int launch_sym(pald_gpu_plan* p, int t0, int t1, cudaStream_t s, bool peers = false,
@@ -1030,7 +1076,7 @@ bool sym_wins(const pald_gpu_plan* p, double marked) {
   const double sms = p->sms, nb = (double)p->nb, nb64 = (double)((p->n + 63) / 64);
   // full-range launch: main pair rounds + the 64-wide tail tiles (if any)
   const double t_sym = std::ceil(p->sym_main_pairs / sms) * 1.44 * (1.0 + 1.45 * marked) +
-                       (p->tail64_count ? std::ceil(p->tail64_count / (2 * sms)) * 0.52 : 0.0);
+                       tail_rounds(p, p->tail64_count) * 1.44;
   const double t_128 = std::ceil(nb * nb / sms);
   const double t_64 = std::ceil(nb64 * nb64 / (2 * sms)) * 0.52;
   return t_sym < std::min(t_128, t_64);

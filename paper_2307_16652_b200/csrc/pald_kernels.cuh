@@ -77,7 +77,7 @@ __host__ __device__ constexpr int stage_bytes(int pass, int tile, bool rank = fa
 #define PALD_RANK_CTAS 1   // registers with 2 stages: 44.1 vs 48.5 combos/SM-cycle)
 #endif
 __host__ __device__ constexpr int ctas_per_sm(int tile, bool rank = false) {
-  return rank ? PALD_RANK_CTAS : tile == 128 ? 1 : 2;
+  return rank ? PALD_RANK_CTAS : tile == 128 ? 1 : tile == 64 ? 2 : 4;
 }
 // Pipeline depth so that stages x stage_bytes fits the shared memory of
 // ctas_per_sm CTAs (227 KB per SM).
@@ -171,11 +171,18 @@ __device__ __forceinline__ float nu_f(float v) { return __uint_as_float(__float_
 template <int TILE>
 __device__ __forceinline__ int row_off(int ty, int i) {
   if constexpr (TILE == 128) return i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4);
+  if constexpr (TILE == 32) return ty * 2 + i;  // 2 x 2 outputs per thread (tail tiles)
   return (i >> 2) * (TILE / 2) + ty * 4 + (i & 3);
 }
 
 template <int TILE, int N>
 __device__ __forceinline__ void lds_vec(const float* __restrict__ row, int t, float (&v)[N]) {
+  if constexpr (N == 2) {
+    const float2 q = reinterpret_cast<const float2*>(row)[t];
+    v[0] = q.x;
+    v[1] = q.y;
+    return;
+  }
 #pragma unroll
   for (int h = 0; h < N / 4; ++h) {
     const float4 q = reinterpret_cast<const float4*>(row)[h * (TILE / 8) + t];
@@ -689,8 +696,11 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE, RANK))
       const float* sb = reinterpret_cast<const float*>(st + BOX);
       const float* sw = reinterpret_cast<const float*>(st + 2 * BOX);
       const int k0 = ch * kBK;
-      const bool a_in = A_NU && (k0 >= c0) && (k0 < c0 + TILE);
-      const bool b_in = B_NU && (k0 >= r0) && (k0 < r0 + TILE);
+      // the chunk overlaps the column (row) tile: per-element transforms
+      // (TILE >= kBK: the chunk lies inside the tile; 32-wide tail tiles sit
+      // inside a 64-point chunk)
+      const bool a_in = A_NU && (k0 < c0 + TILE) && (k0 + kBK > c0);
+      const bool b_in = B_NU && (k0 < r0 + TILE) && (k0 + kBK > r0);
       const int kmax = min(kBK, n - k0);
       if constexpr (RANK) {
         const uint32_t* ra = reinterpret_cast<const uint32_t*>(st);
@@ -784,6 +794,9 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE, RANK))
           const int ca = c0 + tx * 4, cb = c0 + 64 + tx * 4;
           if (ca < n) *reinterpret_cast<float4*>(crow + ca) = make_float4(v[0], v[1], v[2], v[3]);
           if (cb < n) *reinterpret_cast<float4*>(crow + cb) = make_float4(v[4], v[5], v[6], v[7]);
+        } else if constexpr (TILE == 32) {
+          const int cc = c0 + tx * 2;
+          if (cc < n) *reinterpret_cast<float2*>(crow + cc) = make_float2(v[0], v[1]);
         } else {
 #pragma unroll
           for (int h = 0; h < TT / 4; ++h) {
