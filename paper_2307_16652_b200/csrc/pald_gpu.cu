@@ -725,7 +725,8 @@ int plan_load_impl(pald_gpu_plan* p, const float* dD, uint64_t ldd, cudaStream_t
   PALD_CUDA(cudaGetLastError());
   ++p->launches;
   if (ranks) PALD_CUDA(cudaStreamWaitEvent(s, p->ev_ranks, 0));  // W held the rank scratch
-  PALD_CUDA(cudaMemsetAsync(p->u, 0, p->n * p->ld * 4, s));
+  // W accumulates the pass-1 counts; U needs no clearing (focus_finish
+  // writes every entry r, c < n; the row padding is never read)
   PALD_CUDA(cudaMemsetAsync(p->w, 0, p->n * p->ld * 4, s));
   // Triplet: the pair kernel's shared indicator is exact without a scan
   // (its per-element chunks, those inside the row or column tile, cost too
