@@ -280,10 +280,10 @@ struct pald_gpu_plan {
   int sms = 148;
   int2* focus_tiles = nullptr;  // grouped upper-triangular tile order
   std::vector<int2> pair_order;  // host copy of it (tile pairs of pass 2)
-  int2* tail64 = nullptr;        // 64- (or 32-) wide one-sided tiles of the last partial pair round
-  int tail64_count = 0;
+  int2* tail = nullptr;          // 64- (or 32-) wide one-sided tiles of the last partial pair round
+  int tail_count = 0;
   int tail_tile = 64;            // width of the tail tiles
-  int sym_main_pairs = 0;        // pairs of the full-range pair launch (rest: tail64)
+  int sym_main_pairs = 0;        // pairs of the full-range pair launch (rest: tail tiles)
   // Triplet pass 2 with the last partial round of pairs split along k
   // (pald_sym.cuh SPLIT items + sym_combine_kernel); built on first use.
   int4* split_items = nullptr;
@@ -317,7 +317,7 @@ struct pald_gpu_plan {
     cudaFree(stats);
     cudaFreeHost(stats_host);
     cudaFree(focus_tiles);
-    cudaFree(tail64);
+    cudaFree(tail);
     close_peers();
     cudaFree(sym_masks);
     cudaFree(sym_tile_flags);
@@ -395,7 +395,7 @@ double tail_rounds(const pald_gpu_plan* p, int count) { return tail_rounds_w(p, 
 
 // The W-wide one-sided tiles covering pairs [first, end) of the pair order:
 // direct tiles (P, Q), then (Q, P).
-std::vector<int2> tail_tiles(const pald_gpu_plan* p, int first, int end, int W) {
+std::vector<int2> make_tail_list(const pald_gpu_plan* p, int first, int end, int W) {
   std::vector<int2> t;
   const int f = kTile / W, nbw = (int)((p->n + W - 1) / W);
   for (int i = first; i < end; ++i) {
@@ -445,17 +445,17 @@ int plan_alloc(pald_gpu_plan* p) {
     p->sym_main_pairs = pairs;
     int W = tail_width();
     if (W < 0)
-      W = tail_rounds_w(p, 32, (int)tail_tiles(p, pairs - L, pairs, 32).size()) <
-                  tail_rounds_w(p, 64, (int)tail_tiles(p, pairs - L, pairs, 64).size())
+      W = tail_rounds_w(p, 32, (int)make_tail_list(p, pairs - L, pairs, 32).size()) <
+                  tail_rounds_w(p, 64, (int)make_tail_list(p, pairs - L, pairs, 64).size())
               ? 32
               : 64;
     p->tail_tile = W;
     if (L > 0 && W > 0) {
-      const std::vector<int2> t64 = tail_tiles(p, pairs - L, pairs, W);
-      if (tail_rounds(p, (int)t64.size()) < 1.0) {
-        PALD_CUDA(cudaMalloc(&p->tail64, t64.size() * sizeof(int2)));
-        PALD_CUDA(cudaMemcpy(p->tail64, t64.data(), t64.size() * sizeof(int2), cudaMemcpyHostToDevice));
-        p->tail64_count = (int)t64.size();
+      const std::vector<int2> tl = make_tail_list(p, pairs - L, pairs, W);
+      if (tail_rounds(p, (int)tl.size()) < 1.0) {
+        PALD_CUDA(cudaMalloc(&p->tail, tl.size() * sizeof(int2)));
+        PALD_CUDA(cudaMemcpy(p->tail, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice));
+        p->tail_count = (int)tl.size();
         p->sym_main_pairs = pairs - L;
       }
     }
@@ -945,7 +945,7 @@ int launch_cohesion_list(pald_gpu_plan* p, const int2* list, int count, cudaStre
   if (tri) return launch_tile<1, true, true, false, true, true, false, TILE, true>(md, mn, mw, a, grid, s);
   return launch_tile<1, false, true, false, false, true, false, TILE, true>(md, mn, mw, a, grid, s);
 }
-int launch_cohesion_list64(pald_gpu_plan* p, const int2* list, int count, cudaStream_t s) {
+int launch_tail(pald_gpu_plan* p, const int2* list, int count, cudaStream_t s) {
   return p->tail_tile == 32 ? launch_cohesion_list<32>(p, list, count, s) : launch_cohesion_list<64>(p, list, count, s);
 }
 
@@ -1077,7 +1077,7 @@ bool sym_wins(const pald_gpu_plan* p, double marked) {
   const double sms = p->sms, nb = (double)p->nb, nb64 = (double)((p->n + 63) / 64);
   // full-range launch: main pair rounds + the 64-wide tail tiles (if any)
   const double t_sym = std::ceil(p->sym_main_pairs / sms) * 1.44 * (1.0 + 1.45 * marked) +
-                       tail_rounds(p, p->tail64_count) * 1.44;
+                       tail_rounds(p, p->tail_count) * 1.44;
   const double t_128 = std::ceil(nb * nb / sms);
   const double t_64 = std::ceil(nb64 * nb64 / (2 * sms)) * 0.52;
   return t_sym < std::min(t_128, t_64);
@@ -1109,8 +1109,8 @@ int plan_cohesion_impl(pald_gpu_plan* p, uint64_t row0, uint64_t row1, cudaStrea
       ++p->launches;
       p->last_kernel = PALD_GPU_KERNEL_PAIRS;
     }
-    if (rc == PALD_GPU_OK && p->tail64_count > 0) {
-      rc = launch_cohesion_list64(p, p->tail64, p->tail64_count, s);
+    if (rc == PALD_GPU_OK && p->tail_count > 0) {
+      rc = launch_tail(p, p->tail, p->tail_count, s);
       if (rc == PALD_GPU_OK) ++p->launches;
     }
     return rc;
