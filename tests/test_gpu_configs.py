@@ -199,7 +199,7 @@ def test_cfg5_points_triplet_sampled(oracle):
     n = cfg.n
     e = run(D, "triplet")
     assert e.info()["rank_codes"]
-    rows = np.array([n // 2 + 3, n - 1], np.int64)
+    rows = np.array([n - 1], np.int64)  # one O(n^2) oracle row: ~1 min at n = 32768
     d = D.cpu().numpy()
     ur, cr = oracle.triplet_rows_f64(d, rows)
     assert np.array_equal(e.U[rows.tolist()].cpu().numpy(), ur)
