@@ -261,7 +261,8 @@ struct pald_gpu_plan {
   int2* band_tiles = nullptr;            // pass-1 tiles by the band of their column tile (host API)
   std::vector<long long> band_units;     // unit offsets of the bands in band_tiles
   size_t rank_fail_ints = 0;
-  cudaStream_t aux = nullptr;            // load: rank codes beside the range check / layout
+  cudaStream_t aux = nullptr;            // load: rank codes beside the range check / layout;
+                                         // pass 2: tail tiles beside the pair launch
   cudaEvent_t ev_in = nullptr, ev_ranks = nullptr;
   size_t rank_scratch_words = 0;
   CUtensorMap tm_ra, tm_rb;
@@ -674,6 +675,14 @@ int launch_tie_scan(pald_gpu_plan* p, const uint32_t* keys, const int* rows, con
 int check_stats(const pald_gpu_plan* p, const Stats& st, bool validate, bool* fast_out, int* p2_out);
 int tie_summary(pald_gpu_plan* p, cudaStream_t s);
 
+int ensure_aux(pald_gpu_plan* p) {
+  if (p->aux) return PALD_GPU_OK;
+  PALD_CUDA(cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking));
+  PALD_CUDA(cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming));
+  PALD_CUDA(cudaEventCreateWithFlags(&p->ev_ranks, cudaEventDisableTiming));
+  return PALD_GPU_OK;
+}
+
 int plan_load_impl(pald_gpu_plan* p, const float* dD, uint64_t ldd, cudaStream_t s) {
   const int n = (int)p->n;
   Stats init{};
@@ -691,11 +700,7 @@ int plan_load_impl(pald_gpu_plan* p, const float* dD, uint64_t ldd, cudaStream_t
   const bool mark = ranks && p->sym_masks && p->algorithm == PALD_GPU_PAIRWISE && p->policy == PALD_GPU_STRICT &&
                     sym_enabled();
   if (ranks) {
-    if (!p->aux) {
-      PALD_CUDA(cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking));
-      PALD_CUDA(cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming));
-      PALD_CUDA(cudaEventCreateWithFlags(&p->ev_ranks, cudaEventDisableTiming));
-    }
+    if ((rc = ensure_aux(p))) return rc;
     PALD_CUDA(cudaEventRecord(p->ev_in, s));  // D is ready in stream order of s
     PALD_CUDA(cudaStreamWaitEvent(p->aux, p->ev_in, 0));
     if (mark) {
@@ -1104,16 +1109,32 @@ int plan_cohesion_impl(pald_gpu_plan* p, uint64_t row0, uint64_t row1, cudaStrea
         return PALD_GPU_OK;
       }
     }
-    int rc = launch_sym(p, 0, p->sym_main_pairs, s);
-    if (rc == PALD_GPU_OK) {
+    // 64-wide tail tiles (large n, 2+ tail rounds) run on the aux stream
+    // beside the pair launch: their CTAs take the SMs that the pair launch's
+    // CTAs free first (disjoint C entries, read-only inputs): n = 32768 pass
+    // 2 2483.6 -> 2478.5 ms. A one-round 32-wide tail runs after it (beside
+    // it, some tail CTAs were dispatched ahead of pair CTAs: config 3 pass 2
+    // 39.66 -> 39.86 ms).
+    int rc;
+    const bool tail = p->tail_count > 0 && p->tail_tile == 64;
+    if (tail) {
+      if ((rc = ensure_aux(p))) return rc;
+      PALD_CUDA(cudaEventRecord(p->ev_in, s));
+    }
+    if ((rc = launch_sym(p, 0, p->sym_main_pairs, s))) return rc;
+    ++p->launches;
+    p->last_kernel = PALD_GPU_KERNEL_PAIRS;
+    if (tail) {
+      PALD_CUDA(cudaStreamWaitEvent(p->aux, p->ev_in, 0));
+      if ((rc = launch_tail(p, p->tail, p->tail_count, p->aux))) return rc;
       ++p->launches;
-      p->last_kernel = PALD_GPU_KERNEL_PAIRS;
+      PALD_CUDA(cudaEventRecord(p->ev_ranks, p->aux));
+      PALD_CUDA(cudaStreamWaitEvent(s, p->ev_ranks, 0));
+    } else if (p->tail_count > 0) {
+      if ((rc = launch_tail(p, p->tail, p->tail_count, s))) return rc;
+      ++p->launches;
     }
-    if (rc == PALD_GPU_OK && p->tail_count > 0) {
-      rc = launch_tail(p, p->tail, p->tail_count, s);
-      if (rc == PALD_GPU_OK) ++p->launches;
-    }
-    return rc;
+    return PALD_GPU_OK;
   }
   static const int force_tile = [] {
     const char* e = getenv("PALD_GPU_COHESION_TILE");  // testing knob: 64 or 128
