@@ -109,7 +109,10 @@ int pald_gpu_abi_version(void);
  * blocked_triplet<float> / parallel_triplet<float> (blocked.hpp:424-477,
  * parallel.hpp:257-320) after to_real<float> (blocked.hpp:91-96).
  * D, U_out, C_out are HOST pointers, dense (ld = n). U_out may be NULL.
- * Pinned host memory gives full-speed copies. Synchronous. */
+ * Pinned host memory gives full-speed copies. Synchronous. For
+ * 2048 < n <= 32768 D is copied in bands of 2048 rows and pass 1 starts on
+ * the bands that have arrived; validation errors are then reported after
+ * the last band (the result is the same error code and message). */
 int pald_gpu_cohesion_f32(const float* D, uint64_t n, const pald_gpu_opts* opts,
                           int32_t* U_out, float* C_out, pald_gpu_phase_times* times);
 
