@@ -920,9 +920,9 @@ int launch_cohesion(pald_gpu_plan* p, uint64_t row0, uint64_t row1, cudaStream_t
   const int grid = (int)std::min<long long>(tiles, (long long)p->sms * ctas_per_sm(TILE));
   const bool tri = p->algorithm == PALD_GPU_TRIPLET;
   const bool split = p->policy == PALD_GPU_INCLUSIVE_SPLIT;
-  const CUtensorMap& md = TILE == 64 ? p->tm_d64 : p->tm_d;
-  const CUtensorMap& mn = TILE == 64 ? p->tm_dnu64 : p->tm_dnu;
-  const CUtensorMap& mw = TILE == 64 ? p->tm_w64 : p->tm_w;
+  const CUtensorMap& md = TILE == 64 ? p->tm_d64 : TILE == 32 ? p->tm_dt32 : p->tm_d;
+  const CUtensorMap& mn = TILE == 64 ? p->tm_dnu64 : TILE == 32 ? p->tm_dnut32 : p->tm_dnu;
+  const CUtensorMap& mw = TILE == 64 ? p->tm_w64 : TILE == 32 ? p->tm_wt32 : p->tm_w;
   if (!p->exact) {
     return tri     ? launch_tile<1, true, true, false, true, true, false, TILE>(md, mn, mw, a, grid, s)
            : split ? launch_tile<1, false, false, false, false, true, true, TILE>(md, mn, mw, a, grid, s)
@@ -1137,11 +1137,13 @@ int plan_cohesion_impl(pald_gpu_plan* p, uint64_t row0, uint64_t row1, cudaStrea
     return PALD_GPU_OK;
   }
   static const int force_tile = [] {
-    const char* e = getenv("PALD_GPU_COHESION_TILE");  // testing knob: 64 or 128
+    const char* e = getenv("PALD_GPU_COHESION_TILE");  // testing knob: 32, 64 or 128
     return e ? atoi(e) : 0;
   }();
   const bool small = force_tile ? force_tile == 64 : tiles128 < (uint64_t)p->sms;
-  const int rc = small ? launch_cohesion<64>(p, row0, row1, s) : launch_cohesion<kTile>(p, row0, row1, s);
+  const int rc = force_tile == 32 ? launch_cohesion<32>(p, row0, row1, s)
+                 : small          ? launch_cohesion<64>(p, row0, row1, s)
+                                  : launch_cohesion<kTile>(p, row0, row1, s);
   if (rc == PALD_GPU_OK) {
     ++p->launches;
     p->last_kernel = small ? PALD_GPU_KERNEL_TILE64 : PALD_GPU_KERNEL_TILE128;

@@ -21,6 +21,7 @@ SCRIPT = Path(__file__).resolve().parent / "scripts" / "tile_parity.py"
     ("64", "0", "2", ["3", "64", "257", "520"]),
     ("128", "2", "2", ["2", "127", "128", "129", "300", "520"]),
     ("128", "2", "0", ["2", "65", "129", "300"]),
+    ("32", "0", "2", ["2", "33", "65", "129", "300"]),  # the tail tiles' width (pald_gpu.cu tail)
 ])
 def test_cohesion_tile_width(tile, sym, rank, sizes):
     env = dict(os.environ, PALD_GPU_COHESION_TILE=tile, PALD_GPU_SYM=sym, PALD_GPU_RANK=rank)
