@@ -739,7 +739,10 @@ int plan_load_impl(pald_gpu_plan* p, const float* dD, uint64_t ldd, cudaStream_t
   // duplicate scan of the columns of D (marks of the tile-pair kernel) is
   // skipped where the pair kernel cannot win even tie-free.
   if (fast && p->algorithm == PALD_GPU_TRIPLET && sym_enabled() && sym_wins(p, 0.0)) p->sym_ready = true;
-  const bool tie_scan = fast && p->sym_masks && sym_enabled() && sym_wins(p, 0.0);
+  // (a cached plan made for a strict call keeps its masks when reused for
+  // InclusiveSplit: the pair kernel is strict-only)
+  const bool tie_scan = fast && p->sym_masks && p->algorithm == PALD_GPU_PAIRWISE && p->policy == PALD_GPU_STRICT &&
+                        sym_enabled() && sym_wins(p, 0.0);
   if (tie_scan) {
     if (!mark) {  // no rank codes: scan every column of the layout
       PALD_CUDA(cudaMemsetAsync(p->sym_masks, 0, sym_mask_words(p) * sizeof(uint32_t), s));
@@ -1087,7 +1090,9 @@ bool sym_wins(const pald_gpu_plan* p, double marked) {
   const double t_64 = std::ceil(nb64 * nb64 / (2 * sms)) * 0.52;
   return t_sym < std::min(t_128, t_64);
 }
-bool sym_preferred(const pald_gpu_plan* p) { return sym_wins(p, p->sym_marked); }
+// The pair kernel implements the strict policy only (InclusiveSplit takes
+// the one-sided kernel).
+bool sym_preferred(const pald_gpu_plan* p) { return p->policy == PALD_GPU_STRICT && sym_wins(p, p->sym_marked); }
 
 int plan_cohesion_impl(pald_gpu_plan* p, uint64_t row0, uint64_t row1, cudaStream_t s) {
   if (!p->loaded) return set_error(PALD_GPU_ERR_VALIDATION, "plan has no distances loaded");

@@ -374,3 +374,42 @@ def test_host_api_banded_matches_engine_special_layouts(case):
     assert e.exact_path
     assert np.array_equal(u, e.U.cpu().numpy())
     assert np.array_equal(c, e.C.cpu().numpy(), equal_nan=True)
+
+
+def test_cached_plan_strict_then_split():
+    """The one-shot API caches one plan per device and size: a strict call
+    (tie masks, pair kernel) followed by an InclusiveSplit call of the same
+    n must run the split semantics (one-sided kernel), equal to a plan made
+    for InclusiveSplit."""
+    import torch
+
+    from paper_2307_16652_b200 import _lib
+    from paper_2307_16652_b200.api import _raise_for
+    from paper_2307_16652_b200.engine import Engine
+
+    n = 2500
+    # a few duplicates per column: the pair kernel stays preferred for strict,
+    # and InclusiveSplit differs from strict on those ties
+    d = (np.round(random_upper(n, 21) * 2 ** 20) / 2 ** 20).astype(np.float32)
+    lib = _lib.load()
+    u = np.empty((n, n), np.int32)
+    c = np.empty((n, n), np.float32)
+    for policy in (_lib.STRICT, _lib.INCLUSIVE_SPLIT):
+        opts = _lib.make_opts(algorithm=_lib.PAIRWISE, policy=policy)
+        _raise_for(lib.pald_gpu_cohesion_f32(d.ctypes.data, n, C.byref(opts), u.ctypes.data, c.ctypes.data, None))
+    e = Engine(n, "pairwise", policy="split")
+    D = torch.from_numpy(d).cuda()
+    e.run(D)
+    torch.cuda.synchronize()
+    assert np.array_equal(u, e.U.cpu().numpy())
+    assert np.array_equal(c.view(np.uint32), e.C.cpu().numpy().view(np.uint32))
+    # the device-pointer API (load through the range check + layout path)
+    Ud = torch.empty((n, n), dtype=torch.int32, device="cuda")
+    Cd = torch.empty((n, n), dtype=torch.float32, device="cuda")
+    for policy in (_lib.STRICT, _lib.INCLUSIVE_SPLIT):
+        opts = _lib.make_opts(algorithm=_lib.PAIRWISE, policy=policy)
+        _raise_for(lib.pald_gpu_cohesion_f32_device(D.data_ptr(), n, n, C.byref(opts), Ud.data_ptr(), n,
+                                                    Cd.data_ptr(), n, None))
+        torch.cuda.synchronize()
+    assert torch.equal(Ud, e.U)
+    assert torch.equal(Cd.view(torch.int32), e.C.view(torch.int32))
