@@ -472,18 +472,16 @@ int plan_alloc(pald_gpu_plan* p) {
   if ((rc = make_map(&p->tm_dt32, p->ds, p->n, p->ld, 32))) return rc;
   if ((rc = make_map(&p->tm_dnut32, p->dnu, p->n, p->ld, 32))) return rc;
   if ((rc = make_map(&p->tm_wt32, p->w, p->n, p->ld, 32))) return rc;
-  if (p->policy == PALD_GPU_STRICT) {
-    if ((rc = make_map(&p->tm_d32, p->ds, p->n, p->ld, kTile, kSymBK))) return rc;
-    if ((rc = make_map(&p->tm_dnu32, p->dnu, p->n, p->ld, kTile, kSymBK))) return rc;
-    if ((rc = make_map(&p->tm_w32, p->w, p->n, p->ld, kTile, kSymBK))) return rc;
-    p->sym_nch = (int)((p->n + kSymBK - 1) / kSymBK);
-    PALD_CUDA(cudaMalloc(&p->round_bar, sizeof(unsigned int)));
-  }
-  if (p->algorithm == PALD_GPU_PAIRWISE && p->policy == PALD_GPU_STRICT) {
-    PALD_CUDA(cudaMalloc(&p->sym_masks, sym_mask_words(p) * sizeof(uint32_t)));
-    PALD_CUDA(cudaMalloc(&p->sym_tile_flags, p->nb * sizeof(uint32_t)));
-    PALD_CUDA(cudaMalloc(&p->sym_count, sizeof(unsigned long long)));
-  }
+  // Pair-kernel state for every algorithm / policy: the one-shot APIs
+  // reuse a cached plan across calls with other options (same n).
+  if ((rc = make_map(&p->tm_d32, p->ds, p->n, p->ld, kTile, kSymBK))) return rc;
+  if ((rc = make_map(&p->tm_dnu32, p->dnu, p->n, p->ld, kTile, kSymBK))) return rc;
+  if ((rc = make_map(&p->tm_w32, p->w, p->n, p->ld, kTile, kSymBK))) return rc;
+  p->sym_nch = (int)((p->n + kSymBK - 1) / kSymBK);
+  PALD_CUDA(cudaMalloc(&p->round_bar, sizeof(unsigned int)));
+  PALD_CUDA(cudaMalloc(&p->sym_masks, sym_mask_words(p) * sizeof(uint32_t)));
+  PALD_CUDA(cudaMalloc(&p->sym_tile_flags, p->nb * sizeof(uint32_t)));
+  PALD_CUDA(cudaMalloc(&p->sym_count, sizeof(unsigned long long)));
   // The memsets above run on the legacy default stream; callers may use
   // non-blocking streams, so finish them before the plan is handed out.
   PALD_CUDA(cudaDeviceSynchronize());

@@ -413,3 +413,28 @@ def test_cached_plan_strict_then_split():
         torch.cuda.synchronize()
     assert torch.equal(Ud, e.U)
     assert torch.equal(Cd.view(torch.int32), e.C.view(torch.int32))
+
+
+def test_cached_plan_split_then_triplet():
+    """A plan created for an InclusiveSplit call, reused (same n) for a
+    triplet call, must still have the pair kernel's state (tensor maps,
+    chunk count) for the triplet's pass 2."""
+    import torch
+
+    from paper_2307_16652_b200 import _lib
+    from paper_2307_16652_b200.api import _raise_for
+    from paper_2307_16652_b200.engine import Engine
+
+    n = 2600
+    d = random_upper(n, 23)
+    lib = _lib.load()
+    u = np.empty((n, n), np.int32)
+    c = np.empty((n, n), np.float32)
+    for alg, policy in ((_lib.PAIRWISE, _lib.INCLUSIVE_SPLIT), (_lib.TRIPLET, _lib.STRICT)):
+        opts = _lib.make_opts(algorithm=alg, policy=policy)
+        _raise_for(lib.pald_gpu_cohesion_f32(d.ctypes.data, n, C.byref(opts), u.ctypes.data, c.ctypes.data, None))
+    e = Engine(n, "triplet")
+    e.run(torch.from_numpy(d).cuda())
+    torch.cuda.synchronize()
+    assert np.array_equal(u, e.U.cpu().numpy())
+    assert max_rel_diff(c, e.C.cpu().numpy()) <= TOL
