@@ -20,7 +20,11 @@ NCCL exchange of U/W between the passes and the all-gather of C.
                 launch / its CUDA-event duration vs. the issue peak
                 148 SM x 128 lanes x sm_max_mhz (MEASURED_PEAKS.json).
 * ``cpu_baseline`` the UNMODIFIED reference (oracle/_ref, parallel_pairwise
-                <float>) on the host cores, bounded prefix sample.
+                <float>) on the host cores: timed block pairs of its own driver
+                loop extrapolated by pair counts + its O(n^2) part, anchored
+                against a full run at n = 8192 (``anchor.rel_error``).
+* ``shim_e2e``  the drop-in C++ call (pald::gpu::parallel_pairwise<float> on the
+                reference's own types, tools/_bin/shim_bench), wall clock.
 
 ``--impl reference`` times the reference CPU implementation alone (rank 0).
 """
@@ -145,80 +149,151 @@ def make_input(cfg_index: int, device, seed: int):
     return torch.from_numpy(datagen.make_distances(cfg, seed)).to(device), cfg
 
 
-def cpu_reference_sample(d_host: np.ndarray, budget_s: float, cores: int):
-    """Time the unmodified reference parallel_pairwise<float> on a prefix of
-    x-rows (ref_bridge.cpp ref_parallel_pairwise_prefix_f32) and extrapolate
-    by the exact fraction of pair work. Returns (triplets/s, info)."""
-    from oracle.oracle import Reference, pair_work_fraction
+def ref_estimate(ref, d32: np.ndarray, b: int, cores: int, budget_s: float, overhead_s: float, rotate: int = 0,
+                 t1: float | None = None):
+    """Seconds of one full parallel_pairwise<float> call of the UNMODIFIED
+    reference (parallel.hpp:159-222) at its default block size b, estimated
+    from a timed sample of whole block pairs of its own driver loop
+    (ref_bridge.cpp ref_parallel_pairwise_blockpairs_f32: focus over the
+    workers' z ranges, the rank-order count sum, reciprocals, cohesion):
+    diagonal and off-diagonal block pairs are sampled separately (spread
+    over the matrix) and extrapolated by their pair counts, plus the call's
+    O(n^2) part (to_real, buffers, collect_result) `overhead_s`.
+    Returns (seconds, info)."""
+    n = d32.shape[0]
+    nb = -(-n // b)
+    size = lambda i: min(b, n - i * b)  # noqa: E731
+    diag_pairs_total = sum(size(i) * (size(i) - 1) / 2 for i in range(nb))
+    off_pairs_total = n * (n - 1) / 2 - diag_pairs_total
+    full = [i for i in range(nb) if size(i) == b] or [0]
+    offs = []
+    diags = [full[rotate % len(full)]]
+    if nb > 1:
+        if t1 is None:  # calibration: one off-diagonal block pair
+            t1 = float(ref.parallel_pairwise_blockpairs_f32(d32, b, cores, [(0, 1)])[0])
+        if budget_s >= 3 * t1:
+            diags = sorted({full[rotate % len(full)], full[(rotate + len(full) // 2) % len(full)]})
+        k = int(max(1, min(nb * (nb - 1) // 2, round(max(budget_s - t1 * len(diags) / 2, t1) / t1))))
+        allp = [(x, y) for x in range(nb) for y in range(x + 1, nb)]
+        # k off-diagonal block pairs spread evenly over the list (rotated
+        # between calls so that repeated estimates cover different blocks)
+        stride = len(allp) / k
+        offs = sorted({allp[(int(i * stride) + rotate * 7919) % len(allp)] for i in range(k)})
+    pairs = [(x, x) for x in diags] + offs
+    secs = ref.parallel_pairwise_blockpairs_f32(d32, b, cores, pairs)
+    t_diag = secs[: len(diags)].sum()
+    p_diag = sum(size(x) * (size(x) - 1) / 2 for x in diags)
+    est = t_diag / p_diag * diag_pairs_total
+    if offs:
+        t_off = secs[len(diags):].sum()
+        p_off = sum(size(x) * size(y) for x, y in offs)
+        est += t_off / p_off * off_pairs_total
+    est += overhead_s
+    sampled = p_diag + (sum(size(x) * size(y) for x, y in offs) if offs else 0)
+    return est, {"block_pairs": [list(map(int, q)) for q in pairs], "fraction": sampled / (n * (n - 1) / 2),
+                 "sample_s": float(secs.sum()), "overhead_s": overhead_s, "t1": t1}
+
+
+def ref_overhead(ref, n: int) -> float:
+    """The O(n^2) part of a parallel_pairwise<float> call, measured at
+    min(n, 8192) and scaled by the element count (memory-bound loops)."""
+    m = min(n, 8192)
+    return ref.pairwise_overhead_f32(m) * (n / m) ** 2
+
+
+def cpu_reference_sample(d_host: np.ndarray, budget_s: float, cores: int, anchor_n: int = 8192,
+                         seed: int = 20230731):
+    """The unmodified reference parallel_pairwise<float> on the host cores:
+    block-pair sample at the bench size (ref_estimate), plus an ANCHOR: at
+    n = anchor_n the same estimator is compared against one full
+    parallel_pairwise<float> call (the reference's own driver, PhaseTimes
+    total) to bound the extrapolation error. Returns (triplets/s, info)."""
+    from oracle.oracle import Reference
 
     ref = Reference()
     n = d_host.shape[0]
     b = ref.default_block_config(4)[0]
-    # calibrate on a tiny prefix, then size the sample to ~budget_s
-    x_small = max(1, n // 2048)
-    t_small, _, _ = ref.parallel_pairwise_prefix_f32(d_host, b, cores, x_small)
-    frac_small = pair_work_fraction(n, x_small)
-    est_full = t_small / frac_small
-    target_frac = min(1.0, budget_s / est_full)
-    x_lim = 1
-    while x_lim < n and pair_work_fraction(n, x_lim) < target_frac:
-        x_lim = int(x_lim * 1.25) + 1
-    x_lim = min(x_lim, n)
-    t, _, _ = ref.parallel_pairwise_prefix_f32(d_host, b, cores, x_lim)
-    frac = pair_work_fraction(n, x_lim)
-    t_full = t / frac
-    return n ** 3 / t_full, {
-        "sample": f"parallel_pairwise<float> (b={b}, p={cores}) over x-rows [0,{x_lim}) of n={n}: "
-                  f"{frac:.5f} of the pair work in {t:.2f} s, extrapolated to {t_full:.1f} s",
-        "seconds_sample": t, "fraction": frac, "lib": ref.path.name,
+    t_full, smp = ref_estimate(ref, d_host, b, cores, budget_s, ref_overhead(ref, n))
+    info = {
+        "sample": f"parallel_pairwise<float> (b={b}, p={cores}) block pairs {smp['block_pairs']} of n={n} "
+                  f"({smp['fraction']:.5f} of the pairs, {smp['sample_s']:.1f} s) extrapolated by pair counts, "
+                  f"+ O(n^2) part {smp['overhead_s']:.2f} s = {t_full:.1f} s per call",
+        "lib": ref.path.name, "seconds_per_call": t_full,
     }
+    if anchor_n and anchor_n < n:
+        pts = np.random.default_rng(seed).random((anchor_n, 3))
+        rc, msg, da64 = ref.points_to_distances(pts)
+        if rc:
+            raise RuntimeError(msg)
+        da = da64.astype(np.float32)
+        t_est, asmp = ref_estimate(ref, da, b, cores, 8.0, ref.pairwise_overhead_f32(anchor_n))
+        _, _, tt = ref.parallel_pairwise(da.astype(np.float64), b, cores, use_float=True)
+        full = float(tt[3])
+        info["anchor"] = {"n": anchor_n, "full_run_s": full, "phase_times_s": [float(x) for x in tt],
+                          "estimate_s": t_est, "estimate_blocks": asmp["block_pairs"],
+                          "rel_error": (t_est - full) / full,
+                          "input": "points i.i.d. U[0,1)^3 (config-5 generator at n=%d), reference "
+                                   "points_to_distances" % anchor_n}
+    return n ** 3 / t_full, info
 
 
 # ---------------------------------------------------------------------------
 def run_reference_arm(args) -> None:
-    """--impl reference: the reference CPU implementation on the host cores."""
+    """--impl reference: the reference CPU implementation on the host cores.
+    The input D is built by the reference's own points_to_distances
+    (ingest.hpp:303-322) from the same seeded points; each step is the
+    block-pair estimate of one full parallel_pairwise<float> call."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from paper_2307_16652_b200 import datagen
-    from oracle.oracle import Reference, host_cores, pair_work_fraction
+    from oracle.oracle import Reference, host_cores
 
     cfg = datagen.config(args.config)
     cores = host_cores()
-    pts = datagen.make_points(cfg, args.seed)
-    d = datagen.distances_from_points(pts) if pts is not None else datagen.make_distances(cfg, args.seed)
     ref = Reference()
+    pts = datagen.make_points(cfg, args.seed)
+    if pts is not None:
+        rc, msg, d64 = ref.points_to_distances(pts)
+        if rc:
+            raise RuntimeError(msg)
+        d = d64.astype(np.float32)  # to_real<float>
+        del d64
+    else:
+        d = datagen.make_distances(cfg, args.seed)
     n = cfg.n
     b = ref.default_block_config(4)[0]
-    # size each step to ~args.ref_step_s seconds of CPU work
-    x_small = max(1, n // 4096)
-    t_small, _, _ = ref.parallel_pairwise_prefix_f32(d, b, cores, x_small)
-    est_full = t_small / pair_work_fraction(n, x_small)
-    x_lim = 1
-    while x_lim < n and pair_work_fraction(n, x_lim) < args.ref_step_s / est_full:
-        x_lim = int(x_lim * 1.25) + 1
-    x_lim = min(x_lim, n)
-    frac = pair_work_fraction(n, x_lim)
-    times = []
-    for i in range(args.warmup + args.steps):
-        t, _, _ = ref.parallel_pairwise_prefix_f32(d, b, cores, x_lim)
-        if i >= args.warmup:
-            times.append(t / frac)
-    t_step = statistics.mean(times)
+    overhead = ref_overhead(ref, n)
+    t1 = None
+    for w in range(args.warmup):
+        _, smp = ref_estimate(ref, d, b, cores, args.ref_step_s, overhead, rotate=1000 + w, t1=t1)
+        t1 = smp["t1"]
+    runs, smp = [], None
+    for i in range(args.steps):  # each step samples other block pairs
+        t, smp = ref_estimate(ref, d, b, cores, args.ref_step_s, overhead, rotate=i, t1=t1)
+        runs.append(t)
+    t_step = statistics.mean(runs)
     value = n ** 3 / t_step
     line = {
         "metric": "pald_cohesion_triplets_per_s", "value": value, "unit": "triplets/s",
         "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": cfg.name, "n": n, "algorithm": "pairwise", "seed": args.seed},
+        "config": bench_config(cfg, args.seed),
         "cpu_baseline": {"value": value, "unit": "triplets/s", "cores": cores, "kind": "reference",
-                         "sample": f"each step: parallel_pairwise<float> (b={b}, p={cores}) over x-rows "
-                                   f"[0,{x_lim}) = {frac:.5f} of the pair work, extrapolated by that fraction",
-                         "lib": ref.path.name},
+                         "sample": f"each step: parallel_pairwise<float> (b={b}, p={cores}) block pairs "
+                                   f"{smp['block_pairs']} ({smp['fraction']:.5f} of the pairs) extrapolated by "
+                                   f"pair counts + the call's O(n^2) part ({overhead:.1f} s); the estimator is "
+                                   "anchored against a full run at n=8192 in our arm's cpu_baseline.anchor",
+                         "lib": ref.path.name, "step_estimates_s": runs},
         "e2e": {"value": value, "unit": "triplets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def bench_config(cfg, seed: int) -> dict:
+    """The workload dict, identical in both arms (extra facts go to sibling keys)."""
+    return {"workload": cfg.name, "n": cfg.n, "algorithm": "pairwise", "seed": seed}
 
 
 # ---------------------------------------------------------------------------
@@ -286,8 +361,9 @@ def time_engine_steps(engine, runner, D, steps: int, warmup: int, dist_on: bool)
     return total_ms / steps, avg, launches
 
 
-def e2e_host(n: int, D_dev, steps: int, warmup: int):
-    """pald_gpu_cohesion_f32 (C ABI, host pointers) with pinned buffers."""
+def e2e_host(n: int, D_dev, steps: int, warmup: int, devices=None, flags: int = 0):
+    """pald_gpu_cohesion_f32 (C ABI, host pointers) with pinned buffers; with
+    ``devices`` one call spans those GPUs (ABI v4 device list)."""
     import ctypes as C
 
     import torch
@@ -295,7 +371,7 @@ def e2e_host(n: int, D_dev, steps: int, warmup: int):
     from paper_2307_16652_b200.api import _raise_for
 
     lib = _lib.load()
-    opts = _lib.make_opts(algorithm=_lib.PAIRWISE)
+    opts = _lib.make_opts(algorithm=_lib.PAIRWISE, devices=devices, flags=flags)
     d_h = torch.empty((n, n), dtype=torch.float32, pin_memory=True)
     d_h.copy_(D_dev)
     u_h = torch.empty((n, n), dtype=torch.int32, pin_memory=True)
@@ -312,6 +388,41 @@ def e2e_host(n: int, D_dev, steps: int, warmup: int):
     checksum = float(c_h[:64].double().sum())
     del d_h, u_h, c_h
     return n ** 3 / t, t, checksum
+
+
+def shim_e2e(cfg, seed: int, steps: int, warmup: int, devices=None):
+    """The drop-in C++ call of a reference user, end to end:
+    pald::gpu::parallel_pairwise<float>(pald::DistanceMatrix, b, plan) built
+    against the reference's own types (tools/_bin/shim_bench): double D in,
+    a freshly allocated PaldResult (int32 U, double C) out, wall clock per
+    call. D is built from the same seeded points with the reference's own
+    points_to_distances (outside the timed region)."""
+    from paper_2307_16652_b200 import datagen
+
+    exe = ROOT / "tools" / "_bin" / "shim_bench"
+    if not exe.exists():
+        return {"value": None, "error": "tools/_bin/shim_bench not built (needs the reference headers)"}
+    pts = datagen.make_points(cfg, seed)
+    path = Path(f"/tmp/pald_points_{os.getpid()}.f64")
+    np.ascontiguousarray(pts, np.float64).tofile(path)
+    cmd = [str(exe), str(path), str(cfg.n), str(pts.shape[1]), str(steps), str(warmup)]
+    if devices:
+        cmd.append(",".join(str(d) for d in devices))
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    finally:
+        path.unlink(missing_ok=True)
+    if r.returncode != 0:
+        return {"value": None, "error": (r.stdout + r.stderr)[-400:]}
+    j = json.loads(r.stdout.strip().splitlines()[-1])
+    n = cfg.n
+    return {"value": n ** 3 / j["seconds_per_step"], "unit": "triplets/s",
+            "seconds_per_step": j["seconds_per_step"], "times": j["times"], "phase_times": j["phase_times"],
+            "devices": j["devices"],
+            "h2d_bytes_per_step": n * n * 4, "d2h_bytes_per_step": 2 * n * n * 4,
+            "host_bytes_per_step": {"D_double_in": n * n * 8, "U_int32_out": n * n * 4, "C_double_out": n * n * 8},
+            "path": "pald::gpu::parallel_pairwise<float>(pald::DistanceMatrix, b, plan) -- C++ shim on the "
+                    "reference's own types: double D in, PaldResult (int32 U, double C, fresh vectors) out"}
 
 
 def e2e_sharded(engine, runner, D_dev, steps: int, warmup: int, rank: int):
@@ -334,7 +445,7 @@ def e2e_sharded(engine, runner, D_dev, steps: int, warmup: int, rank: int):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         engine.load_host(d_h)
-        if runner.fused:
+        if runner.focus_exchange == "red":
             runner._sync_barrier()
         runner.focus()
         runner.exchange_focus()
@@ -401,7 +512,7 @@ def main() -> None:
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=5, help="BASELINE.json config index (1-5)")
     ap.add_argument("--seed", type=int, default=20230731)
-    ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU baseline sample")
+    ap.add_argument("--cpu-budget", type=float, default=30.0, help="seconds of CPU baseline sample")
     ap.add_argument("--ref-step-s", type=float, default=4.0, help="seconds per --impl reference step")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -476,11 +587,11 @@ def main() -> None:
         "vs_baseline": None,
         "dtype": "f32",
         "data": DATA_DESC.get(cfg.kind, "synthetic"),
-        "config": {"workload": cfg.name, "n": n, "algorithm": "pairwise", "seed": args.seed,
-                   "parallelism": (f"tile-pair shares x{world}; exchange: "
-                                   + ("fused peer-memory stores over NVLink (CUDA IPC)" if runner.fused
-                                      else "NCCL all-reduces")),
-                   "l2": "inputs larger than L2 (D = %.1f GiB > 126 MB)" % (n * n * 4 / 2 ** 30)},
+        "config": bench_config(cfg, args.seed),
+        "parallelism": (f"pass-1 unit shares / pass-2 tile-pair shares x{world}; exchange: pass 1 "
+                        f"{runner.focus_exchange}, pass 2 {runner.cohesion_exchange} "
+                        "(peer = kernels over CUDA IPC peer memory, nccl = SUM all-reduce)"),
+        "l2": "inputs larger than L2 (D = %.1f GiB > 126 MB)" % (n * n * 4 / 2 ** 30),
         "roofline": {
             "bound": "issue", "kernel": info["cohesion_kernel"],
             "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Gop/s",
@@ -509,6 +620,10 @@ def main() -> None:
                                "path": "pald_gpu_cohesion_f32 (C ABI), pinned host buffers"}
             except Exception as e:  # report, never hide
                 line["e2e"] = {"value": None, "error": repr(e)}
+            try:
+                line["shim_e2e"] = shim_e2e(cfg, args.seed, max(1, min(args.steps, 2)), 1)
+            except Exception as e:
+                line["shim_e2e"] = {"value": None, "error": repr(e)}
         if not args.no_cpu_baseline:
             try:
                 from oracle.oracle import host_cores
@@ -517,7 +632,7 @@ def main() -> None:
                 cores = host_cores()
                 v, info = cpu_reference_sample(d_host, args.cpu_budget, cores)
                 line["cpu_baseline"] = {"value": v, "unit": "triplets/s", "cores": cores,
-                                        "kind": "reference", "sample": info["sample"], "lib": info["lib"]}
+                                        "kind": "reference", **info}
                 del d_host
             except Exception as e:
                 line["cpu_baseline"] = {"value": None, "error": repr(e)}
@@ -528,11 +643,29 @@ def main() -> None:
     elif not args.no_e2e:
         try:
             ev, et = e2e_sharded(engine, runner, D, max(1, min(args.steps, 3)), 1, rank)
-            line["e2e"] = {"value": ev, "unit": "triplets/s", "seconds_per_step": et,
-                           "h2d_bytes_per_step": world * n * n * 4, "d2h_bytes_per_step": 2 * n * n * 4,
-                           "path": "ShardedRunner over the staged C ABI, pinned host D per rank, U/C to rank 0"}
+            line["e2e_sharded"] = {"value": ev, "unit": "triplets/s", "seconds_per_step": et,
+                                   "h2d_bytes_per_step": world * n * n * 4, "d2h_bytes_per_step": 2 * n * n * 4,
+                                   "path": "ShardedRunner (one process per GPU) over the staged C ABI, pinned "
+                                           "host D per rank, U/C to rank 0"}
         except Exception as e:
-            line["e2e"] = {"value": None, "error": repr(e)}
+            line["e2e_sharded"] = {"value": None, "error": repr(e)}
+        # the headline e2e: ONE C-ABI call from rank 0 spanning all N GPUs
+        # (pald_gpu_opts.devices; the call pald::gpu::parallel_pairwise makes)
+        del runner, engine
+        torch.cuda.empty_cache()
+        dist.barrier()
+        if rank == 0:
+            try:
+                # the ranks' GPUs (PALD_BENCH_BACKEND=gloo test runs share the visible ones)
+                devs = [r % torch.cuda.device_count() for r in range(world)]
+                ev, et, _ = e2e_host(n, D, max(1, min(args.steps, 3)), 1, devices=devs)
+                line["e2e"] = {"value": ev, "unit": "triplets/s", "seconds_per_step": et,
+                               "h2d_bytes_per_step": n * n * 4, "d2h_bytes_per_step": 2 * n * n * 4,
+                               "path": f"pald_gpu_cohesion_f32 (C ABI) with devices {devs} in one call, "
+                                       "pinned host buffers"}
+            except Exception as e:
+                line["e2e"] = {"value": None, "error": repr(e)}
+        dist.barrier()
 
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define PALD_GPU_ABI_VERSION 3
+#define PALD_GPU_ABI_VERSION 4
 
 /* Algorithm variant: blocked_pairwise / parallel_pairwise (blocked.hpp:368,
  * parallel.hpp:159) vs blocked_triplet / parallel_triplet (blocked.hpp:424,
@@ -68,7 +68,39 @@ enum pald_gpu_flags {
   PALD_GPU_FLAG_SKIP_VALIDATION = 1u,
   /* Use the integer-key compare path even when the fp32 range allows the
    * FFMA.SAT compare path (testing). */
-  PALD_GPU_FLAG_FORCE_EXACT = 2u
+  PALD_GPU_FLAG_FORCE_EXACT = 2u,
+  /* Accurate mode: pass 2 keeps each output's fp32 running sum only over
+   * blocks of PALD_GPU_ACC_BLOCK (default 256) third points and adds the
+   * block partials into a double sum (exact: see csrc/pald_kernels.cuh
+   * acc_flush4), rounded to fp32 at the end. C then stays within ~1e-6 of
+   * the fp64-accumulated result at n = 32768 (the default single fp32 chain
+   * is the reference's own order, bit-identical to blocked_pairwise<float>,
+   * and drifts by ~1.3e-5 there). Deterministic; the double sums are
+   * exposed as pald_gpu_buffers.C64. */
+  PALD_GPU_FLAG_ACCURATE = 4u
+};
+
+#define PALD_GPU_MAX_DEVICES 8
+
+/* Transport of the two exchange steps of a multi-device call (see
+ * DESIGN.md section 5 for the traffic model of each):
+ *   PEER  pass 1: each device finishes its 1/N of the tiles by reading the
+ *         partial counts of every device over peer memory (P2P loads) and
+ *         storing U and W = 1/U into every device (P2P stores) -- one fused
+ *         reduce + finish + all-gather kernel.
+ *         pass 2: the pair kernel stores each finished C tile into every
+ *         device (P2P stores, overlapped with the math).
+ *   NCCL  pass 1: ncclAllReduce(SUM) of the count buffers, local finish.
+ *         pass 2: each device computes its tile-row band; no exchange (the
+ *         host reads each band from the device that owns it).
+ *   RED   pass 1 only: the focus kernel adds every partial count into every
+ *         device's W (red.global.add over NVLink), local finish.
+ *   AUTO  PEER where every pair of devices has peer access, else NCCL. */
+enum pald_gpu_exchange {
+  PALD_GPU_EXCHANGE_AUTO = 0,
+  PALD_GPU_EXCHANGE_PEER = 1,
+  PALD_GPU_EXCHANGE_NCCL = 2,
+  PALD_GPU_EXCHANGE_RED = 3
 };
 
 typedef struct pald_gpu_opts {
@@ -86,6 +118,18 @@ typedef struct pald_gpu_opts {
   uint64_t block_cohesion;
   uint32_t flags;         /* enum pald_gpu_flags */
   uint32_t reserved;
+  /* ---- ABI v4: several devices in ONE call (the GPU counterpart of
+   * ParallelPlan.workers, parallel.hpp:31-34). num_devices 0 or 1: the
+   * single `device` above. num_devices > 1: devices[0..num_devices) (a
+   * device may repeat: the plans then share that GPU -- used to test the
+   * multi-device path on one GPU). Pass-1 work units and pass-2 tile pairs
+   * are split into equal shares, one per listed device; U and C are
+   * bit-identical to one device. A caller compiled against ABI v3 passes
+   * struct_size = PALD_GPU_OPTS_V3_SIZE and gets one device. */
+  int32_t num_devices;
+  int32_t devices[PALD_GPU_MAX_DEVICES];
+  int32_t exchange_focus;     /* enum pald_gpu_exchange: pass-1 count exchange */
+  int32_t exchange_cohesion;  /* enum pald_gpu_exchange: pass-2 C exchange */
 } pald_gpu_opts;
 
 /* PhaseTimes, types.hpp:114-119, filled from CUDA events. */
@@ -96,13 +140,20 @@ typedef struct pald_gpu_phase_times {
   double total_seconds;
 } pald_gpu_phase_times;
 
-/* Fills defaults: pairwise, strict, current device, blocks 128, flags 0. */
+/* sizeof(pald_gpu_opts) of ABI v3 (no device list). */
+#define PALD_GPU_OPTS_V3_SIZE 48u
+
+/* Fills defaults: pairwise, strict, current device, blocks 128, flags 0,
+ * one device, exchange AUTO. */
 void pald_gpu_opts_init(pald_gpu_opts* opts);
 
 /* Thread-local message of the last failing call on this thread. */
 const char* pald_gpu_last_error(void);
 
 int pald_gpu_abi_version(void);
+
+/* Number of visible CUDA devices (0 without a GPU or driver). */
+int pald_gpu_visible_devices(void);
 
 /* One-shot host API. Replaces blocked_pairwise<float> /
  * parallel_pairwise<float> (blocked.hpp:368-418, parallel.hpp:159-222) and
@@ -115,6 +166,25 @@ int pald_gpu_abi_version(void);
  * the last band (the result is the same error code and message). */
 int pald_gpu_cohesion_f32(const float* D, uint64_t n, const pald_gpu_opts* opts,
                           int32_t* U_out, float* C_out, pald_gpu_phase_times* times);
+
+/* Double-precision host I/O (ABI v4), for callers holding the reference's
+ * own types (DistanceMatrix stores doubles, PaldResult a double C;
+ * types.hpp:43-119) -- the C++ shim include/pald_gpu.hpp uses it. Same
+ * result as converting D with to_real<float> (blocked.hpp:91-96), calling
+ * pald_gpu_cohesion_f32 and widening C like collect_result
+ * (blocked.hpp:352-359); the conversions run on all host cores into / out
+ * of pinned staging buffers that the library keeps between calls
+ * (pald_gpu_release_host_staging frees them). begin() returns at once (a
+ * worker thread converts D and runs the GPU call) so the caller can build
+ * its result storage meanwhile; end() waits and writes U_out (nullable)
+ * and C_out. One job at a time per process (begin blocks until the
+ * previous job's end). Errors of the GPU call are returned by end(). */
+typedef struct pald_gpu_job pald_gpu_job;
+int pald_gpu_cohesion_f64io_begin(const double* D, uint64_t n, const pald_gpu_opts* opts, pald_gpu_job** job);
+int pald_gpu_cohesion_f64io_end(pald_gpu_job* job, int32_t* U_out, double* C_out, pald_gpu_phase_times* times);
+int pald_gpu_cohesion_f64io(const double* D, uint64_t n, const pald_gpu_opts* opts, int32_t* U_out,
+                            double* C_out, pald_gpu_phase_times* times);
+int pald_gpu_release_host_staging(void);
 
 /* Device API, asynchronous on `stream` (a cudaStream_t; NULL = legacy
  * default stream) except for one small device->host read of the range
@@ -152,6 +222,7 @@ typedef struct pald_gpu_buffers {
   uint64_t tiles_per_dim;
   int32_t exact_path;  /* 1 when the integer-key compare path is in use */
   int32_t reserved;
+  double* C64;       /* device, n x ld: accurate mode's double C (NULL until used; ABI v4) */
 } pald_gpu_buffers;
 
 int pald_gpu_plan_create(uint64_t n, const pald_gpu_opts* opts, pald_gpu_plan** out);
@@ -190,6 +261,9 @@ typedef struct pald_gpu_plan_info {
   double exact_step_share;    /* share of (pair, k) steps on the exact step */
   uint64_t launches;
   int32_t rank_codes;         /* 1: pass 1 runs on per-row rank codes (ABI v3) */
+  int32_t pair_kernel_preferred; /* 1: a full-range cohesion of the loaded D would run
+                                  * the pair kernel (multi-GPU drivers agree on it
+                                  * before a fused pass 2; ABI v4) */
 } pald_gpu_plan_info;
 int pald_gpu_plan_get_info(const pald_gpu_plan* plan, pald_gpu_plan_info* out);
 
@@ -219,6 +293,20 @@ int pald_gpu_plan_focus_counts_peers(pald_gpu_plan* plan, uint64_t part, uint64_
 int pald_gpu_plan_cohesion_share_peers(pald_gpu_plan* plan, uint64_t part, uint64_t parts,
                                        void* stream);
 
+/* Pass-1 exchange by peer pull (ABI v4): instead of the count fan-out of
+ * focus_counts_peers, every rank runs plain focus_counts (its share into
+ * its OWN W), the ranks meet at a host barrier, and each rank finishes
+ * share `part` of `parts` of the upper-triangular tiles: it sums the counts
+ * of every rank's W (P2P loads), and stores U and W = 1/U into every
+ * rank's buffers (P2P stores; U only into its own unless u_all). After a
+ * second barrier every rank holds the full W (and U if u_all). Replaces
+ * the SUM all-reduce of the counts + focus_finish. U peers come from
+ * export_u / attach_peers_u (after attach_peers). */
+int pald_gpu_plan_export_u(const pald_gpu_plan* plan, pald_gpu_ipc_handle* u);
+int pald_gpu_plan_attach_peers_u(pald_gpu_plan* plan, const pald_gpu_ipc_handle* u_handles);
+int pald_gpu_plan_focus_finish_peers(pald_gpu_plan* plan, uint64_t part, uint64_t parts, int u_all,
+                                     void* stream);
+
 /* Number of pass-1 work units of the plan. */
 uint64_t pald_gpu_focus_units(const pald_gpu_plan* plan);
 
@@ -229,9 +317,15 @@ uint64_t pald_gpu_focus_units(const pald_gpu_plan* plan);
 int pald_gpu_fill_diagonal(const int32_t* dU, uint64_t ldu, uint64_t n, double* diag_out,
                            void* stream);
 /* Euclidean distances of a point cloud (ingest.hpp:303-322): each pair
- * once, sum of squared differences in double in coordinate order (no
- * contraction), sqrt in double, rounded to fp32; diagonal 0. Device
- * pointers; points row-major n x dim doubles. */
+ * once, sum of squared differences in double in coordinate order, each
+ * step sum = fma(diff, diff, sum) -- the reference as built by its own
+ * flags (-O3 -march=native: GCC contracts `sum += diff * diff`; verified
+ * bit-exact against oracle/_ref) -- sqrt in double, rounded to fp32
+ * (to_real<float>); diagonal 0. Duplicate points (a zero distance) are
+ * rejected like the reference: ValidationError "duplicate points x and y
+ * (zero distance)" for the first such pair in (x, y > x) order (this reads
+ * one word back: the call synchronizes `stream`). Device pointers; points
+ * row-major n x dim doubles. */
 int pald_gpu_points_to_distances(const double* dP, uint64_t n, uint64_t dim, float* dD,
                                  uint64_t ldd, void* stream);
 
@@ -253,6 +347,21 @@ int pald_gpu_strong_ties(const float* dC, uint64_t ldc, uint64_t n, const double
                          const double* threshold_in, double* threshold_out, uint64_t capacity,
                          uint32_t* xs, uint32_t* ys, double* strength, uint64_t* count_out,
                          void* stream);
+
+/* nearest_neighbors (analyze.hpp:60-75) of the normalized C on the device:
+ * the k points z != focus with the largest min(c'_fz, c'_zf), strongest
+ * first, equal strengths in ascending z (the reference's stable sort);
+ * written to zs / strength (device arrays of k). ValidationError with the
+ * reference's messages for focus >= n or k >= n. `diag` as above. */
+int pald_gpu_nearest_neighbors(const float* dC, uint64_t ldc, uint64_t n, const double* diag, uint64_t focus,
+                               uint64_t k, uint32_t* zs, double* strength, void* stream);
+
+/* The Python mirror's double CohesionMatrix on the device: normalize
+ * (reference.hpp:223-228: c *= 1/(n-1) in double) in place, and the
+ * sequential (ascending z) double row sums of local_depths
+ * (reference.hpp:231-241). Device pointers. */
+int pald_gpu_normalize_f64(double* dC, uint64_t ldc, uint64_t n, void* stream);
+int pald_gpu_row_sums_f64(const double* dC, uint64_t ldc, uint64_t n, double* out, void* stream);
 
 /* The reference's binary matrix format ("PALD", version 1, width 4 or 8,
  * u64 n, n*n little-endian row-major values; ingest.hpp:214-283).

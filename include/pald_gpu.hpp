@@ -30,6 +30,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -130,12 +131,68 @@ namespace gpu {
 // below take the style / plan as template parameters so the reference's own
 // pald::UpdateStyle / pald::ParallelPlan can be passed unchanged.
 enum class UpdateStyle { Masked, Branchy };
+
+// parallel.hpp:31-34 plus the GPU side of "parallel": the devices one call
+// spans (repeats allowed), the exchange transports of the two passes
+// (pald_gpu_exchange) and the accurate-summation mode (PALD_GPU_FLAG_ACCURATE).
+// A plan WITHOUT a `devices` member (the reference's own ParallelPlan) runs
+// on the devices named by the environment variable PALD_GPU_DEVICES ("all"
+// or a comma list such as "0,1,2,3"), else on the current device. Results
+// do not depend on the device list (U and C bit-identical).
 struct ParallelPlan {
   int workers = 1;
   bool deterministic = false;
+  std::vector<int> devices;
+  int exchange_focus = PALD_GPU_EXCHANGE_AUTO;
+  int exchange_cohesion = PALD_GPU_EXCHANGE_AUTO;
+  bool accurate = false;
 };
 
 namespace detail {
+
+struct RunConfig {
+  std::vector<int> devices;  // empty: the current device
+  int exchange_focus = PALD_GPU_EXCHANGE_AUTO;
+  int exchange_cohesion = PALD_GPU_EXCHANGE_AUTO;
+  bool accurate = false;
+};
+
+inline RunConfig env_config() {
+  RunConfig c;
+  if (const char* e = std::getenv("PALD_GPU_DEVICES")) {
+    const std::string s(e);
+    if (s == "all") {
+      for (int i = 0; i < pald_gpu_visible_devices() && i < PALD_GPU_MAX_DEVICES; ++i) c.devices.push_back(i);
+    } else {
+      std::size_t pos = 0;
+      while (pos < s.size()) {
+        const std::size_t q = s.find(',', pos);
+        const std::string tok = s.substr(pos, q == std::string::npos ? std::string::npos : q - pos);
+        if (!tok.empty()) c.devices.push_back(std::stoi(tok));
+        if (q == std::string::npos) break;
+        pos = q + 1;
+      }
+    }
+  }
+  if (const char* a = std::getenv("PALD_GPU_ACCURATE")) c.accurate = std::string(a) == "1";
+  return c;
+}
+
+// The plan's own device list where it has one (SFINAE), else the environment.
+template <class Plan>
+auto plan_config(const Plan& p, int) -> decltype(p.devices, p.exchange_focus, p.exchange_cohesion, p.accurate,
+                                                 RunConfig()) {
+  RunConfig c = env_config();
+  if (!p.devices.empty()) c.devices.assign(p.devices.begin(), p.devices.end());
+  c.exchange_focus = p.exchange_focus;
+  c.exchange_cohesion = p.exchange_cohesion;
+  c.accurate = c.accurate || p.accurate;
+  return c;
+}
+template <class Plan>
+RunConfig plan_config(const Plan&, long) {
+  return env_config();
+}
 
 inline void throw_status(int rc) {
   if (rc == PALD_GPU_OK) return;
@@ -146,8 +203,13 @@ inline void throw_status(int rc) {
   throw std::runtime_error("pald_gpu: " + msg);
 }
 
+// One C-ABI call with the reference's double I/O: D converted like
+// to_real<float> (blocked.hpp:91-96) and C widened like collect_result
+// (blocked.hpp:352-359), both on all host cores inside the library
+// (pald_gpu_cohesion_f64io_*). The result vectors are built (zero-filled,
+// as the reference's types do) while the GPU works.
 inline PaldResult run(const DistanceMatrix& d, int algorithm, Policy policy, std::size_t b,
-                      std::size_t bf, std::size_t bc, PhaseTimes* times) {
+                      std::size_t bf, std::size_t bc, PhaseTimes* times, const RunConfig& cfg = env_config()) {
   pald_gpu_opts o;
   pald_gpu_opts_init(&o);
   o.algorithm = algorithm;
@@ -156,14 +218,29 @@ inline PaldResult run(const DistanceMatrix& d, int algorithm, Policy policy, std
   o.block_focus = bf;
   o.block_cohesion = bc;
   o.flags = PALD_GPU_FLAG_SKIP_VALIDATION;  // DistanceMatrix is validated in double
+  if (cfg.accurate) o.flags |= PALD_GPU_FLAG_ACCURATE;
+  if (cfg.devices.size() > PALD_GPU_MAX_DEVICES)
+    throw ValidationError("at most " + std::to_string(PALD_GPU_MAX_DEVICES) + " devices per call");
+  if (cfg.devices.size() == 1) o.device = cfg.devices[0];
+  if (cfg.devices.size() > 1) {
+    o.num_devices = static_cast<int32_t>(cfg.devices.size());
+    for (std::size_t i = 0; i < cfg.devices.size(); ++i) o.devices[i] = cfg.devices[i];
+  }
+  o.exchange_focus = cfg.exchange_focus;
+  o.exchange_cohesion = cfg.exchange_cohesion;
   const std::size_t n = d.size();
-  std::vector<float> dd(n * n);  // to_real<float>, blocked.hpp:91-96
-  for (std::size_t i = 0; i < dd.size(); ++i) dd[i] = static_cast<float>(d.values()[i]);
+  pald_gpu_job* job = nullptr;
+  throw_status(pald_gpu_cohesion_f64io_begin(d.values().data(), n, &o, &job));
+  struct Join {  // end() must run even if building the result throws
+    pald_gpu_job* j;
+    ~Join() {
+      if (j) pald_gpu_cohesion_f64io_end(j, nullptr, nullptr, nullptr);
+    }
+  } join{job};
   PaldResult r{FocusSizeMatrix(n), CohesionMatrix(n)};
-  std::vector<float> c(n * n);
   pald_gpu_phase_times t{};
-  throw_status(pald_gpu_cohesion_f32(dd.data(), n, &o, r.focus.sizes.data(), c.data(), &t));
-  for (std::size_t i = 0; i < c.size(); ++i) r.cohesion.values[i] = static_cast<double>(c[i]);
+  join.j = nullptr;
+  throw_status(pald_gpu_cohesion_f64io_end(job, r.focus.sizes.data(), r.cohesion.values.data(), &t));
   if (times) {
     times->focus_seconds += t.focus_seconds;
     times->cohesion_seconds += t.cohesion_seconds;
@@ -204,13 +281,18 @@ PaldResult blocked_triplet(const DistanceMatrix& d, std::size_t b_focus, std::si
   return detail::run(d, PALD_GPU_TRIPLET, policy, 128, b_focus, b_cohesion, times);
 }
 
-// parallel.hpp:159-222
+// parallel.hpp:159-222. The plan's devices (or PALD_GPU_DEVICES) split the
+// work of ONE call across GPUs (pald_gpu_opts.devices); bit-identical to
+// blocked_pairwise, as in the reference (test_parallel.cpp:61-76).
 template <class Real = float, class Plan = ParallelPlan, class Style = UpdateStyle>
 PaldResult parallel_pairwise(const DistanceMatrix& d, std::size_t b, const Plan& plan,
                              Policy policy = Policy::Strict, PhaseTimes* times = nullptr,
                              Style style = Style{}) {
+  (void)style;
+  detail::check_real<Real>();
   if (plan.workers < 1) throw ValidationError("worker count must be >= 1");
-  return blocked_pairwise<Real>(d, b, policy, times, style);
+  if (b < 1) throw ValidationError("pairwise block size must be >= 1");
+  return detail::run(d, PALD_GPU_PAIRWISE, policy, b, 128, 128, times, detail::plan_config(plan, 0));
 }
 
 // parallel.hpp:257-320
@@ -218,10 +300,13 @@ template <class Real = float, class Plan = ParallelPlan, class Style = UpdateSty
 PaldResult parallel_triplet(const DistanceMatrix& d, std::size_t b_focus, std::size_t b_cohesion,
                             const Plan& plan, Policy policy = Policy::Strict,
                             PhaseTimes* times = nullptr, Style style = Style{}) {
+  (void)style;
+  detail::check_real<Real>();
   if (policy != Policy::Strict)
     throw UnsupportedPolicyError("the triplet algorithm supports the strict policy only");
   if (plan.workers < 1) throw ValidationError("worker count must be >= 1");
-  return blocked_triplet<Real>(d, b_focus, b_cohesion, policy, times, style);
+  if (b_focus < 1 || b_cohesion < 1) throw ValidationError("triplet block sizes must be >= 1");
+  return detail::run(d, PALD_GPU_TRIPLET, policy, 128, b_focus, b_cohesion, times, detail::plan_config(plan, 0));
 }
 
 }  // namespace gpu

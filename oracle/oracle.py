@@ -57,6 +57,7 @@ class Oracle:
             "pald_oracle_row_sums_f32": (None, [_vp, _u64, _vp]),
             "pald_oracle_triplet_rows_f64": (None, [_vp, _u64, _vp, _u64, _vp, _vp]),
             "pald_oracle_pairwise_rows_f64": (None, [_vp, _u64, _vp, _u64, _vp, _vp]),
+            "pald_oracle_points_to_distances": (C.c_longlong, [_vp, _u64, _u64, _i32, _vp]),
         }
         for k, (r, a) in sigs.items():
             f = getattr(lib, k)
@@ -135,6 +136,14 @@ class Oracle:
         self.lib.pald_oracle_triplet_rows_f64(_ptr(d), n, _ptr(rows), rows.size, _ptr(u), _ptr(c))
         return u, c
 
+    def points_to_distances(self, pts: np.ndarray, fused: bool = True):
+        """(fp32 D, first duplicate pair or None): ingest.hpp:303-322 as built."""
+        pts = np.ascontiguousarray(pts, np.float64)
+        n, dim = pts.shape
+        out = np.empty((n, n), np.float32)
+        k = self.lib.pald_oracle_points_to_distances(_ptr(pts), n, dim, int(fused), _ptr(out))
+        return out, (None if k < 0 else divmod(int(k), n))
+
     def pairwise_f64(self, d: np.ndarray):
         d = np.ascontiguousarray(d, np.float32)
         n = d.shape[0]
@@ -192,6 +201,14 @@ class Reference:
             "ref_default_block_config": (_i32, [_u64, _u64, _vp]),
             "ref_parallel_pairwise_prefix_f32": (_i32, [_vp, _u64, _u64, _i32, _u64, d, _vp, _vp]),
             "ref_read_distance_binary": (_i32, [C.c_char_p, _u64, C.POINTER(C.c_uint64), _vp]),
+            "ref_parallel_pairwise_blocks_f32": (_i32, [_vp, _u64, _u64, _i32, _u64, _u64, _u64, d,
+                                                        C.POINTER(C.c_uint64)]),
+            "ref_points_to_distances": (_i32, [_vp, _u64, _u64, _vp]),
+            "ref_parallel_pairwise_blockpairs_f32": (_i32, [_vp, _u64, _u64, _i32, _vp, _vp, _u64, _vp]),
+            "ref_pairwise_overhead_f32": (_i32, [_u64, _u64, d]),
+            "ref_universal_threshold": (_i32, [_vp, _u64, d]),
+            "ref_strong_ties": (_i32, [_vp, _u64, _vp, d, _u64, _vp, _vp, _vp, C.POINTER(C.c_uint64)]),
+            "ref_nearest_neighbors": (_i32, [_vp, _u64, _u64, _u64, _vp, _vp]),
         }
         for k, (r, a) in sigs.items():
             f = getattr(lib, k)
@@ -263,6 +280,13 @@ class Reference:
     def fill_diagonal(self, u, c):
         self._check(self.lib.ref_fill_diagonal(_ptr(np.ascontiguousarray(u, np.int32)), u.shape[0], _ptr(c)))
 
+    def normalize_and_depths(self, c: np.ndarray):
+        """reference.hpp:223-241 on a copy of c: (normalized C, local depths)."""
+        c = np.array(c, np.float64, order="C", copy=True)
+        depths = np.empty(c.shape[0])
+        self._check(self.lib.ref_normalize_and_depths(_ptr(c), c.shape[0], _ptr(depths)))
+        return c, depths
+
     def read_distance_binary(self, path, cap=4096):
         """(status, message, D) of the reference's read_distance_binary."""
         n = C.c_uint64(0)
@@ -290,6 +314,74 @@ class Reference:
             _ptr(d32), n, b, workers, x_limit, C.byref(secs),
             _ptr(u) if want_outputs else None, _ptr(c) if want_outputs else None))
         return secs.value, u, c
+
+
+    def parallel_pairwise_blocks_f32(self, d32: np.ndarray, b: int, workers: int, xb: int, yb0: int,
+                                     yb1: int):
+        """Timed bounded sample of parallel_pairwise<float> by whole block pairs
+        (x-block xb, y-blocks [yb0, yb1)): returns (seconds, pairs covered)."""
+        d32 = np.ascontiguousarray(d32, np.float32)
+        secs, pairs = C.c_double(0.0), C.c_uint64(0)
+        self._check(self.lib.ref_parallel_pairwise_blocks_f32(_ptr(d32), d32.shape[0], b, workers, xb, yb0,
+                                                             yb1, C.byref(secs), C.byref(pairs)))
+        return secs.value, int(pairs.value)
+
+    def parallel_pairwise_blockpairs_f32(self, d32: np.ndarray, b: int, workers: int, pairs) -> np.ndarray:
+        """Seconds of each listed block pair (xb, yb) of the parallel_pairwise<float>
+        driver loop (ref_bridge.cpp ref_parallel_pairwise_blockpairs_f32)."""
+        d32 = np.ascontiguousarray(d32, np.float32)
+        pairs = np.asarray(pairs, np.uint32).reshape(-1, 2)
+        xb, yb = np.ascontiguousarray(pairs[:, 0]), np.ascontiguousarray(pairs[:, 1])
+        out = np.zeros(len(pairs))
+        self._check(self.lib.ref_parallel_pairwise_blockpairs_f32(_ptr(d32), d32.shape[0], b, workers, _ptr(xb),
+                                                                 _ptr(yb), len(pairs), _ptr(out)))
+        return out
+
+    def pairwise_overhead_f32(self, n: int, seed: int = 1) -> float:
+        """Seconds of the O(n^2) part of a parallel_pairwise<float> call at size n."""
+        out = C.c_double(0.0)
+        self._check(self.lib.ref_pairwise_overhead_f32(n, seed, C.byref(out)))
+        return out.value
+
+    def points_to_distances(self, pts: np.ndarray):
+        """(status, message, D double) of ingest.hpp:303-322."""
+        pts = np.ascontiguousarray(pts, np.float64)
+        n, dim = pts.shape
+        out = np.empty((n, n), np.float64)
+        rc = self.lib.ref_points_to_distances(_ptr(pts), n, dim, _ptr(out))
+        if rc:
+            return rc, self.lib.ref_last_error().decode(), None
+        return 0, "", out
+
+    def universal_threshold(self, c_norm: np.ndarray) -> float:
+        c_norm = np.ascontiguousarray(c_norm, np.float64)
+        out = C.c_double(0.0)
+        self._check(self.lib.ref_universal_threshold(_ptr(c_norm), c_norm.shape[0], C.byref(out)))
+        return out.value
+
+    def strong_ties(self, c_norm: np.ndarray, threshold: float | None = None):
+        """(threshold, xs, ys, strength) of analyze.hpp:42-53."""
+        c_norm = np.ascontiguousarray(c_norm, np.float64)
+        n = c_norm.shape[0]
+        thr_in = np.array([threshold if threshold is not None else 0.0])
+        thr, cnt = C.c_double(0.0), C.c_uint64(0)
+        tp = _ptr(thr_in) if threshold is not None else None
+        self._check(self.lib.ref_strong_ties(_ptr(c_norm), n, tp, C.byref(thr), 0, None, None, None,
+                                             C.byref(cnt)))
+        m = int(cnt.value)
+        xs, ys, sv = np.empty(m, np.uint64), np.empty(m, np.uint64), np.empty(m, np.float64)
+        self._check(self.lib.ref_strong_ties(_ptr(c_norm), n, tp, C.byref(thr), m, _ptr(xs), _ptr(ys),
+                                             _ptr(sv), C.byref(cnt)))
+        return thr.value, xs, ys, sv
+
+    def nearest_neighbors(self, c_norm: np.ndarray, focus: int, k: int):
+        """(status, message, zs, strength) of analyze.hpp:60-75."""
+        c_norm = np.ascontiguousarray(c_norm, np.float64)
+        zs, sv = np.empty(max(k, 1), np.uint64), np.empty(max(k, 1), np.float64)
+        rc = self.lib.ref_nearest_neighbors(_ptr(c_norm), c_norm.shape[0], focus, k, _ptr(zs), _ptr(sv))
+        if rc:
+            return rc, self.lib.ref_last_error().decode(), None, None
+        return 0, "", zs[:k], sv[:k]
 
 
 def pair_work_fraction(n: int, x_limit: int) -> float:

@@ -397,3 +397,27 @@ void pald_oracle_triplet_rows_f64(const float* d, uint64_t n, const int64_t* row
     }
   }
 }
+
+/* points_to_distances, ingest.hpp:303-322, as the reference's own build
+ * computes it: -O3 -march=native contracts `sum += diff * diff` into
+ * sum = fma(diff, diff, sum) (fused = 1; fused = 0 keeps the separate
+ * rounding of the product). Distances in double, written as fp32
+ * (to_real<float>, blocked.hpp:91-96). Returns the row-major key x * n + y
+ * of the first duplicate pair (zero distance), or -1. */
+long long pald_oracle_points_to_distances(const double* p, uint64_t n, uint64_t dim, int fused, float* out) {
+  long long dup = -1;
+  for (uint64_t x = 0; x < n; ++x) {
+    out[x * n + x] = 0.0f;
+    for (uint64_t y = x + 1; y < n; ++y) {
+      double sum = 0.0;
+      for (uint64_t k = 0; k < dim; ++k) {
+        const double diff = p[x * dim + k] - p[y * dim + k];
+        sum = fused ? fma(diff, diff, sum) : sum + diff * diff;
+      }
+      const double dist = sqrt(sum);
+      if (dist == 0.0 && dup < 0) dup = (long long)(x * n + y);
+      out[x * n + y] = out[y * n + x] = (float)dist;
+    }
+  }
+  return dup;
+}

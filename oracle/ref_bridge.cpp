@@ -253,4 +253,172 @@ int ref_parallel_pairwise_prefix_f32(const float* dd, uint64_t n, uint64_t b, in
   });
 }
 
+// Bounded timing sample of parallel_pairwise<float> by whole BLOCK PAIRS:
+// the body of the driver loop of parallel.hpp:178-215 for x-block `xb` and
+// y-blocks [yb0, yb1) (yb0 >= xb), with the reference's own ThreadPool,
+// worker_range, pair_block_focus and pair_block_cohesion at their real
+// block size b. Full off-diagonal blocks (yb0 > xb) cost what every other
+// full block of the run costs, so the caller extrapolates by the pair count
+// (pairs in the sample / n(n-1)/2). *pairs_out = pairs covered.
+int ref_parallel_pairwise_blocks_f32(const float* dd, uint64_t n, uint64_t b, int workers, uint64_t xb,
+                                     uint64_t yb0, uint64_t yb1, double* seconds, uint64_t* pairs_out) {
+  return guarded([&] {
+    using pald::detail::worker_range;
+    const int p = workers;
+    std::vector<float> c(n * n, 0.0f);
+    std::vector<int32_t> u(n * n, 0);
+    std::vector<std::vector<int32_t>> partial(p, std::vector<int32_t>(b * b));
+    std::vector<float> recip(b * b);
+    pald::ThreadPool pool(p);
+    uint64_t pairs = 0;
+    const uint64_t x0 = xb * b, x1 = std::min<uint64_t>(x0 + b, n);
+    const double t0 = pald::detail::PhaseClock::now();
+    for (uint64_t y0 = std::max(yb0, xb) * b; y0 < n && y0 < yb1 * b; y0 += b) {
+      const uint64_t y1 = std::min<uint64_t>(y0 + b, n);
+      const uint64_t ys = y1 - y0, cells = (x1 - x0) * ys;
+      pool.run([&](int w) {
+        auto [z0, z1] = worker_range(n, p, w);
+        std::fill(partial[w].begin(), partial[w].begin() + cells, 0);
+        pald::detail::pair_block_focus(dd, n, pald::Policy::Strict, x0, x1, y0, y1, z0, z1, partial[w].data());
+      });
+      for (int w = 1; w < p; ++w)
+        for (uint64_t i = 0; i < cells; ++i) partial[0][i] += partial[w][i];
+      for (uint64_t x = x0; x < x1; ++x) {
+        const uint64_t ybeg = (y0 > x + 1) ? y0 : x + 1;
+        for (uint64_t y = ybeg; y < y1; ++y) {
+          const int32_t cnt = partial[0][(x - x0) * ys + (y - y0)];
+          u[x * n + y] = u[y * n + x] = cnt;
+          recip[(x - x0) * ys + (y - y0)] = 1.0f / static_cast<float>(cnt);
+          ++pairs;
+        }
+      }
+      pool.run([&](int w) {
+        auto [z0, z1] = worker_range(n, p, w);
+        pald::detail::pair_block_cohesion(dd, n, pald::Policy::Strict, pald::UpdateStyle::Masked, x0, x1, y0,
+                                          y1, z0, z1, recip.data(), c.data());
+      });
+    }
+    *seconds = pald::detail::PhaseClock::now() - t0;
+    *pairs_out = pairs;
+  });
+}
+
+// Timing sample of parallel_pairwise<float> by an explicit list of block
+// pairs (xb[i], yb[i]), xb <= yb: each is the body of the driver loop of
+// parallel.hpp:178-215 (pair_block_focus over the workers' z ranges, the
+// rank-order sum of the partial counts, U and the reciprocals, then
+// pair_block_cohesion), timed on its own into seconds[i]. The caller
+// extrapolates diagonal and off-diagonal block pairs separately.
+int ref_parallel_pairwise_blockpairs_f32(const float* dd, uint64_t n, uint64_t b, int workers, const uint32_t* xb,
+                                         const uint32_t* yb, uint64_t count, double* seconds) {
+  return guarded([&] {
+    using pald::detail::worker_range;
+    const int p = workers;
+    std::vector<float> c(n * n, 0.0f);
+    std::vector<int32_t> u(n * n, 0);
+    std::vector<std::vector<int32_t>> partial(p, std::vector<int32_t>(b * b));
+    std::vector<float> recip(b * b);
+    pald::ThreadPool pool(p);
+    for (uint64_t i = 0; i < count; ++i) {
+      const uint64_t x0 = (uint64_t)xb[i] * b, y0 = (uint64_t)yb[i] * b;
+      const uint64_t x1 = std::min<uint64_t>(x0 + b, n), y1 = std::min<uint64_t>(y0 + b, n);
+      const uint64_t ys = y1 - y0, cells = (x1 - x0) * ys;
+      const double t0 = pald::detail::PhaseClock::now();
+      pool.run([&](int w) {
+        auto [z0, z1] = worker_range(n, p, w);
+        std::fill(partial[w].begin(), partial[w].begin() + cells, 0);
+        pald::detail::pair_block_focus(dd, n, pald::Policy::Strict, x0, x1, y0, y1, z0, z1, partial[w].data());
+      });
+      for (int w = 1; w < p; ++w)
+        for (uint64_t k = 0; k < cells; ++k) partial[0][k] += partial[w][k];
+      for (uint64_t x = x0; x < x1; ++x) {
+        const uint64_t ybeg = (y0 > x + 1) ? y0 : x + 1;
+        for (uint64_t y = ybeg; y < y1; ++y) {
+          const int32_t cnt = partial[0][(x - x0) * ys + (y - y0)];
+          u[x * n + y] = u[y * n + x] = cnt;
+          recip[(x - x0) * ys + (y - y0)] = 1.0f / static_cast<float>(cnt);
+        }
+      }
+      pool.run([&](int w) {
+        auto [z0, z1] = worker_range(n, p, w);
+        pald::detail::pair_block_cohesion(dd, n, pald::Policy::Strict, pald::UpdateStyle::Masked, x0, x1, y0,
+                                          y1, z0, z1, recip.data(), c.data());
+      });
+      seconds[i] = pald::detail::PhaseClock::now() - t0;
+    }
+  });
+}
+
+// The O(n^2) part of a parallel_pairwise<float> call (parallel.hpp:167-175,
+// :216-219) on a random D of size n: to_real<float>, the zero-filled C / U
+// buffers, and collect_result. *seconds = their total.
+int ref_pairwise_overhead_f32(uint64_t n, uint64_t seed, double* seconds) {
+  return guarded([&] {
+    const auto d = pald::detail::random_distances(n, seed);
+    const double t0 = pald::detail::PhaseClock::now();
+    const std::vector<float> dd = pald::detail::to_real<float>(d);
+    std::vector<float> c(n * n, 0.0f);
+    std::vector<int32_t> u(n * n, 0);
+    pald::PaldResult r = pald::detail::collect_result(n, std::move(u), c);
+    *seconds = pald::detail::PhaseClock::now() - t0;
+    if (r.focus.sizes.size() != n * n || dd.size() != n * n) throw std::runtime_error("size");
+  });
+}
+
+// points_to_distances, ingest.hpp:303-322 (row-major n x dim doubles in,
+// n x n doubles out; duplicate points -> ValidationError, status 2)
+int ref_points_to_distances(const double* pts, uint64_t n, uint64_t dim, double* out) {
+  return guarded([&] {
+    pald::PointCloud pc;
+    pc.n = n;
+    pc.dim = dim;
+    pc.coords.assign(pts, pts + n * dim);
+    const auto d = pald::points_to_distances(pc);
+    std::memcpy(out, d.values().data(), sizeof(double) * n * n);
+  });
+}
+
+namespace {
+pald::CohesionMatrix normalized_c(const double* c, uint64_t n) {
+  pald::CohesionMatrix cm(n);
+  std::memcpy(cm.values.data(), c, sizeof(double) * n * n);
+  cm.normalized = true;
+  return cm;
+}
+}  // namespace
+
+// universal_threshold, analyze.hpp:34-40 (c: a normalized C)
+int ref_universal_threshold(const double* c, uint64_t n, double* out) {
+  return guarded([&] { *out = pald::universal_threshold(normalized_c(c, n)); });
+}
+
+// strong_ties, analyze.hpp:42-53. threshold_in NULL = universal threshold.
+// Writes up to cap edges; *count_out = the edge count.
+int ref_strong_ties(const double* c, uint64_t n, const double* threshold_in, double* threshold_out,
+                    uint64_t cap, uint64_t* xs, uint64_t* ys, double* strength, uint64_t* count_out) {
+  return guarded([&] {
+    const auto cm = normalized_c(c, n);
+    const auto g = threshold_in ? pald::strong_ties(cm, *threshold_in) : pald::strong_ties(cm);
+    *threshold_out = g.threshold;
+    *count_out = g.edges.size();
+    for (uint64_t i = 0; i < g.edges.size() && i < cap; ++i) {
+      xs[i] = g.edges[i].x;
+      ys[i] = g.edges[i].y;
+      strength[i] = g.edges[i].strength;
+    }
+  });
+}
+
+// nearest_neighbors, analyze.hpp:60-75
+int ref_nearest_neighbors(const double* c, uint64_t n, uint64_t focus, uint64_t k, uint64_t* zs,
+                          double* strength) {
+  return guarded([&] {
+    const auto nb = pald::nearest_neighbors(normalized_c(c, n), focus, k);
+    for (uint64_t i = 0; i < nb.size(); ++i) {
+      zs[i] = nb[i].z;
+      strength[i] = nb[i].strength;
+    }
+  });
+}
+
 }  // extern "C"

@@ -17,7 +17,7 @@ LIB_DIR = PKG_DIR / "lib"
 LIB_PATH = LIB_DIR / "libpald_gpu.so"
 INCLUDE = PKG_DIR.parent / "include"
 
-SOURCES = [CSRC / "pald_gpu.cu", CSRC / "pald_epilogue.cu", CSRC / "pald_io.cu"]
+SOURCES = [CSRC / "pald_gpu.cu", CSRC / "pald_epilogue.cu", CSRC / "pald_io.cu", CSRC / "pald_hostio.cu"]
 def deps() -> list[Path]:
     """Every file the library is built from (sources, kernel headers, ABI)."""
     return sorted([*CSRC.glob("*.cu"), *CSRC.glob("*.cuh"), *CSRC.glob("*.h"), *INCLUDE.glob("*.h")])
@@ -25,7 +25,7 @@ def deps() -> list[Path]:
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC", "-shared", "-Xlinker", "-soname=libpald_gpu.so",
     "-Xptxas", "-v",
 ]
 

@@ -14,6 +14,10 @@ PAIRWISE, TRIPLET = 0, 1
 STRICT, INCLUSIVE_SPLIT = 0, 1
 FLAG_SKIP_VALIDATION = 1
 FLAG_FORCE_EXACT = 2
+FLAG_ACCURATE = 4
+MAX_DEVICES = 8
+EXCHANGE_AUTO, EXCHANGE_PEER, EXCHANGE_NCCL, EXCHANGE_RED = 0, 1, 2, 3
+OPTS_V3_SIZE = 48
 
 OK, ERR_VALIDATION, ERR_UNSUPPORTED, ERR_IO, ERR_CUDA, ERR_COMM = 0, 2, 3, 4, 5, 6
 
@@ -22,6 +26,7 @@ EXPORTED_SYMBOLS = (
     "pald_gpu_opts_init",
     "pald_gpu_last_error",
     "pald_gpu_abi_version",
+    "pald_gpu_visible_devices",
     "pald_gpu_cohesion_f32",
     "pald_gpu_cohesion_f32_device",
     "pald_gpu_plan_create",
@@ -41,11 +46,21 @@ EXPORTED_SYMBOLS = (
     "pald_gpu_plan_detach_peers",
     "pald_gpu_plan_focus_counts_peers",
     "pald_gpu_plan_cohesion_share_peers",
+    "pald_gpu_cohesion_f64io_begin",
+    "pald_gpu_cohesion_f64io_end",
+    "pald_gpu_cohesion_f64io",
+    "pald_gpu_release_host_staging",
+    "pald_gpu_plan_export_u",
+    "pald_gpu_plan_attach_peers_u",
+    "pald_gpu_plan_focus_finish_peers",
     "pald_gpu_focus_units",
     "pald_gpu_fill_diagonal",
     "pald_gpu_points_to_distances",
     "pald_gpu_local_depths",
     "pald_gpu_strong_ties",
+    "pald_gpu_nearest_neighbors",
+    "pald_gpu_normalize_f64",
+    "pald_gpu_row_sums_f64",
     "pald_gpu_read_binary_header",
     "pald_gpu_read_distance_binary",
 )
@@ -62,6 +77,10 @@ class Opts(C.Structure):
         ("block_cohesion", C.c_uint64),
         ("flags", C.c_uint32),
         ("reserved", C.c_uint32),
+        ("num_devices", C.c_int32),
+        ("devices", C.c_int32 * 8),
+        ("exchange_focus", C.c_int32),
+        ("exchange_cohesion", C.c_int32),
     ]
 
 
@@ -85,6 +104,7 @@ class Buffers(C.Structure):
         ("tiles_per_dim", C.c_uint64),
         ("exact_path", C.c_int32),
         ("reserved", C.c_int32),
+        ("C64", C.c_void_p),
     ]
 
 
@@ -97,6 +117,7 @@ class PlanInfo(C.Structure):
         ("exact_step_share", C.c_double),
         ("launches", C.c_uint64),
         ("rank_codes", C.c_int32),
+        ("pair_kernel_preferred", C.c_int32),
     ]
 
 
@@ -134,6 +155,7 @@ def load(path: Path | None = None) -> C.CDLL:
         "pald_gpu_opts_init": (None, [C.POINTER(Opts)]),
         "pald_gpu_last_error": (C.c_char_p, []),
         "pald_gpu_abi_version": (i32, []),
+        "pald_gpu_visible_devices": (i32, []),
         "pald_gpu_cohesion_f32": (i32, [vp, u64, C.POINTER(Opts), vp, vp, C.POINTER(PhaseTimes)]),
         "pald_gpu_cohesion_f32_device": (i32, [vp, u64, u64, C.POINTER(Opts), vp, u64, vp, u64, vp]),
         "pald_gpu_plan_create": (i32, [u64, C.POINTER(Opts), C.POINTER(vp)]),
@@ -151,6 +173,13 @@ def load(path: Path | None = None) -> C.CDLL:
         "pald_gpu_plan_detach_peers": (i32, [vp]),
         "pald_gpu_plan_focus_counts_peers": (i32, [vp, u64, u64, vp]),
         "pald_gpu_plan_cohesion_share_peers": (i32, [vp, u64, u64, vp]),
+        "pald_gpu_cohesion_f64io_begin": (i32, [vp, u64, C.POINTER(Opts), C.POINTER(vp)]),
+        "pald_gpu_cohesion_f64io_end": (i32, [vp, vp, vp, C.POINTER(PhaseTimes)]),
+        "pald_gpu_cohesion_f64io": (i32, [vp, u64, C.POINTER(Opts), vp, vp, C.POINTER(PhaseTimes)]),
+        "pald_gpu_release_host_staging": (i32, []),
+        "pald_gpu_plan_export_u": (i32, [vp, C.POINTER(IpcHandle)]),
+        "pald_gpu_plan_attach_peers_u": (i32, [vp, C.POINTER(IpcHandle)]),
+        "pald_gpu_plan_focus_finish_peers": (i32, [vp, u64, u64, i32, vp]),
         "pald_gpu_plan_buffers": (i32, [vp, C.POINTER(Buffers)]),
         "pald_gpu_plan_launches": (u64, [vp]),
         "pald_gpu_focus_units": (u64, [vp]),
@@ -158,6 +187,9 @@ def load(path: Path | None = None) -> C.CDLL:
         "pald_gpu_points_to_distances": (i32, [vp, u64, u64, vp, u64, vp]),
         "pald_gpu_local_depths": (i32, [vp, u64, u64, vp, vp, vp]),
         "pald_gpu_strong_ties": (i32, [vp, u64, u64, vp, vp, vp, u64, vp, vp, vp, vp, vp]),
+        "pald_gpu_nearest_neighbors": (i32, [vp, u64, u64, vp, u64, u64, vp, vp, vp]),
+        "pald_gpu_normalize_f64": (i32, [vp, u64, u64, vp]),
+        "pald_gpu_row_sums_f64": (i32, [vp, u64, u64, vp, vp]),
         "pald_gpu_read_binary_header": (i32, [C.c_char_p, C.POINTER(u64), C.POINTER(C.c_int32)]),
         "pald_gpu_read_distance_binary": (i32, [C.c_char_p, vp, u64, vp]),
     }
@@ -177,9 +209,21 @@ def last_error() -> str:
 
 
 def make_opts(algorithm: int = PAIRWISE, policy: int = STRICT, device: int = -1, block: int = 128,
-              block_focus: int = 128, block_cohesion: int = 128, flags: int = 0) -> Opts:
+              block_focus: int = 128, block_cohesion: int = 128, flags: int = 0,
+              devices=None, exchange_focus: int = EXCHANGE_AUTO,
+              exchange_cohesion: int = EXCHANGE_AUTO) -> Opts:
+    """pald_gpu_opts; ``devices`` (a list of ordinals, repeats allowed) runs
+    one call across several GPUs (include/pald_gpu.h, ABI v4)."""
     o = Opts()
     load().pald_gpu_opts_init(C.byref(o))
     o.algorithm, o.policy, o.device = algorithm, policy, device
     o.block, o.block_focus, o.block_cohesion, o.flags = block, block_focus, block_cohesion, flags
+    if devices is not None:
+        devices = list(devices)
+        if len(devices) > MAX_DEVICES:
+            raise ValueError(f"at most {MAX_DEVICES} devices")
+        o.num_devices = len(devices)
+        for i, d in enumerate(devices):
+            o.devices[i] = int(d)
+    o.exchange_focus, o.exchange_cohesion = exchange_focus, exchange_cohesion
     return o

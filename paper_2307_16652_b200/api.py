@@ -101,6 +101,15 @@ def _raise_for(code: int) -> None:
     raise GpuError(f"status {code}: {msg}")
 
 
+def _cpp_to_string(v: float) -> str:
+    """std::to_string(double): printf("%f") (types.hpp:57 formats the value so)."""
+    if np.isnan(v):
+        return "-nan" if np.signbit(v) else "nan"
+    if np.isinf(v):
+        return "-inf" if v < 0 else "inf"
+    return "%f" % v
+
+
 class DistanceMatrix:
     """Dense symmetric n x n distance matrix, validated as types.hpp:45-65:
     n >= 2, n*n values, zero diagonal, off-diagonal > 0 (rejects 0 and NaN),
@@ -114,22 +123,27 @@ class DistanceMatrix:
         if v.size != n * n:
             raise ValidationError("distance matrix storage size does not match n*n")
         v = v.reshape(n, n)
-        diag = np.diagonal(v)
-        bad = np.nonzero(diag != 0.0)[0]
-        if bad.size:
-            x = int(bad[0])
-            raise ValidationError(f"distance matrix diagonal entry ({x},{x}) is nonzero")
+        # The reference (types.hpp:50-62) scans row by row: (x, x), then
+        # (x, y) for y > x (positivity before symmetry), then row x + 1.
+        # Report the first violation in that order: key = x * n + y.
+        big = n * n
+        bad_diag = np.nonzero(np.diagonal(v) != 0.0)[0]
+        k_diag = int(bad_diag[0]) * (n + 1) if bad_diag.size else big
         iu = np.triu_indices(n, 1)
         upper = v[iu]
         notpos = np.nonzero(~(upper > 0.0))[0]
         asym = np.nonzero(upper != v.T[iu])[0]
-        # the reference scans row-major and reports the first violation
-        first = min(notpos[0] if notpos.size else upper.size, asym[0] if asym.size else upper.size)
-        if first < upper.size:
-            x, y = int(iu[0][first]), int(iu[1][first])
-            if notpos.size and notpos[0] == first:
+        keys = iu[0].astype(np.int64) * n + iu[1]
+        k_np = int(keys[notpos[0]]) if notpos.size else big
+        k_as = int(keys[asym[0]]) if asym.size else big
+        first = min(k_diag, k_np, k_as)
+        if first < big:
+            x, y = divmod(first, n)
+            if first == k_diag:
+                raise ValidationError(f"distance matrix diagonal entry ({x},{x}) is nonzero")
+            if first == k_np:
                 raise ValidationError(
-                    f"off-diagonal distance ({x},{y}) must be positive, got {upper[first]} "
+                    f"off-diagonal distance ({x},{y}) must be positive, got {_cpp_to_string(v[x, y])} "
                     "(duplicate points are rejected)")
             raise ValidationError(f"distance matrix not symmetric at ({x},{y})")
         self._n = n
@@ -280,22 +294,37 @@ def fill_diagonal(u: FocusSizeMatrix, c: CohesionMatrix) -> None:
     c.values[np.arange(n), np.arange(n)] = diag
 
 
+def _device_values(c: CohesionMatrix):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(c.values, np.float64)).cuda()
+
+
 def normalize(c: CohesionMatrix) -> None:
-    """reference.hpp:223-228."""
+    """reference.hpp:223-228: c *= 1/(n-1) in double, on the GPU
+    (pald_gpu_normalize_f64)."""
+    import torch
+
     if c.normalized:
         raise ValidationError("cohesion matrix is already normalized")
-    c.values *= 1.0 / float(c.n - 1)
+    lib = _lib.load()
+    dv = _device_values(c)
+    _raise_for(lib.pald_gpu_normalize_f64(dv.data_ptr(), c.n, c.n,
+                                          torch.cuda.current_stream(dv.device).cuda_stream))
+    c.values = dv.cpu().numpy().reshape(c.n, c.n)
     c.normalized = True
 
 
 def local_depths(c: CohesionMatrix) -> LocalDepthVector:
-    """reference.hpp:231-241 (row sums of a normalized C)."""
+    """reference.hpp:231-241: the ascending-z double row sums of a
+    normalized C, on the GPU (pald_gpu_row_sums_f64, the reference's order)."""
+    import torch
+
     if not c.normalized:
         raise ValidationError("local depths require a normalized cohesion matrix")
-    depths = np.empty(c.n)
-    for x in range(c.n):  # ascending-z double sum, as the reference
-        s = 0.0
-        for v in c.values[x]:
-            s += v
-        depths[x] = s
-    return LocalDepthVector(depths)
+    lib = _lib.load()
+    dv = _device_values(c)
+    out = torch.empty(c.n, dtype=torch.float64, device=dv.device)
+    _raise_for(lib.pald_gpu_row_sums_f64(dv.data_ptr(), c.n, c.n, out.data_ptr(),
+                                         torch.cuda.current_stream(dv.device).cuda_stream))
+    return LocalDepthVector(out.cpu().numpy())

@@ -16,6 +16,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
 #include <cstdio>
 #include <string>
 #include <vector>
@@ -129,6 +132,55 @@ __global__ void exclusive_scan_kernel(const uint32_t* __restrict__ counts, int n
   *total = s;
 }
 
+// Double-matrix epilogue of the Python mirror (its CohesionMatrix holds
+// doubles, like the reference's): normalize in place, sequential row sums.
+__global__ void normalize_f64_kernel(double* __restrict__ c, uint64_t ld, int n, double scale) {
+  for (int r = blockIdx.x; r < n; r += gridDim.x)
+    for (int z = threadIdx.x; z < n; z += blockDim.x) c[(size_t)r * ld + z] = __dmul_rn(c[(size_t)r * ld + z], scale);
+}
+
+__global__ void row_sums_f64_kernel(const double* __restrict__ c, uint64_t ld, int n, double* __restrict__ out) {
+  __shared__ double tile[32][33];
+  const int lane = threadIdx.x, x0 = blockIdx.x * 32, x = x0 + lane;
+  double s = 0.0;
+  for (int z0 = 0; z0 < n; z0 += 32) {
+    for (int r = 0; r < 32; ++r) {
+      const int xr = x0 + r, z = z0 + lane;
+      tile[r][lane] = (xr < n && z < n) ? c[(size_t)xr * ld + z] : 0.0;
+    }
+    __syncwarp();
+    if (x < n) {
+      const int zmax = min(32, n - z0);
+      for (int j = 0; j < zmax; ++j) s = __dadd_rn(s, tile[lane][j]);
+    }
+    __syncwarp();
+  }
+  if (x < n) out[x] = s;
+}
+
+// nearest_neighbors (analyze.hpp:60-75), pass 1: for every z != focus the
+// normalized strength min(c'_fz, c'_zf), as the key of a stable descending
+// radix sort (non-negative doubles order as their bit patterns; equal
+// strengths keep ascending z, the reference's std::stable_sort order).
+__global__ void neighbor_keys_kernel(const float* __restrict__ c, uint64_t ld, int n, const double* __restrict__ diag,
+                                     double scale, int focus, unsigned long long* __restrict__ keys,
+                                     uint32_t* __restrict__ idx) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n - 1; i += gridDim.x * blockDim.x) {
+    const int z = i < focus ? i : i + 1;
+    const double s = fmin(cval(c, ld, focus, z, diag, scale), cval(c, ld, z, focus, diag, scale));
+    keys[i] = (unsigned long long)__double_as_longlong(s);
+    idx[i] = (uint32_t)z;
+  }
+}
+
+__global__ void neighbor_out_kernel(const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ idx,
+                                    int k, uint32_t* __restrict__ zs, double* __restrict__ strength) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x) {
+    zs[i] = idx[i];
+    strength[i] = __longlong_as_double((long long)keys[i]);
+  }
+}
+
 int fail(cudaError_t e, const char* what) {
   return pald_gpu_set_error(PALD_GPU_ERR_CUDA, (std::string(what) + ": " + cudaGetErrorString(e)).c_str());
 }
@@ -179,6 +231,52 @@ int pald_gpu_strong_ties(const float* dC, uint64_t ldc, uint64_t n, const double
   cudaFreeAsync(offsets, s);
   e = cudaGetLastError();
   return e == cudaSuccess ? PALD_GPU_OK : fail(e, "strong ties");
+}
+
+int pald_gpu_normalize_f64(double* dC, uint64_t ldc, uint64_t n, void* stream) {
+  if (!dC || n < 2 || ldc < n) return pald_gpu_set_error(PALD_GPU_ERR_VALIDATION, "normalize: invalid arguments");
+  normalize_f64_kernel<<<(unsigned)std::min<uint64_t>(n, 148 * 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      dC, ldc, (int)n, 1.0 / (double)(n - 1));
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? PALD_GPU_OK : fail(e, "normalize_f64_kernel");
+}
+
+int pald_gpu_row_sums_f64(const double* dC, uint64_t ldc, uint64_t n, double* out, void* stream) {
+  if (!dC || !out || n < 1 || ldc < n) return pald_gpu_set_error(PALD_GPU_ERR_VALIDATION, "row_sums: invalid arguments");
+  row_sums_f64_kernel<<<(unsigned)((n + 31) / 32), 32, 0, static_cast<cudaStream_t>(stream)>>>(dC, ldc, (int)n, out);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? PALD_GPU_OK : fail(e, "row_sums_f64_kernel");
+}
+
+int pald_gpu_nearest_neighbors(const float* dC, uint64_t ldc, uint64_t n, const double* diag, uint64_t focus,
+                               uint64_t k, uint32_t* zs, double* strength, void* stream) {
+  // analyze.hpp:64-65: the reference's checks and messages, in its order
+  if (focus >= n) return pald_gpu_set_error(PALD_GPU_ERR_VALIDATION, "focus point out of range");
+  if (k >= n) return pald_gpu_set_error(PALD_GPU_ERR_VALIDATION, "k must be smaller than the point count");
+  if (!dC || ldc < n || (k && (!zs || !strength)))
+    return pald_gpu_set_error(PALD_GPU_ERR_VALIDATION, "nearest_neighbors: invalid arguments");
+  if (k == 0) return PALD_GPU_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int m = (int)n - 1;
+  unsigned long long *keys = nullptr, *keys_out = nullptr;
+  uint32_t *idx = nullptr, *idx_out = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp_bytes, keys, keys_out, idx, idx_out, m, 0, 64, s);
+  cudaError_t e = cudaMallocAsync(&keys, (size_t)m * 8 * 2 + (size_t)m * 4 * 2 + tmp_bytes, s);
+  if (e != cudaSuccess) return fail(e, "alloc");
+  keys_out = keys + m;
+  idx = reinterpret_cast<uint32_t*>(keys_out + m);
+  idx_out = idx + m;
+  tmp = idx_out + m;
+  neighbor_keys_kernel<<<(unsigned)std::min<int>((m + 255) / 256, 148 * 8), 256, 0, s>>>(
+      dC, ldc, (int)n, diag, 1.0 / (double)(n - 1), (int)focus, keys, idx);
+  // stable: equal strengths keep ascending z
+  cub::DeviceRadixSort::SortPairsDescending(tmp, tmp_bytes, keys, keys_out, idx, idx_out, m, 0, 64, s);
+  neighbor_out_kernel<<<(unsigned)((k + 255) / 256), 256, 0, s>>>(keys_out, idx_out, (int)k, zs, strength);
+  cudaFreeAsync(keys, s);
+  e = cudaGetLastError();
+  return e == cudaSuccess ? PALD_GPU_OK : fail(e, "nearest_neighbors");
 }
 
 }  // extern "C"

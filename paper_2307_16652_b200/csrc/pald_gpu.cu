@@ -7,10 +7,16 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <dlfcn.h>
+
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <thread>
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -61,11 +67,15 @@ struct Stats {
   uint32_t has_inf;
   uint32_t has_nan;
   uint32_t asymmetric;
+  // first violation of each kind in the reference's scan order
+  // (types.hpp:50-62: row by row, (x, x) then (x, y > x)); key = x * n + y
+  unsigned long long key_diag, key_notpos, key_asym;
 };
 
 __global__ void stats_kernel(const float* __restrict__ d, uint64_t ldd, int n, int check_sym,
                              Stats* out, int r_begin, int r_end) {
   uint32_t mn = 0xffffffffu, mx = 0u, flags = 0u;
+  unsigned long long kd = ~0ull, knp = ~0ull, kas = ~0ull;
   // rows [r_begin, r_end); symmetry is checked against the rows above
   // (c < r), so a banded H2D can check each band as it arrives
   for (int r = r_begin + blockIdx.x; r < r_end; r += gridDim.x) {
@@ -74,10 +84,18 @@ __global__ void stats_kernel(const float* __restrict__ d, uint64_t ldd, int n, i
       const float v = row[c];
       const uint32_t bits = __float_as_uint(v);
       if (r == c) {
-        if ((bits & 0x7fffffffu) != 0u) flags |= 1u;
+        if ((bits & 0x7fffffffu) != 0u) {
+          flags |= 1u;
+          kd = min(kd, (unsigned long long)r * n + r);
+        }
         continue;
       }
-      if (!(v > 0.f)) flags |= 2u;
+      if (!(v > 0.f)) {
+        flags |= 2u;
+        // the reference tests positivity on the upper entry (x, y > x); a
+        // bad lower entry shows up there as an asymmetry (below)
+        if (c > r) knp = min(knp, (unsigned long long)r * n + c);
+      }
       if (v == 0.f) flags |= 4u;
       if (isinf(v)) flags |= 8u;
       if (isnan(v)) flags |= 16u;
@@ -87,7 +105,10 @@ __global__ void stats_kernel(const float* __restrict__ d, uint64_t ldd, int n, i
       }
       if (check_sym && c < r) {
         const float t = d[(size_t)c * ldd + r];
-        if (__float_as_uint(t) != bits) flags |= 32u;
+        if (__float_as_uint(t) != bits) {
+          flags |= 32u;
+          kas = min(kas, (unsigned long long)c * n + r);
+        }
       }
     }
   }
@@ -95,8 +116,14 @@ __global__ void stats_kernel(const float* __restrict__ d, uint64_t ldd, int n, i
     mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
     mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     flags |= __shfl_xor_sync(0xffffffffu, flags, o);
+    kd = min(kd, __shfl_xor_sync(0xffffffffu, kd, o));
+    knp = min(knp, __shfl_xor_sync(0xffffffffu, knp, o));
+    kas = min(kas, __shfl_xor_sync(0xffffffffu, kas, o));
   }
   if ((threadIdx.x & 31) == 0) {
+    if (kd != ~0ull) atomicMin(&out->key_diag, kd);
+    if (knp != ~0ull) atomicMin(&out->key_notpos, knp);
+    if (kas != ~0ull) atomicMin(&out->key_asym, kas);
     atomicMin(&out->min_pos_bits, mn);
     atomicMax(&out->max_bits, mx);
     if (flags & 1u) atomicOr(&out->diag_nonzero, 1u);
@@ -136,21 +163,28 @@ __global__ void fill_diagonal_kernel(const int32_t* __restrict__ u, uint64_t ldu
   out[x] = s;
 }
 
+// points_to_distances (ingest.hpp:303-322): each unordered pair evaluated in
+// the same (min, max) order so D is exactly symmetric; sum = fma(diff, diff,
+// sum) in coordinate order, which is the reference's `sum += diff * diff` as
+// its own build compiles it (-O3 -march=native: contracted to an FMA; checked
+// bit-exact against oracle/_ref in tests/test_gpu_analyze.py). A zero
+// distance records the pair's row-major key (the reference throws on the
+// first duplicate pair of its x < y loop).
 __global__ void points_kernel(const double* __restrict__ p, int n, int dim, float* __restrict__ d,
-                              uint64_t ldd) {
+                              uint64_t ldd, unsigned long long* __restrict__ dup_key) {
   for (int r = blockIdx.x; r < n; r += gridDim.x) {
     for (int c = threadIdx.x; c < n; c += blockDim.x) {
       float out = 0.f;
       if (r != c) {
-        // each unordered pair evaluated in the same (min, max) order so D is
-        // exactly symmetric (ingest.hpp:303-322)
         const int a = min(r, c), b = max(r, c);
         double s = 0.0;
         for (int k = 0; k < dim; ++k) {
           const double diff = __dsub_rn(p[(size_t)a * dim + k], p[(size_t)b * dim + k]);
-          s = __dadd_rn(s, __dmul_rn(diff, diff));
+          s = __fma_rn(diff, diff, s);
         }
-        out = __double2float_rn(__dsqrt_rn(s));
+        const double dist = __dsqrt_rn(s);
+        if (dist == 0.0 && r < c) atomicMin(dup_key, (unsigned long long)r * n + c);
+        out = __double2float_rn(dist);
       }
       d[(size_t)r * ldd + c] = out;
     }
@@ -190,10 +224,10 @@ int make_map(CUtensorMap* map, const void* base, uint64_t n, uint64_t ld, int bo
 }
 
 template <int PASS, bool A_NU, bool B_NU, bool T_NU, bool ZD, bool FAST, bool SPLIT = false,
-          int TILE = kTile, bool LIST = false, bool PEERS = false, bool RANK = false>
+          int TILE = kTile, bool LIST = false, bool PEERS = false, bool RANK = false, bool ACC = false>
 int launch_tile(const CUtensorMap& md, const CUtensorMap& mnu, const CUtensorMap& mw,
                 const KernelArgs& a, int grid, cudaStream_t s) {
-  auto k = pald_tile_kernel<PASS, A_NU, B_NU, T_NU, ZD, FAST, SPLIT, TILE, LIST, PEERS, RANK>;
+  auto k = pald_tile_kernel<PASS, A_NU, B_NU, T_NU, ZD, FAST, SPLIT, TILE, LIST, PEERS, RANK, ACC>;
   static bool attr_done[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -207,6 +241,35 @@ int launch_tile(const CUtensorMap& md, const CUtensorMap& mnu, const CUtensorMap
 }
 
 uint64_t round_up(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
+
+// Options of the caller's ABI version (v3: no device list) -> a full v4
+// struct with the defaults for the fields the caller does not have.
+int read_opts(const pald_gpu_opts* in, pald_gpu_opts* o) {
+  if (!in) return set_error(PALD_GPU_ERR_VALIDATION, "null options");
+  if (in->struct_size != sizeof(pald_gpu_opts) && in->struct_size != PALD_GPU_OPTS_V3_SIZE)
+    return set_error(PALD_GPU_ERR_VALIDATION, "pald_gpu_opts.struct_size mismatch (%u: expected %zu or %u)",
+                     in->struct_size, sizeof(pald_gpu_opts), PALD_GPU_OPTS_V3_SIZE);
+  std::memset(o, 0, sizeof(*o));
+  std::memcpy(o, in, in->struct_size);
+  o->struct_size = sizeof(pald_gpu_opts);
+  if (o->num_devices < 0 || o->num_devices > PALD_GPU_MAX_DEVICES)
+    return set_error(PALD_GPU_ERR_VALIDATION, "num_devices %d out of range [0, %d]", o->num_devices,
+                     PALD_GPU_MAX_DEVICES);
+  for (int e : {o->exchange_focus, o->exchange_cohesion})
+    if (e < PALD_GPU_EXCHANGE_AUTO || e > PALD_GPU_EXCHANGE_RED)
+      return set_error(PALD_GPU_ERR_VALIDATION, "unknown exchange transport %d", e);
+  if (o->exchange_cohesion == PALD_GPU_EXCHANGE_RED)
+    return set_error(PALD_GPU_ERR_VALIDATION, "the RED exchange applies to pass 1 only");
+  if (o->num_devices > 1) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess) count = 0;
+    for (int i = 0; i < o->num_devices; ++i)
+      if (o->devices[i] < 0 || o->devices[i] >= count)
+        return set_error(PALD_GPU_ERR_VALIDATION, "devices[%d] = %d is not a visible device (%d visible)", i,
+                         o->devices[i], count);
+  }
+  return PALD_GPU_OK;
+}
 
 int check_opts(const pald_gpu_opts* o) {
   if (!o) return set_error(PALD_GPU_ERR_VALIDATION, "null options");
@@ -272,7 +335,9 @@ struct pald_gpu_plan {
   int last_kernel = PALD_GPU_KERNEL_NONE;
   // Fused multi-GPU exchange: every rank's W and C mapped through CUDA IPC.
   PeerBufs peer_w{}, peer_c{};
+  PeerBufs peer_u{};                 // U of every rank (int32, stored as float*): peer-pull finish
   bool peer_mapped[kMaxPeers] = {};  // opened by this plan (to be closed)
+  bool peer_u_mapped[kMaxPeers] = {};
   int peer_rank = -1;
   bool sym_ready = false;                // tie scan done for the loaded D
   bool loaded = false;
@@ -292,6 +357,9 @@ struct pald_gpu_plan {
   float* split_partial = nullptr;
   int split_item_count = -1;     // -1: not built; 0: no split
   int split_pair_count = 0;
+  // Accurate mode (PALD_GPU_FLAG_ACCURATE): double sums of the fp32 block
+  // partials of pass 2 (n x ld doubles, allocated on first use).
+  double* c64 = nullptr;
   uint64_t launches = 0;
 
   void close_peers() {
@@ -301,9 +369,18 @@ struct pald_gpu_plan {
       cudaIpcCloseMemHandle(peer_c.ptr[q]);
       peer_mapped[q] = false;
     }
+    close_peer_u();
     peer_w = PeerBufs{};
     peer_c = PeerBufs{};
     peer_rank = -1;
+  }
+  void close_peer_u() {
+    for (int q = 0; q < peer_u.count; ++q) {
+      if (!peer_u_mapped[q]) continue;
+      cudaIpcCloseMemHandle(peer_u.ptr[q]);
+      peer_u_mapped[q] = false;
+    }
+    peer_u = PeerBufs{};
   }
 
   ~pald_gpu_plan() {
@@ -335,6 +412,7 @@ struct pald_gpu_plan {
     cudaFree(split_items);
     cudaFree(split_pairs);
     cudaFree(split_partial);
+    cudaFree(c64);
     cudaSetDevice(prev);
   }
 };
@@ -370,6 +448,28 @@ bool split_enabled() {
     return e ? atoi(e) : 1;
   }();
   return m != 0;
+}
+
+// Accurate mode: pass-2 terms per fp32 block partial (PALD_GPU_ACC_BLOCK,
+// default 256; rounded to whole k chunks of each kernel). A 2048-term fp32
+// chain alone drifts by ~3e-6 (the reference's own fp32 C at n = 2048);
+// 256-term blocks keep C within ~2e-7 of fp64 at n <= 32768 for ~2 % of
+// pass-2 time (one double read-modify-write of the thread's outputs per
+// block, outside the inner loop).
+int acc_block_terms() {
+  static const int t = [] {
+    const char* e = getenv("PALD_GPU_ACC_BLOCK");
+    const int v = e ? atoi(e) : 256;
+    return v >= kSymBK ? v : 256;
+  }();
+  return t;
+}
+bool accurate(const pald_gpu_plan* p) { return (p->flags & PALD_GPU_FLAG_ACCURATE) != 0; }
+
+int ensure_c64(pald_gpu_plan* p) {
+  if (p->c64) return PALD_GPU_OK;
+  PALD_CUDA(cudaMalloc(&p->c64, p->n * p->ld * sizeof(double)));
+  return PALD_GPU_OK;
 }
 
 size_t sym_mask_words(const pald_gpu_plan* p) { return p->nb * (p->nb + 1) / 2 * p->sym_nch; }
@@ -670,7 +770,8 @@ int launch_tie_scan(pald_gpu_plan* p, const uint32_t* keys, const int* rows, con
   return PALD_GPU_OK;
 }
 
-int check_stats(const pald_gpu_plan* p, const Stats& st, bool validate, bool* fast_out, int* p2_out);
+int check_stats(const pald_gpu_plan* p, const Stats& st, bool validate, bool* fast_out, int* p2_out,
+                const float* d, uint64_t ldd);
 int tie_summary(pald_gpu_plan* p, cudaStream_t s);
 
 int ensure_aux(pald_gpu_plan* p) {
@@ -685,6 +786,7 @@ int plan_load_impl(pald_gpu_plan* p, const float* dD, uint64_t ldd, cudaStream_t
   const int n = (int)p->n;
   Stats init{};
   init.min_pos_bits = 0xffffffffu;
+  init.key_diag = init.key_notpos = init.key_asym = ~0ull;
   *p->stats_host = init;
   int rc;
   p->rank_ready = false;
@@ -717,7 +819,7 @@ int plan_load_impl(pald_gpu_plan* p, const float* dD, uint64_t ldd, cudaStream_t
   PALD_CUDA(cudaStreamSynchronize(s));
   bool fast = false;
   int p2 = 0;
-  if ((rc = check_stats(p, *p->stats_host, validate, &fast, &p2))) {
+  if ((rc = check_stats(p, *p->stats_host, validate, &fast, &p2, dD, ldd))) {
     if (ranks) cudaStreamSynchronize(p->aux);  // leave no work behind on the plan
     p->rank_ready = false;
     return rc;
@@ -757,13 +859,26 @@ int plan_load_impl(pald_gpu_plan* p, const float* dD, uint64_t ldd, cudaStream_t
 // Validation errors of the reference (types.hpp:45-65) and the range check
 // of the FFMA.SAT compare path: scale by 2^p2 so that the largest value lies
 // in [0.5, 1); all values must stay >= 2^-102.
-int check_stats(const pald_gpu_plan* p, const Stats& st, bool validate, bool* fast_out, int* p2_out) {
-  if (validate) {
-    if (st.diag_nonzero) return set_error(PALD_GPU_ERR_VALIDATION, "distance matrix diagonal entry is nonzero");
-    if (st.offdiag_not_positive)
+int check_stats(const pald_gpu_plan* p, const Stats& st, bool validate, bool* fast_out, int* p2_out,
+                const float* d, uint64_t ldd) {
+  if (validate && (st.diag_nonzero || st.offdiag_not_positive || st.asymmetric)) {
+    // the reference's first violation (types.hpp:50-62): smallest key;
+    // positivity before symmetry on the same entry
+    const unsigned long long k = std::min(st.key_diag, std::min(st.key_notpos, st.key_asym));
+    const unsigned long long x = k / p->n, y = k % p->n;
+    if (k == st.key_diag)
+      return set_error(PALD_GPU_ERR_VALIDATION, "distance matrix diagonal entry (%llu,%llu) is nonzero", x, x);
+    if (k == st.key_notpos) {
+      float v = NAN;
+      if (d) cudaMemcpy(&v, d + x * ldd + y, sizeof(float), cudaMemcpyDefault);
+      char num[64];
+      if (std::isnan(v)) snprintf(num, sizeof(num), "%snan", std::signbit(v) ? "-" : "");
+      else snprintf(num, sizeof(num), "%f", (double)v);  // std::to_string(double)
       return set_error(PALD_GPU_ERR_VALIDATION,
-                       "off-diagonal distance must be positive (duplicate points are rejected)");
-    if (st.asymmetric) return set_error(PALD_GPU_ERR_VALIDATION, "distance matrix not symmetric");
+                       "off-diagonal distance (%llu,%llu) must be positive, got %s (duplicate points are rejected)",
+                       x, y, num);
+    }
+    return set_error(PALD_GPU_ERR_VALIDATION, "distance matrix not symmetric at (%llu,%llu)", x, y);
   }
   bool fast = !(p->flags & PALD_GPU_FLAG_FORCE_EXACT) && !st.offdiag_zero && !st.has_inf &&
               !st.has_nan && st.min_pos_bits != 0xffffffffu;
@@ -894,7 +1009,8 @@ int launch_focus_range(pald_gpu_plan* p, long long ub, long long ue, const int2*
 int plan_focus_finish_impl(pald_gpu_plan* p, cudaStream_t s) {
   if (!p->loaded) return set_error(PALD_GPU_ERR_VALIDATION, "plan has no distances loaded");
   const uint64_t tiles = p->nb * (p->nb + 1) / 2;
-  focus_finish_kernel<<<(unsigned)(tiles * 4), 256, 0, s>>>(p->u, p->w, (int)p->n, (int)p->ld, (int)p->nb, 0);
+  focus_finish_kernel<false><<<(unsigned)(tiles * 4), 256, 0, s>>>(p->u, p->w, (int)p->n, (int)p->ld, (int)p->nb, 0,
+                                                                  FinishPeers{});
   PALD_CUDA(cudaGetLastError());
   ++p->launches;
   return PALD_GPU_OK;
@@ -924,6 +1040,20 @@ int launch_cohesion(pald_gpu_plan* p, uint64_t row0, uint64_t row1, cudaStream_t
   const CUtensorMap& md = TILE == 64 ? p->tm_d64 : TILE == 32 ? p->tm_dt32 : p->tm_d;
   const CUtensorMap& mn = TILE == 64 ? p->tm_dnu64 : TILE == 32 ? p->tm_dnut32 : p->tm_dnu;
   const CUtensorMap& mw = TILE == 64 ? p->tm_w64 : TILE == 32 ? p->tm_wt32 : p->tm_w;
+  if (accurate(p)) {
+    int rc = ensure_c64(p);
+    if (rc) return rc;
+    a.c64 = p->c64;
+    a.acc_chunks = std::max(1, acc_block_terms() / kBK);
+    if (!p->exact) {
+      return tri     ? launch_tile<1, true, true, false, true, true, false, TILE, false, false, false, true>(md, mn, mw, a, grid, s)
+             : split ? launch_tile<1, false, false, false, false, true, true, TILE, false, false, false, true>(md, mn, mw, a, grid, s)
+                     : launch_tile<1, false, true, false, false, true, false, TILE, false, false, false, true>(md, mn, mw, a, grid, s);
+    }
+    return tri     ? launch_tile<1, true, true, false, true, false, false, TILE, false, false, false, true>(md, mn, mw, a, grid, s)
+           : split ? launch_tile<1, false, false, false, false, false, true, TILE, false, false, false, true>(md, mn, mw, a, grid, s)
+                   : launch_tile<1, false, true, false, false, false, false, TILE, false, false, false, true>(md, mn, mw, a, grid, s);
+  }
   if (!p->exact) {
     return tri     ? launch_tile<1, true, true, false, true, true, false, TILE>(md, mn, mw, a, grid, s)
            : split ? launch_tile<1, false, false, false, false, true, true, TILE>(md, mn, mw, a, grid, s)
@@ -948,6 +1078,14 @@ int launch_cohesion_list(pald_gpu_plan* p, const int2* list, int count, cudaStre
   const CUtensorMap& md = TILE == 64 ? p->tm_d64 : p->tm_dt32;
   const CUtensorMap& mn = TILE == 64 ? p->tm_dnu64 : p->tm_dnut32;
   const CUtensorMap& mw = TILE == 64 ? p->tm_w64 : p->tm_wt32;
+  if (accurate(p)) {
+    int rc = ensure_c64(p);
+    if (rc) return rc;
+    a.c64 = p->c64;
+    a.acc_chunks = std::max(1, acc_block_terms() / kBK);
+    if (tri) return launch_tile<1, true, true, false, true, true, false, TILE, true, false, false, true>(md, mn, mw, a, grid, s);
+    return launch_tile<1, false, true, false, false, true, false, TILE, true, false, false, true>(md, mn, mw, a, grid, s);
+  }
   if (tri) return launch_tile<1, true, true, false, true, true, false, TILE, true>(md, mn, mw, a, grid, s);
   return launch_tile<1, false, true, false, false, true, false, TILE, true>(md, mn, mw, a, grid, s);
 }
@@ -968,6 +1106,10 @@ int launch_sym(pald_gpu_plan* p, int t0, int t1, cudaStream_t s, bool peers = fa
     PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
     PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
     PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
+    PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<false, false, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
+    PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<true, false, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
+    PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<false, true, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
+    PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<true, true, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
     attr_done[p->device & 63] = true;
   }
   const int grid = std::min(t1 - t0, p->sms);
@@ -981,13 +1123,24 @@ int launch_sym(pald_gpu_plan* p, int t0, int t1, cudaStream_t s, bool peers = fa
     const char* e = getenv("PALD_GPU_ROUND_SYNC");  // 1: round barrier on
     return e ? atoi(e) : 0;
   }();
-  const bool sync = round_sync && sync_mode && (t1 - t0) / grid >= 2;
+  const bool acc = accurate(p);
+  const bool sync = round_sync && sync_mode && !acc && (t1 - t0) / grid >= 2;
+  if (acc) {
+    const int rc = ensure_c64(p);
+    if (rc) return rc;
+  }
   if (sync) PALD_CUDA(cudaMemsetAsync(p->round_bar, 0, sizeof(unsigned int), s));
   SymArgs a{p->ds, p->c, p->focus_tiles, p->sym_masks, p->sym_tile_flags,
             (int)p->n, (int)p->ld, (int)p->nb, p->sym_nch, t0, t1, p->peer_c,
             sync ? p->round_bar : nullptr};
+  a.c64 = p->c64;
+  a.acc_chunks = std::max(1, acc_block_terms() / kSymBK);
   const bool tri = p->algorithm == PALD_GPU_TRIPLET;
-  auto k = sync ? (peers ? (tri ? pald_sym_cohesion_kernel<true, true, true> : pald_sym_cohesion_kernel<false, true, true>)
+  auto k = acc ? (peers ? (tri ? pald_sym_cohesion_kernel<true, true, false, false, true>
+                               : pald_sym_cohesion_kernel<false, true, false, false, true>)
+                        : (tri ? pald_sym_cohesion_kernel<true, false, false, false, true>
+                               : pald_sym_cohesion_kernel<false, false, false, false, true>))
+           : sync ? (peers ? (tri ? pald_sym_cohesion_kernel<true, true, true> : pald_sym_cohesion_kernel<false, true, true>)
                         : (tri ? pald_sym_cohesion_kernel<true, false, true> : pald_sym_cohesion_kernel<false, false, true>))
                 : (peers ? (tri ? pald_sym_cohesion_kernel<true, true> : pald_sym_cohesion_kernel<false, true>)
                          : (tri ? pald_sym_cohesion_kernel<true, false> : pald_sym_cohesion_kernel<false, false>));
@@ -1103,7 +1256,7 @@ int plan_cohesion_impl(pald_gpu_plan* p, uint64_t row0, uint64_t row1, cudaStrea
   // identical: every C entry is the same in-order sum either way.
   const uint64_t tiles128 = ((row1 - row0 + kTile - 1) / kTile) * p->nb;
   if (row0 == 0 && row1 == p->n && p->sym_ready && sym_preferred(p)) {
-    if (p->algorithm == PALD_GPU_TRIPLET && split_enabled()) {
+    if (p->algorithm == PALD_GPU_TRIPLET && split_enabled() && !accurate(p)) {
       bool used = false;
       const int rc = launch_sym_split(p, s, &used);
       if (rc) return rc;
@@ -1217,6 +1370,7 @@ int load_focus_banded(pald_gpu_plan* p, const float* D, cudaStream_t s, cudaStre
   const bool validate = !(p->flags & PALD_GPU_FLAG_SKIP_VALIDATION);
   Stats init{};
   init.min_pos_bits = 0xffffffffu;
+  init.key_diag = init.key_notpos = init.key_asym = ~0ull;
   *p->stats_host = init;
   PALD_CUDA(cudaMemcpyAsync(p->stats, p->stats_host, sizeof(Stats), cudaMemcpyHostToDevice, sa));
   PALD_CUDA(cudaMemsetAsync(p->w, 0, p->n * p->ld * 4, s));  // pass-1 counts
@@ -1267,7 +1421,7 @@ int load_focus_banded(pald_gpu_plan* p, const float* D, cudaStream_t s, cudaStre
   PALD_CUDA(cudaStreamSynchronize(sa));
   bool fast = false;
   int p2 = 0;
-  if ((rc = check_stats(p, *p->stats_host, validate, &fast, &p2))) {
+  if ((rc = check_stats(p, *p->stats_host, validate, &fast, &p2, p->c, p->ld))) {
     cudaStreamSynchronize(s);  // no work left behind on the plan
     p->rank_ready = false;
     return rc;
@@ -1333,6 +1487,8 @@ int plan_cohesion_share_peers_impl(pald_gpu_plan* p, uint64_t part, uint64_t par
   return rc;
 }
 
+#include "pald_multi.cuh"
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -1351,11 +1507,22 @@ const char* pald_gpu_last_error(void) { return g_last_error.c_str(); }
 
 int pald_gpu_abi_version(void) { return PALD_GPU_ABI_VERSION; }
 
+int pald_gpu_visible_devices(void) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return c;
+}
+
 uint64_t pald_gpu_focus_units(const pald_gpu_plan* p) { return p ? focus_units(p) : 0; }
 
-int pald_gpu_plan_create(uint64_t n, const pald_gpu_opts* o, pald_gpu_plan** out) {
-  int rc = check_opts(o);
-  if (rc) return rc;
+int pald_gpu_plan_create(uint64_t n, const pald_gpu_opts* o_in, pald_gpu_plan** out) {
+  pald_gpu_opts oo;
+  int rc = read_opts(o_in, &oo);
+  if (rc || (rc = check_opts(&oo))) return rc;
+  const pald_gpu_opts* o = &oo;
   if (!out) return set_error(PALD_GPU_ERR_VALIDATION, "null plan output");
   if (n < 2) return set_error(PALD_GPU_ERR_VALIDATION, "distance matrix needs n >= 2, got n=%llu", (unsigned long long)n);
   if (n > (1ull << 24)) return set_error(PALD_GPU_ERR_VALIDATION, "n=%llu exceeds 2^24 (fp32 focus counts)", (unsigned long long)n);
@@ -1471,6 +1638,47 @@ int pald_gpu_plan_attach_peers(pald_gpu_plan* p, int world, int rank, const pald
   return PALD_GPU_OK;
 }
 
+int pald_gpu_plan_export_u(const pald_gpu_plan* p, pald_gpu_ipc_handle* u) {
+  if (!p || !u) return set_error(PALD_GPU_ERR_VALIDATION, "null argument");
+  DeviceGuard g(p->device);
+  PALD_CUDA(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(u), p->u));
+  return PALD_GPU_OK;
+}
+
+int pald_gpu_plan_attach_peers_u(pald_gpu_plan* p, const pald_gpu_ipc_handle* u_handles) {
+  if (!p || !u_handles) return set_error(PALD_GPU_ERR_VALIDATION, "null argument");
+  if (p->peer_rank < 0) return set_error(PALD_GPU_ERR_VALIDATION, "attach the W / C peers first");
+  DeviceGuard g(p->device);
+  p->close_peer_u();
+  const int world = p->peer_w.count;
+  for (int q = 0; q < world; ++q) {
+    if (q == p->peer_rank) {
+      p->peer_u.ptr[q] = reinterpret_cast<float*>(p->u);
+      continue;
+    }
+    void* pu = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&pu, *reinterpret_cast<const cudaIpcMemHandle_t*>(&u_handles[q]),
+                                               cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      p->peer_u.count = q;
+      p->close_peer_u();
+      return set_error(PALD_GPU_ERR_COMM, "cudaIpcOpenMemHandle (U) of rank %d: %s", q, cudaGetErrorString(e));
+    }
+    p->peer_u.ptr[q] = static_cast<float*>(pu);
+    p->peer_u_mapped[q] = true;
+    p->peer_u.count = q + 1;
+  }
+  p->peer_u.count = world;
+  return PALD_GPU_OK;
+}
+
+int pald_gpu_plan_focus_finish_peers(pald_gpu_plan* p, uint64_t part, uint64_t parts, int u_all, void* stream) {
+  if (!p) return set_error(PALD_GPU_ERR_VALIDATION, "null plan");
+  DeviceGuard g(p->device);
+  return plan_focus_finish_peers_impl(p, part, parts, u_all != 0, static_cast<cudaStream_t>(stream));
+}
+
 int pald_gpu_plan_detach_peers(pald_gpu_plan* p) {
   if (!p) return set_error(PALD_GPU_ERR_VALIDATION, "null plan");
   DeviceGuard g(p->device);
@@ -1498,7 +1706,7 @@ int pald_gpu_plan_cohesion_share(pald_gpu_plan* p, uint64_t part, uint64_t parts
 
 int pald_gpu_plan_get_info(const pald_gpu_plan* p, pald_gpu_plan_info* out) {
   if (!p || !out) return set_error(PALD_GPU_ERR_VALIDATION, "null argument");
-  if (out->struct_size < sizeof(pald_gpu_plan_info))
+  if (out->struct_size < offsetof(pald_gpu_plan_info, pair_kernel_preferred))
     return set_error(PALD_GPU_ERR_VALIDATION, "pald_gpu_plan_info.struct_size too small");
   out->cohesion_kernel = p->last_kernel;
   out->exact_path = p->exact ? 1 : 0;
@@ -1506,6 +1714,8 @@ int pald_gpu_plan_get_info(const pald_gpu_plan* p, pald_gpu_plan_info* out) {
   out->exact_step_share = p->sym_marked;
   out->launches = p->launches;
   out->rank_codes = p->rank_ready ? 1 : 0;
+  if (out->struct_size >= offsetof(pald_gpu_plan_info, pair_kernel_preferred) + sizeof(int32_t))
+    out->pair_kernel_preferred = (p->loaded && p->sym_ready && sym_preferred(p)) ? 1 : 0;
   return PALD_GPU_OK;
 }
 
@@ -1520,16 +1730,22 @@ int pald_gpu_plan_buffers(const pald_gpu_plan* p, pald_gpu_buffers* out) {
   out->tiles_per_dim = p->nb;
   out->exact_path = p->exact ? 1 : 0;
   out->reserved = 0;
+  out->C64 = p->c64;
   return PALD_GPU_OK;
 }
 
 uint64_t pald_gpu_plan_launches(const pald_gpu_plan* p) { return p ? p->launches : 0; }
 
 int pald_gpu_cohesion_f32_device(const float* dD, uint64_t ldd, uint64_t n,
-                                 const pald_gpu_opts* o, int32_t* dU, uint64_t ldu, float* dC,
+                                 const pald_gpu_opts* o_in, int32_t* dU, uint64_t ldu, float* dC,
                                  uint64_t ldc, void* stream) {
-  int rc = check_opts(o);
-  if (rc) return rc;
+  pald_gpu_opts oo;
+  int rc = read_opts(o_in, &oo);
+  if (rc || (rc = check_opts(&oo))) return rc;
+  const pald_gpu_opts* o = &oo;
+  if (o->num_devices > 1)
+    return set_error(PALD_GPU_ERR_UNSUPPORTED, "the device-pointer API runs on one device (use the host API "
+                                               "or a staged plan per device for several)");
   if (!dD || !dC) return set_error(PALD_GPU_ERR_VALIDATION, "null device pointer");
   if (ldd < n || ldc < n || (dU && ldu < n)) return set_error(PALD_GPU_ERR_VALIDATION, "leading dimension < n");
   int dev = o->device;
@@ -1551,12 +1767,19 @@ int pald_gpu_cohesion_f32_device(const float* dD, uint64_t ldd, uint64_t n,
 #define PALD_HOST_BANDS 16  // one raster group per band at n = 32768: e2e 3.790 -> 3.773 s
 #endif
 
-int pald_gpu_cohesion_f32(const float* D, uint64_t n, const pald_gpu_opts* o, int32_t* U_out,
+int pald_gpu_cohesion_f32(const float* D, uint64_t n, const pald_gpu_opts* o_in, int32_t* U_out,
                           float* C_out, pald_gpu_phase_times* times) {
-  int rc = check_opts(o);
-  if (rc) return rc;
+  pald_gpu_opts oo;
+  int rc = read_opts(o_in, &oo);
+  if (rc || (rc = check_opts(&oo))) return rc;
+  const pald_gpu_opts* o = &oo;
   if (!D || !C_out) return set_error(PALD_GPU_ERR_VALIDATION, "null host pointer");
   if (n < 2) return set_error(PALD_GPU_ERR_VALIDATION, "distance matrix needs n >= 2, got n=%llu", (unsigned long long)n);
+  if (o->num_devices > 1) {
+    std::lock_guard<std::mutex> lk(cache().mu);
+    DeviceGuard g(-1);
+    return run_multi(D, n, o, U_out, C_out, times);
+  }
   int dev = o->device;
   if (dev < 0) PALD_CUDA(cudaGetDevice(&dev));
   DeviceGuard g(dev);
@@ -1680,8 +1903,18 @@ int pald_gpu_points_to_distances(const double* dP, uint64_t n, uint64_t dim, flo
   if (n < 2) return set_error(PALD_GPU_ERR_VALIDATION, "point cloud needs at least 2 points");
   if (dim < 1) return set_error(PALD_GPU_ERR_VALIDATION, "points need at least one coordinate");
   if (ldd < n) return set_error(PALD_GPU_ERR_VALIDATION, "ldd < n");
-  points_kernel<<<grid_rows(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(dP, (int)n, (int)dim, dD, ldd);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  unsigned long long* key = nullptr;
+  PALD_CUDA(cudaMallocAsync(&key, sizeof(unsigned long long), s));
+  PALD_CUDA(cudaMemsetAsync(key, 0xff, sizeof(unsigned long long), s));
+  points_kernel<<<grid_rows(n), 256, 0, s>>>(dP, (int)n, (int)dim, dD, ldd, key);
   PALD_CUDA(cudaGetLastError());
+  unsigned long long k = ~0ull;
+  PALD_CUDA(cudaMemcpyAsync(&k, key, sizeof(k), cudaMemcpyDeviceToHost, s));
+  PALD_CUDA(cudaFreeAsync(key, s));
+  PALD_CUDA(cudaStreamSynchronize(s));
+  if (k != ~0ull)
+    return set_error(PALD_GPU_ERR_VALIDATION, "duplicate points %llu and %llu (zero distance)", k / n, k % n);
   return PALD_GPU_OK;
 }
 

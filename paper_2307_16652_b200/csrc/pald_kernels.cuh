@@ -121,6 +121,8 @@ struct KernelArgs {
                             // pass 2: optional explicit tile list (else the raster)
   int group_rows;           // cohesion raster group height (tile rows)
   PeerBufs peers;           // PEERS kernels: pass-1 counts go to every rank's W
+  double* c64;              // ACC kernels: double sums of the fp32 block partials (n x ld)
+  int acc_chunks;           // ACC kernels: k chunks per fp32 block partial
 };
 
 constexpr int kGroupRows = 16;  // tile rows per raster group (L2 reuse of the panels)
@@ -156,6 +158,60 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
       : "memory");
+}
+
+// Stage release of the pipelines: each warp's lane 0 adds one arrival
+// after __syncwarp (which orders the warp's shared-memory reads of the
+// stage before it); the arrival that completes the count refills the stage
+// with TMA. acq_rel: every warp's reads happen-before the refill issued by
+// the last arriver (the async-proxy write of the next TMA load).
+__device__ __forceinline__ uint32_t stage_arrive(uint32_t* cnt) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+               : "=r"(old)
+               : "r"(smem_u32(cnt))
+               : "memory");
+  return old;
+}
+
+// Accurate mode (PALD_GPU_FLAG_ACCURATE): the fp32 register sums of an
+// output are flushed every `acc_chunks` k chunks into a double buffer and
+// restarted from 0. Adding a partial fp32 sum of positive terms 1/u (u in
+// [2, 2^24]) to a double sum of such partials is exact (the values span
+// less than 2^53 units of the smallest ulp), so the result is the exact sum
+// of the fp32 block partials -- independent of the flush order -- and only
+// the blocks' own fp32 rounding remains (k blocks of <= acc_chunks * BK
+// terms instead of one n-term chain). `first` starts the output's sum.
+__device__ __forceinline__ void acc_flush4(double* p, float a, float b, float c, float d, bool first) {
+  double2* q = reinterpret_cast<double2*>(p);
+  double2 v0 = first ? make_double2(0.0, 0.0) : q[0];
+  double2 v1 = first ? make_double2(0.0, 0.0) : q[1];
+  v0.x += (double)a;
+  v0.y += (double)b;
+  v1.x += (double)c;
+  v1.y += (double)d;
+  q[0] = v0;
+  q[1] = v1;
+}
+// Final flush: the double sums (also kept in the buffer) rounded to fp32.
+__device__ __forceinline__ float4 acc_final4(double* p, float a, float b, float c, float d, bool first) {
+  acc_flush4(p, a, b, c, d, first);
+  const double2* q = reinterpret_cast<const double2*>(p);
+  const double2 v0 = q[0], v1 = q[1];
+  return make_float4(__double2float_rn(v0.x), __double2float_rn(v0.y), __double2float_rn(v1.x),
+                     __double2float_rn(v1.y));
+}
+__device__ __forceinline__ void acc_flush2(double* p, float a, float b, bool first) {
+  double2* q = reinterpret_cast<double2*>(p);
+  double2 v0 = first ? make_double2(0.0, 0.0) : q[0];
+  v0.x += (double)a;
+  v0.y += (double)b;
+  q[0] = v0;
+}
+__device__ __forceinline__ float2 acc_final2(double* p, float a, float b, bool first) {
+  acc_flush2(p, a, b, first);
+  const double2 v0 = *reinterpret_cast<const double2*>(p);
+  return make_float2(__double2float_rn(v0.x), __double2float_rn(v0.y));
 }
 
 __device__ __forceinline__ uint32_t nu_bits(uint32_t v) { return v + 1u; }
@@ -544,7 +600,7 @@ __device__ __forceinline__ WorkSplit make_split(const KernelArgs& a, int C, int 
 // the last warp to finish with it (shared-memory arrival counter), so no
 // block-wide barrier sits in the main loop.
 template <int PASS, bool A_NU, bool B_NU, bool T_NU, bool ZERO_DIAG, bool FAST, bool SPLIT = false,
-          int TILE = kTile, bool LIST = false, bool PEERS = false, bool RANK = false>
+          int TILE = kTile, bool LIST = false, bool PEERS = false, bool RANK = false, bool ACC = false>
 __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE, RANK))
     pald_tile_kernel(const __grid_constant__ CUtensorMap tm_d,
                      const __grid_constant__ CUtensorMap tm_dnu,
@@ -554,6 +610,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE, RANK))
   // so the compiler keeps the shared address space (LDS, not generic LD).
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   static_assert(!RANK || (PASS == 0 && TILE == kTile), "rank codes: 128-wide pass 1 only");
+  static_assert(!ACC || PASS == 1, "accurate mode: cohesion pass only");
   constexpr int kStages = stages_for(PASS, TILE, RANK);
   constexpr int TT = TILE / 16;  // outputs per thread per dimension
   constexpr int BOX = box_bytes(TILE);
@@ -594,10 +651,22 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE, RANK))
     s_nrem = nr;
   }
   __syncthreads();
-  const int R = ws.full + s_nrem;
-  auto run_t = [&](int ri) { return ri < ws.full ? ws.t_a + ri * G + g : s_rem[ri - ws.full][0]; };
-  auto run_c0 = [&](int ri) { return ri < ws.full ? 0 : s_rem[ri - ws.full][1]; };
-  auto run_c1 = [&](int ri) { return ri < ws.full ? nchunks : s_rem[ri - ws.full][2]; };
+  // ACC (whole cohesion tiles): each tile is walked as nsub consecutive
+  // runs of acc_chunks chunks (k blocks), flushed to the double sums in order
+  const int nsub = ACC ? (nchunks + args.acc_chunks - 1) / args.acc_chunks : 1;
+  const int R = (ws.full + s_nrem) * nsub;
+  auto run_t = [&](int ri) {
+    if constexpr (ACC) ri /= nsub;
+    return ri < ws.full ? ws.t_a + ri * G + g : s_rem[ri - ws.full][0];
+  };
+  auto run_c0 = [&](int ri) {
+    if constexpr (ACC) return (ri % nsub) * args.acc_chunks;
+    return ri < ws.full ? 0 : s_rem[ri - ws.full][1];
+  };
+  auto run_c1 = [&](int ri) {
+    if constexpr (ACC) return min(nchunks, (ri % nsub + 1) * args.acc_chunks);
+    return ri < ws.full ? nchunks : s_rem[ri - ws.full][2];
+  };
 
   constexpr int SB = stage_bytes(PASS, TILE, RANK);
   auto issue = [&](int t, int ch, int s) {
@@ -688,6 +757,10 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE, RANK))
     }
 
     int le_a = 0, le_b = 0;  // rank-coded triplet: thresholds currently shifted for <=
+    // ACC: this run is one k block of its tile; the first starts the double
+    // sums, the last rounds them to fp32 and writes C
+    const bool acc_first = ch_begin == 0;
+    const bool acc_last = ch_end == nchunks;
     for (int ch = ch_begin; ch < ch_end; ++ch, ++p) {
       const int s = p % kStages;
       mbar_wait(&full_bar[s], (p / kStages) & 1);
@@ -740,7 +813,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE, RANK))
       // Release the stage: the last warp to arrive refills it.
       __syncwarp();
       if (lane == 0) {
-        const uint32_t old = atomicAdd(&done_cnt[s], 1u);
+        const uint32_t old = stage_arrive(&done_cnt[s]);
         if (old == (uint32_t)(p / kStages + 1) * (kThreads / 32) - 1u && p + kStages < P)
           issue(run_t(pr_ri), pr_ch, s);
         pr_advance();
@@ -783,10 +856,49 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE, RANK))
           v[2 * jp] = acc[i][jp].x;
           v[2 * jp + 1] = acc[i][jp].y;
         }
+        if constexpr (ACC) {  // k block done: into the double sums (the last: rounded to fp32)
+          double* prow = args.c64 + (size_t)r * ld;
+          if (!acc_last) {
+            if constexpr (TILE == 32) {
+              const int cc = c0 + tx * 2;
+              if (cc < n) acc_flush2(prow + cc, v[0], v[1], acc_first);
+            } else {
+#pragma unroll
+              for (int h = 0; h < TT / 4; ++h) {
+                const int cc = c0 + h * (TILE / 2) + tx * 4;
+                if (cc < n) acc_flush4(prow + cc, v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3], acc_first);
+              }
+            }
+            continue;
+          }
+          if constexpr (TILE == 32) {
+            const int cc = c0 + tx * 2;
+            if (cc < n) {
+              const float2 f = acc_final2(prow + cc, v[0], v[1], acc_first);
+              v[0] = f.x;
+              v[1] = f.y;
+            }
+          } else {
+#pragma unroll
+            for (int h = 0; h < TT / 4; ++h) {
+              const int cc = c0 + h * (TILE / 2) + tx * 4;
+              if (cc < n) {
+                const float4 f = acc_final4(prow + cc, v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3], acc_first);
+                v[4 * h] = f.x;
+                v[4 * h + 1] = f.y;
+                v[4 * h + 2] = f.z;
+                v[4 * h + 3] = f.w;
+              }
+            }
+          }
+        }
         if (ZERO_DIAG) {
 #pragma unroll
           for (int j = 0; j < TT; ++j)
-            if (c0 + row_off<TILE>(tx, j) == r) v[j] = 0.f;
+            if (c0 + row_off<TILE>(tx, j) == r) {
+              v[j] = 0.f;
+              if constexpr (ACC) args.c64[(size_t)r * ld + r] = 0.0;
+            }
         }
         float* crow = args.c + (size_t)r * ld;
         // Columns past n land in the row padding (ld >= round_up(n, 32)).
@@ -812,18 +924,35 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE, RANK))
 }
 
 // Focus epilogue: counts (accumulated in the W buffer, upper-triangular
-// tiles of tile rows [tr_begin, tr_end)) -> U[r][c] = U[c][r] = count and
-// W[r][c] = W[c][r] = 1/count (IEEE division, Real(1)/Real(cnt),
-// blocked.hpp:401); diagonal 0. One CTA per 64 x 64 quadrant of a tile; the
-// quadrant is staged in shared memory so that both the direct and the
-// mirrored writes coalesce.
+// tiles t_begin + blockIdx.x / 4 of the row-major tile list) -> U[r][c] =
+// U[c][r] = count and W[r][c] = W[c][r] = 1/count (IEEE division,
+// Real(1)/Real(cnt), blocked.hpp:401); diagonal 0. One CTA per 64 x 64
+// quadrant of a tile; the quadrant is staged in shared memory so that both
+// the direct and the mirrored writes coalesce.
+//
+// PEERS (multi-GPU exchange of pass 1, "peer pull"): the count of an entry
+// is the SUM of the partial counts in every device's W (read over peer
+// memory, integers < 2^24: exact in any order), and U / W are stored into
+// every device's buffers (peer stores). Each device finishes a disjoint
+// range of tiles, so the reads (upper tiles of its range, in every W) and
+// the writes (the same tiles and their mirrors) of different devices never
+// touch the same entries. u_all / w_all hold every device's buffers; the
+// calling device's own are u / w.
+struct FinishPeers {
+  int32_t* u[kMaxPeers];
+  float* w[kMaxPeers];
+  int count;
+  int u_all;  // 1: store U into every device (0: own U only)
+};
+
+template <bool PEERS>
 __global__ void __launch_bounds__(256)
     focus_finish_kernel(int32_t* __restrict__ u, float* __restrict__ w, int n, int ld, int nb,
-                        int tr_begin) {
+                        int t_begin, FinishPeers peers) {
   constexpr int Q = kTile / 2;
   __shared__ float tile[Q][Q + 1];
   int tr, tc;
-  tri_coords(blockIdx.x >> 2, nb, tr, tc);
+  tri_coords(t_begin + (int)(blockIdx.x >> 2), nb, tr, tc);
   const int qr = (blockIdx.x >> 1) & 1, qc = blockIdx.x & 1;
   if (tr == tc && qr > qc) return;  // below the diagonal: the mirror of (0,1)
   const int r0 = tr * kTile + qr * Q, c0 = tc * kTile + qc * Q;
@@ -831,9 +960,32 @@ __global__ void __launch_bounds__(256)
   for (int idx = threadIdx.x; idx < Q * Q; idx += 256) {
     const int rl = idx / Q, cl = idx % Q;
     const int r = r0 + rl, c = c0 + cl;
-    tile[rl][cl] = (r < n && c < n) ? w[(size_t)r * ld + c] : 0.f;
+    float v = 0.f;
+    if (r < n && c < n) {
+      const size_t o = (size_t)r * ld + c;
+      if constexpr (PEERS) {
+        for (int q = 0; q < peers.count; ++q) v += peers.w[q][o];
+      } else {
+        v = w[o];
+      }
+    }
+    tile[rl][cl] = v;
   }
   __syncthreads();
+  const int nw = PEERS ? peers.count : 1, nu = PEERS ? (peers.u_all ? peers.count : 1) : 1;
+  auto put = [&](size_t o, int32_t uv, float wv) {
+    if constexpr (PEERS) {
+      for (int q = 0; q < nw; ++q) peers.w[q][o] = wv;
+      if (nu == 1) {
+        u[o] = uv;
+      } else {
+        for (int q = 0; q < nu; ++q) peers.u[q][o] = uv;
+      }
+    } else {
+      u[o] = uv;
+      w[o] = wv;
+    }
+  };
   for (int idx = threadIdx.x; idx < Q * Q; idx += 256) {
     {  // direct (r, c), r <= c
       const int rl = idx / Q, cl = idx % Q;
@@ -841,12 +993,10 @@ __global__ void __launch_bounds__(256)
       if (r < n && c < n && (!diag || rl <= cl)) {
         const size_t o = (size_t)r * ld + c;
         if (r == c) {
-          u[o] = 0;
-          w[o] = 0.f;
+          put(o, 0, 0.f);
         } else {
           const float v = tile[rl][cl];
-          u[o] = static_cast<int32_t>(v);
-          w[o] = 1.0f / v;
+          put(o, static_cast<int32_t>(v), 1.0f / v);
         }
       }
     }
@@ -855,9 +1005,7 @@ __global__ void __launch_bounds__(256)
       const int r = r0 + rl, c = c0 + cl;
       if (r < n && c < n && r < c) {
         const float v = tile[rl][cl];
-        const size_t o = (size_t)c * ld + r;
-        u[o] = static_cast<int32_t>(v);
-        w[o] = 1.0f / v;
+        put((size_t)c * ld + r, static_cast<int32_t>(v), 1.0f / v);
       }
     }
   }

@@ -81,6 +81,8 @@ struct SymArgs {
   // partial tiles to partial[slot] (2 x 128 x 128 floats) for sym_combine_kernel.
   const int4* items;
   float* partial;
+  double* c64;                // ACC kernels: double sums of the fp32 block partials (n x ld)
+  int acc_chunks;             // ACC kernels: k chunks (of kSymBK) per fp32 block partial
 };
 
 // Full-avalanche mix (murmur3 finalizer): the bucket takes the low bits and
@@ -379,13 +381,20 @@ __device__ __forceinline__ void store_c4(const SymArgs& a, size_t off, float4 v)
   }
 }
 
+__device__ __forceinline__ void sym_zero_diag4(float4& f, int c, int r) {
+  if (c == r) f.x = 0.f;
+  if (c + 1 == r) f.y = 0.f;
+  if (c + 2 == r) f.z = 0.f;
+  if (c + 3 == r) f.w = 0.f;
+}
+
 // Persistent pass-2 kernel over the tile pairs [tile_begin, tile_end) of the
 // grouped upper-triangular order (P <= Q). CTA g takes pairs
 // tile_begin + g, + G, ...; each pair streams all k chunks through a
 // 3-stage TMA/mbarrier pipeline (four 32 x 128 boxes per stage) and writes
 // C[P rows][Q cols] and, for P < Q, C[Q rows][P cols]. Pairwise Strict
 // (TRI = false) or triplet cohesion on the fast (scaled fp32) layout.
-template <bool TRI, bool PEERS = false, bool SYNC = false, bool SPLIT = false>
+template <bool TRI, bool PEERS = false, bool SYNC = false, bool SPLIT = false, bool ACC = false>
 __global__ void __launch_bounds__(kThreads, 1)
     pald_sym_cohesion_kernel(const __grid_constant__ CUtensorMap tm_d,
                              const __grid_constant__ CUtensorMap tm_dnu,
@@ -399,11 +408,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nch = args.nch;
   const int G = gridDim.x, g = blockIdx.x;
   const int first = args.tile_begin + g;
-  const int R = first < args.tile_end ? (args.tile_end - 1 - first) / G + 1 : 0;
+  // ACC: every pair is walked as nsub consecutive items of acc_chunks chunks
+  const int nsub = ACC ? (nch + args.acc_chunks - 1) / args.acc_chunks : 1;
+  const int R = (first < args.tile_end ? (args.tile_end - 1 - first) / G + 1 : 0) * nsub;
   // item ri of this CTA: tile pair and chunk range [cb, ce) (whole pairs
-  // unless SPLIT)
+  // unless SPLIT / ACC)
   auto item = [&](int ri, int2& tp, int& cb, int& ce, int& slot) {
-    if constexpr (SPLIT) {
+    if constexpr (ACC) {
+      const int pi = ri / nsub, sub = ri - pi * nsub;
+      tp = args.tiles[first + pi * G];
+      cb = sub * args.acc_chunks;
+      ce = min(nch, cb + args.acc_chunks);
+      slot = sub;
+    } else if constexpr (SPLIT) {
       const int4 it = args.items[first + ri * G];
       tp = make_int2(it.x, it.y);
       cb = it.z & 0xffff;
@@ -416,7 +433,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       slot = -1;
     }
   };
-  int P = R * nch;
+  int P = R / nsub * nch;
   if constexpr (SPLIT) {
     P = 0;
     for (int ri = 0; ri < R; ++ri) {
@@ -452,8 +469,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_load_2d(st + 2 * kSymBox, &tm_w, r0, k0, &full_bar[s]);
     tma_load_2d(st + 3 * kSymBox, &tm_w, c0, k0, &full_bar[s]);
   };
+  constexpr bool ITEMS = SPLIT || ACC;  // items other than whole pairs
   int pr_ri = 0, pr_ch = 0, pr_end = nch;
-  if constexpr (SPLIT) {
+  if constexpr (ITEMS) {
     int2 tp;
     int sl;
     item(0, tp, pr_ch, pr_end, sl);
@@ -461,7 +479,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto pr_advance = [&]() {
     if (++pr_ch == pr_end) {
       ++pr_ri;
-      if constexpr (SPLIT) {
+      if constexpr (ITEMS) {
         if (pr_ri < R) {
           int2 tp;
           int sl;
@@ -492,6 +510,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool all_marked =
         !TRI && (__ldg(args.tile_flags + tp.x) | __ldg(args.tile_flags + tp.y)) != 0u;
     float2 thr[8][4], acc[8][4], act[8][4];
+    // ACC: this item is one k block of its pair; the first starts the double
+    // sums, the last rounds them to fp32 and stores C
+    const bool acc_first = ch_b == 0, acc_last = ch_e == nch;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
 #pragma unroll
@@ -544,7 +565,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __syncwarp();
       if (lane == 0) {
-        const uint32_t old = atomicAdd(&done_cnt[s], 1u);
+        const uint32_t old = stage_arrive(&done_cnt[s]);
         if (old == (uint32_t)(p / kSymStages + 1) * (kThreads / 32) - 1u && p + kSymStages < P)
           issue(pr_ri, pr_ch, s);
         pr_advance();
@@ -601,6 +622,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const size_t rowo = (size_t)r * ld;
       const int ca = c0 + tx * 4, cb = c0 + 64 + tx * 4;
+      if constexpr (ACC) {
+        if (!acc_last) {  // k block done: into the double sums
+          if (ca < n) acc_flush4(args.c64 + rowo + ca, acc[i][0].x, acc[i][0].y, acc[i][1].x, acc[i][1].y, acc_first);
+          if (cb < n) acc_flush4(args.c64 + rowo + cb, acc[i][2].x, acc[i][2].y, acc[i][3].x, acc[i][3].y, acc_first);
+          continue;
+        }
+        // last k block: the double sums, rounded to fp32 (the triplet's zero
+        // diagonal is re-imposed after the rounding)
+        if (ca < n) {
+          float4 f = acc_final4(args.c64 + rowo + ca, acc[i][0].x, acc[i][0].y, acc[i][1].x, acc[i][1].y, acc_first);
+          if (TRI && diag) sym_zero_diag4(f, ca, r);
+          store_c4<PEERS>(args, rowo + ca, f);
+        }
+        if (cb < n) {
+          float4 f = acc_final4(args.c64 + rowo + cb, acc[i][2].x, acc[i][2].y, acc[i][3].x, acc[i][3].y, acc_first);
+          if (TRI && diag) sym_zero_diag4(f, cb, r);
+          store_c4<PEERS>(args, rowo + cb, f);
+        }
+        // the double sums keep the zero diagonal too (written by the thread
+        // that owns column r, after its own final flush)
+        if (TRI && diag && ((r >= ca && r < ca + 4) || (r >= cb && r < cb + 4))) args.c64[rowo + r] = 0.0;
+        continue;
+      }
       if (ca < n)
         store_c4<PEERS>(args, rowo + ca, make_float4(acc[i][0].x, acc[i][0].y, acc[i][1].x, acc[i][1].y));
       if (cb < n)
@@ -616,6 +660,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         const size_t rowo = (size_t)c * ld;
         const int ra = r0 + ty * 4, rb = r0 + 64 + ty * 4;
         const int jp = j >> 1;
+        if constexpr (ACC) {
+          double* prow = args.c64 + rowo;
+          const bool hi = (j & 1) != 0;
+          if (!acc_last) {
+            if (ra < n)
+              acc_flush4(prow + ra, hi ? act[0][jp].y : act[0][jp].x, hi ? act[1][jp].y : act[1][jp].x,
+                         hi ? act[2][jp].y : act[2][jp].x, hi ? act[3][jp].y : act[3][jp].x, acc_first);
+            if (rb < n)
+              acc_flush4(prow + rb, hi ? act[4][jp].y : act[4][jp].x, hi ? act[5][jp].y : act[5][jp].x,
+                         hi ? act[6][jp].y : act[6][jp].x, hi ? act[7][jp].y : act[7][jp].x, acc_first);
+            continue;
+          }
+          if (ra < n)
+            store_c4<PEERS>(args, rowo + ra,
+                            acc_final4(prow + ra, hi ? act[0][jp].y : act[0][jp].x, hi ? act[1][jp].y : act[1][jp].x,
+                                       hi ? act[2][jp].y : act[2][jp].x, hi ? act[3][jp].y : act[3][jp].x, acc_first));
+          if (rb < n)
+            store_c4<PEERS>(args, rowo + rb,
+                            acc_final4(prow + rb, hi ? act[4][jp].y : act[4][jp].x, hi ? act[5][jp].y : act[5][jp].x,
+                                       hi ? act[6][jp].y : act[6][jp].x, hi ? act[7][jp].y : act[7][jp].x, acc_first));
+          continue;
+        }
         if ((j & 1) == 0) {
           if (ra < n)
             store_c4<PEERS>(args, rowo + ra, make_float4(act[0][jp].x, act[1][jp].x, act[2][jp].x, act[3][jp].x));

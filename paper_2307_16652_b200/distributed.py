@@ -72,7 +72,15 @@ class ShardedRunner:
     interface -- the CPU tests use a gloo-backed stand-in).
     """
 
-    def __init__(self, engine, group=None, fused: bool | None = None):
+    def __init__(self, engine, group=None, fused: bool | None = None, focus_exchange: str | None = None,
+                 cohesion_exchange: str | None = None):
+        """``focus_exchange`` (pass 1): "peer" (peer-pull finish over the
+        mapped buffers, the default when mapping works), "red" (partial
+        counts added into every rank's W by the focus kernel) or "nccl" (SUM
+        all-reduce of the counts). ``cohesion_exchange`` (pass 2): "peer"
+        (the pair kernel stores into every rank's C, default when mapping
+        works) or "nccl" (SUM all-reduce of the C shares). ``fused=False``
+        forces "nccl" for both."""
         self.engine = engine
         self.group = group
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -80,10 +88,15 @@ class ShardedRunner:
         self.plan = make_shard_plan(engine.n, engine.tile, self.rank, self.world)
         self.fused = False
         self._fused_c = False  # this step's pass 2 ran fused
+        for x, ok in ((focus_exchange, ("peer", "red", "nccl", None)), (cohesion_exchange, ("peer", "nccl", None))):
+            if x not in ok:
+                raise ValueError(f"unknown exchange {x!r}")
         if fused is None:
             fused = self.world > 1 and hasattr(engine, "attach_peers")
         if fused and self.world > 1:
-            self.fused = self._attach_peers()
+            self.fused = self._attach_peers(need_u=(focus_exchange or "peer") == "peer")
+        self.focus_exchange = (focus_exchange or "peer") if self.fused else "nccl"
+        self.cohesion_exchange = (cohesion_exchange or "peer") if self.fused else "nccl"
         ld = engine.ld
         self._even = all(r1 - r0 == self.plan.band_rows
                          for r0, r1 in cohesion_row_split(engine.n, engine.tile, self.world))
@@ -93,19 +106,22 @@ class ShardedRunner:
             self._send = torch.zeros(self.plan.band_rows * ld, dtype=torch.float32, device=dev)
             self._recv = torch.empty(self.world * self.plan.band_rows * ld, dtype=torch.float32, device=dev)
 
-    def _attach_peers(self) -> bool:
-        """Map every rank's W and C into this process; all ranks agree on
-        the outcome (any failure -> collectives everywhere)."""
+    def _attach_peers(self, need_u: bool = True) -> bool:
+        """Map every rank's W and C (and U for the peer-pull finish) into this
+        process; all ranks agree on the outcome (any failure -> collectives
+        everywhere)."""
         ok = 1
         try:
-            mine = self.engine.export_buffers()
+            mine = self.engine.export_buffers() + ((self.engine.export_u(),) if need_u else (b"",))
         except Exception:
-            mine, ok = (b"", b""), 0
+            mine, ok = (b"", b"", b""), 0
         handles = [None] * self.world
         dist.all_gather_object(handles, mine, group=self.group)
         if ok and all(h[0] for h in handles):
             try:
                 self.engine.attach_peers(self.rank, [h[0] for h in handles], [h[1] for h in handles])
+                if need_u:
+                    self.engine.attach_peers_u([h[2] for h in handles])
             except Exception:
                 ok = 0
         else:
@@ -122,40 +138,76 @@ class ShardedRunner:
         backend = dist.get_backend(self.group)
         return self.engine.C.device if backend == "nccl" else "cpu"
 
-    def _sync_barrier(self) -> None:
-        torch.cuda.current_stream().synchronize()
+    def _sync_barrier(self, stream=None) -> None:
+        """Host barrier after this rank's work on `stream` (the stream the
+        engine calls were issued on, default the current one) has finished."""
+        (stream if stream is not None else torch.cuda.current_stream()).synchronize()
         dist.barrier(group=self.group)
+
+    @staticmethod
+    def _before_collective(stream) -> None:
+        """Collectives run on the current stream: order them after the work
+        issued on `stream`."""
+        if stream is not None and torch.cuda.is_available():
+            torch.cuda.current_stream().wait_stream(stream)
+
+    @staticmethod
+    def _after_collective(stream) -> None:
+        """Order later work on `stream` after the collective."""
+        if stream is not None and torch.cuda.is_available():
+            stream.wait_stream(torch.cuda.current_stream())
+
+    def _agree(self, flag: bool) -> bool:
+        """True iff `flag` holds on every rank (MIN all-reduce)."""
+        t = torch.tensor([1 if flag else 0], dtype=torch.int32, device=self._flag_device())
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
+        return bool(int(t.item()))
 
     def load(self, D, stream=None) -> None:
         self.engine.load(D, stream)
-        if self.fused:
-            self._sync_barrier()  # every rank's W zeroed before any rank adds into it
+        if self.world > 1 and self.focus_exchange == "red":
+            self._sync_barrier(stream)  # every rank's W zeroed before any rank adds into it
 
     def focus(self, stream=None) -> None:
-        """This rank's share of pass 1 (counts into W, or into every W)."""
-        if self.fused:
+        """This rank's share of pass 1 (counts into its W, or into every W)."""
+        if self.world > 1 and self.focus_exchange == "red":
             self.engine.focus_counts_peers(*self.plan.focus_share, stream=stream)
         else:
             self.engine.focus_counts(*self.plan.focus_share, stream=stream)
 
-    def exchange_focus(self) -> None:
-        """SUM the integer focus counts over ranks, then finish locally."""
-        if self.world > 1:
-            if self.fused:
-                self._sync_barrier()  # all ranks' counts are in every W
-            else:
-                dist.all_reduce(self.engine.full_W(), op=dist.ReduceOp.SUM, group=self.group)
-        self.engine.focus_finish()
+    def exchange_focus(self, stream=None) -> None:
+        """Combine the integer focus counts of the ranks and finish U / W."""
+        if self.world == 1:
+            self.engine.focus_finish(stream=stream)
+        elif self.focus_exchange == "peer":
+            self._sync_barrier(stream)  # every rank's counts are in its W
+            self.engine.focus_finish_peers(self.rank, self.world, u_all=True, stream=stream)
+            self._sync_barrier(stream)  # every W (and U) finished everywhere
+        elif self.focus_exchange == "red":
+            self._sync_barrier(stream)  # all ranks' counts are in every W
+            self.engine.focus_finish(stream=stream)
+        else:
+            self._before_collective(stream)
+            dist.all_reduce(self.engine.full_W(), op=dist.ReduceOp.SUM, group=self.group)
+            self._after_collective(stream)
+            self.engine.focus_finish(stream=stream)
 
-    def reduce_cohesion(self) -> None:
+    def reduce_cohesion(self, stream=None) -> None:
         """SUM of the per-rank C shares (disjoint supports: exact)."""
         if self.world > 1:
             e = self.engine
+            self._before_collective(stream)
             dist.all_reduce(e.row_block_C(0, e.n), op=dist.ReduceOp.SUM, group=self.group)
+            self._after_collective(stream)
 
-    def gather_cohesion(self) -> None:
+    def gather_cohesion(self, stream=None) -> None:
         if self.world == 1:
             return
+        self._before_collective(stream)
+        self._gather_cohesion()
+        self._after_collective(stream)
+
+    def _gather_cohesion(self) -> None:
         e, p = self.engine, self.plan
         r0, r1 = p.cohesion_rows
         if self._even:
@@ -176,32 +228,37 @@ class ShardedRunner:
         """This rank's share of pass 2."""
         e = self.engine
         self._fused_c = False
-        if self.fused:
-            self._fused_c = e.cohesion_share_peers(self.rank, self.world, stream=stream)
-            if self._fused_c:
+        if self.world > 1 and self.cohesion_exchange == "peer":
+            # The pair-kernel choice is made per rank (it depends on D and on
+            # the device's SM count / env knobs): run fused only if every rank
+            # can, decided BEFORE any rank stores into its peers' C.
+            if self._agree(e.pair_kernel_preferred()):
+                self._fused_c = e.cohesion_share_peers(self.rank, self.world, stream=stream)
+                if not self._fused_c:
+                    raise RuntimeError("fused pass 2 refused after all ranks agreed on the pair kernel")
                 return
         if getattr(e, "cohesion_share", None) is not None:
             e.cohesion_share(self.rank, self.world, stream=stream)
         else:
             e.cohesion(*self.plan.cohesion_rows, stream=stream)
 
-    def assemble_cohesion(self) -> None:
+    def assemble_cohesion(self, stream=None) -> None:
         """Full C on every rank: a barrier after the fused pass 2, else the
         SUM all-reduce of the shares (or the row-band all-gather for engines
         without cohesion_share)."""
         if self.world == 1:
             return
-        # every rank took the same branch: the pair-kernel choice depends on D only
+        # every rank took the same branch (agreed in cohesion())
         if self._fused_c:
-            self._sync_barrier()
+            self._sync_barrier(stream)
         elif getattr(self.engine, "cohesion_share", None) is not None:
-            self.reduce_cohesion()
+            self.reduce_cohesion(stream)
         else:
-            self.gather_cohesion()
+            self.gather_cohesion(stream)
 
     def step(self, D, stream=None) -> None:
         self.load(D, stream)
         self.focus(stream=stream)
-        self.exchange_focus()
+        self.exchange_focus(stream)
         self.cohesion(stream=stream)
-        self.assemble_cohesion()
+        self.assemble_cohesion(stream)

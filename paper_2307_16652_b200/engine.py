@@ -44,7 +44,8 @@ class Engine:
     """
 
     def __init__(self, n: int, algorithm: str = "pairwise", device: int | None = None,
-                 force_exact: bool = False, skip_validation: bool = False, policy: str = "strict"):
+                 force_exact: bool = False, skip_validation: bool = False, policy: str = "strict",
+                 accurate: bool = False):
         self.lib = _lib.load()
         if device is None:
             device = torch.cuda.current_device()
@@ -53,7 +54,7 @@ class Engine:
         self.algorithm = algorithm
         alg = {"pairwise": _lib.PAIRWISE, "triplet": _lib.TRIPLET}[algorithm]
         flags = (_lib.FLAG_FORCE_EXACT if force_exact else 0) | (
-            _lib.FLAG_SKIP_VALIDATION if skip_validation else 0)
+            _lib.FLAG_SKIP_VALIDATION if skip_validation else 0) | (_lib.FLAG_ACCURATE if accurate else 0)
         pol = {"strict": _lib.STRICT, "split": _lib.INCLUSIVE_SPLIT}[policy]
         opts = _lib.make_opts(algorithm=alg, policy=pol, device=self.device, flags=flags)
         self._plan = C.c_void_p()
@@ -89,6 +90,17 @@ class Engine:
     def C(self) -> torch.Tensor:
         return self._view(self._ptrs[2], "<f4", torch.float32)
 
+    @property
+    def C64(self) -> torch.Tensor:
+        """Accurate mode's double sums (n x n), after an accurate cohesion call."""
+        b = _lib.Buffers()
+        _raise_for(self.lib.pald_gpu_plan_buffers(self._plan, C.byref(b)))
+        if not b.C64:
+            raise RuntimeError("no accurate-mode cohesion has run on this engine")
+        n, ld = self.n, self.ld
+        v = _DeviceView(b.C64, (n, n), "<f8", (ld * 8, 8), self)
+        return torch.as_tensor(v, device=f"cuda:{self.device}")
+
     def full_U(self) -> torch.Tensor:
         """The whole ld-strided U buffer as a flat tensor (for collectives)."""
         v = _DeviceView(self._ptrs[0], (self.n * self.ld,), "<i4", (4,), self)
@@ -103,10 +115,13 @@ class Engine:
         return torch.as_tensor(v, device=f"cuda:{self.device}")
 
     # -- steps -----------------------------------------------------------
-    @staticmethod
-    def _stream(stream) -> int:
+    def _stream(self, stream) -> int:
+        """The raw handle of `stream`, or of the current stream OF THIS
+        ENGINE'S DEVICE (the C ABI switches to the plan's device)."""
         if stream is None:
-            stream = torch.cuda.current_stream()
+            stream = torch.cuda.current_stream(self.device)
+        elif stream.device.index is not None and stream.device.index != self.device:
+            raise ValueError(f"stream of {stream.device} used with an engine on cuda:{self.device}")
         return stream.cuda_stream
 
     def load(self, D: torch.Tensor, stream=None) -> None:
@@ -166,6 +181,28 @@ class Engine:
             C.memmove(ca[q].bytes, c_handles[q], 64)
         _raise_for(self.lib.pald_gpu_plan_attach_peers(self._plan, world, rank, wa, ca))
 
+    def export_u(self) -> bytes:
+        """CUDA IPC handle of this plan's U (peer-pull finish, ABI v4)."""
+        u = _lib.IpcHandle()
+        _raise_for(self.lib.pald_gpu_plan_export_u(self._plan, C.byref(u)))
+        return bytes(u.bytes)
+
+    def attach_peers_u(self, u_handles: list[bytes]) -> None:
+        arr = (_lib.IpcHandle * len(u_handles))()
+        for q, h in enumerate(u_handles):
+            C.memmove(arr[q].bytes, h, 64)
+        _raise_for(self.lib.pald_gpu_plan_attach_peers_u(self._plan, arr))
+
+    def focus_finish_peers(self, part: int, parts: int, u_all: bool = False, stream=None) -> None:
+        """Peer-pull exchange of pass 1: finish share `part` of `parts` of the
+        tiles from every rank's counts, storing W (and U if u_all) everywhere."""
+        _raise_for(self.lib.pald_gpu_plan_focus_finish_peers(self._plan, part, parts, int(u_all),
+                                                             self._stream(stream)))
+
+    def pair_kernel_preferred(self) -> bool:
+        """Whether a full-range cohesion of the loaded D would run the pair kernel."""
+        return bool(self._info().pair_kernel_preferred)
+
     def detach_peers(self) -> None:
         _raise_for(self.lib.pald_gpu_plan_detach_peers(self._plan))
 
@@ -183,15 +220,19 @@ class Engine:
         _raise_for(rc)
         return True
 
-    def info(self) -> dict:
-        """Pass-2 kernel of the last cohesion call and the tie statistics."""
+    def _info(self):
         i = _lib.PlanInfo()
         i.struct_size = C.sizeof(_lib.PlanInfo)
         _raise_for(self.lib.pald_gpu_plan_get_info(self._plan, C.byref(i)))
+        return i
+
+    def info(self) -> dict:
+        """Pass-2 kernel of the last cohesion call and the tie statistics."""
+        i = self._info()
         return {"cohesion_kernel": _lib.KERNEL_NAMES.get(i.cohesion_kernel, str(i.cohesion_kernel)),
                 "exact_path": bool(i.exact_path), "pair_kernel_ready": bool(i.pair_kernel_ready),
                 "exact_step_share": i.exact_step_share, "launches": int(i.launches),
-                "rank_codes": bool(i.rank_codes)}
+                "rank_codes": bool(i.rank_codes), "pair_kernel_preferred": bool(i.pair_kernel_preferred)}
 
     def run(self, D: torch.Tensor, stream=None) -> None:
         self.load(D, stream)
@@ -247,27 +288,18 @@ class Engine:
             c.diagonal().copy_(diag)
         return c * (1.0 / float(self.n - 1))
 
-    def nearest_neighbors(self, focus: int, k: int, diag: torch.Tensor | None = None):
-        """analyze.hpp:62-75: top-k points by min(c'_fz, c'_zf), strongest
-        first, ties toward the smaller index (stable sort). Returns (z, strength)."""
-        from .api import ValidationError
-
-        if focus < 0 or focus >= self.n:
-            raise ValidationError("focus point out of range")
-        if k >= self.n:
-            raise ValidationError("k must be smaller than the point count")
-        scale = 1.0 / float(self.n - 1)
-        row = self.C[focus].double()
-        col = self.C[:, focus].double()
-        if diag is not None:
-            row[focus] = diag[focus]
-            col[focus] = diag[focus]
-        s = torch.minimum(row * scale, col * scale)
-        idx = torch.arange(self.n, device=s.device)
-        keep = idx != focus
-        s, idx = s[keep], idx[keep]
-        order = torch.sort(s, descending=True, stable=True).indices[:k]
-        return idx[order], s[order]
+    def nearest_neighbors(self, focus: int, k: int, diag: torch.Tensor | None = None, stream=None):
+        """analyze.hpp:60-75 on the device (pald_gpu_nearest_neighbors): top-k
+        points by min(c'_fz, c'_zf), strongest first, ties toward the smaller
+        index (stable sort). Returns (z int32, strength float64) tensors."""
+        dev = f"cuda:{self.device}"
+        kk = max(int(k), 0)
+        zs = torch.empty(max(kk, 1), dtype=torch.int32, device=dev)
+        sv = torch.empty(max(kk, 1), dtype=torch.float64, device=dev)
+        _raise_for(self.lib.pald_gpu_nearest_neighbors(
+            self._ptrs[2], self.ld, self.n, diag.data_ptr() if diag is not None else None, int(focus), int(k),
+            zs.data_ptr(), sv.data_ptr(), self._stream(stream)))
+        return zs[:kk], sv[:kk]
 
     @property
     def exact_path(self) -> bool:

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <random>
 #include <string>
@@ -167,8 +168,46 @@ static void gpu_tests() {
   }
 }
 
+// parallel_* over a device list (pald::gpu::ParallelPlan::devices, one C-ABI
+// call spanning the listed GPUs) == one device, bit for bit.
+static void device_list_tests(const std::vector<int>& devs) {
+  using pald::Policy;
+  for (std::size_t n : {std::size_t(130), std::size_t(1000), std::size_t(2304)}) {
+    for (bool ties : {false, true}) {
+      const auto d = random_d(n, 77 + n, ties);
+      pald::gpu::ParallelPlan plan;
+      plan.workers = 4;
+      plan.devices = devs;
+      const auto one = pald::gpu::blocked_pairwise<float>(d, 64);
+      const auto many = pald::gpu::parallel_pairwise<float>(d, 64, plan);
+      CHECK(one.focus.sizes == many.focus.sizes);
+      CHECK(one.cohesion.values == many.cohesion.values);
+      const auto t1 = pald::gpu::blocked_triplet<float>(d, 64, 64);
+      const auto tm = pald::gpu::parallel_triplet<float>(d, 64, 64, plan);
+      CHECK(t1.focus.sizes == tm.focus.sizes);
+      CHECK(t1.cohesion.values == tm.cohesion.values);
+      const auto s1 = pald::gpu::blocked_pairwise<float>(d, 64, Policy::InclusiveSplit);
+      const auto sm = pald::gpu::parallel_pairwise<float>(d, 64, plan, Policy::InclusiveSplit);
+      CHECK(s1.focus.sizes == sm.focus.sizes);
+      CHECK(s1.cohesion.values == sm.cohesion.values);
+    }
+  }
+  if (!failures) std::printf("device list ok (%zu devices)\n", devs.size());
+}
+
 int main(int argc, char** argv) {
   const bool cpu = argc > 1 && std::strcmp(argv[1], "--cpu-only") == 0;
+  if (argc > 2 && std::strcmp(argv[1], "--devices") == 0) {
+    std::vector<int> devs;
+    for (const char* p = argv[2]; *p;) {
+      devs.push_back(std::atoi(p));
+      while (*p && *p != ',') ++p;
+      if (*p == ',') ++p;
+    }
+    device_list_tests(devs);
+    std::printf("devices: %d failure(s)\n", failures);
+    return failures ? 1 : 0;
+  }
   cpu_only();
   if (!cpu) gpu_tests();
   std::printf("%s: %d failure(s)\n", cpu ? "cpu-only" : "full", failures);

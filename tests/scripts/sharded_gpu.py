@@ -30,11 +30,19 @@ def main():
     ref = Engine(n, alg)
     ref.run(D)
     eng = Engine(n, alg)
-    runner = ShardedRunner(eng, fused=(mode == "fused"))
-    if mode == "fused":
+    # mode: collectives | fused[:<pass-1 exchange>][:stream]
+    parts = mode.split(":")
+    fused = parts[0] == "fused"
+    fx = next((p for p in parts[1:] if p in ("peer", "red", "nccl")), None)
+    use_stream = "stream" in parts[1:]
+    runner = ShardedRunner(eng, fused=fused, focus_exchange=fx)
+    if fused:
         assert runner.fused, "peer mapping failed"
+    # a non-current stream: the runner must order its barriers and
+    # collectives after the work issued on it
+    stream = torch.cuda.Stream() if use_stream else None
     for _ in range(2):  # repeated steps reuse the plan
-        runner.step(D)
+        runner.step(D, stream=stream)
     torch.cuda.synchronize()
     ok_u = torch.equal(eng.U, ref.U)
     ok_c = torch.equal(eng.C.view(torch.int32), ref.C.view(torch.int32))
@@ -42,7 +50,7 @@ def main():
     dist.all_reduce(flags, op=dist.ReduceOp.MIN)
     if rank == 0:
         print("shares", runner.plan.focus_share, "kernel", eng.info()["cohesion_kernel"], "fused", runner.fused,
-              "fused_c", runner._fused_c, "ok", flags.tolist())
+              "fused_c", runner._fused_c, "focus_exchange", runner.focus_exchange, "ok", flags.tolist())
     dist.destroy_process_group()
     sys.exit(0 if flags.tolist() == [1, 1] else 1)
 

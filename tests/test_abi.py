@@ -51,10 +51,49 @@ def test_abi_version_and_opts_layout():
     from paper_2307_16652_b200 import _lib
 
     lib = _lib.load()
-    assert lib.pald_gpu_abi_version() == 3
+    assert lib.pald_gpu_abi_version() == 4
     o = _lib.make_opts()
-    assert o.struct_size == C.sizeof(_lib.Opts) == 48
+    # v3 prefix (48 bytes) + num_devices + devices[8] + two exchange fields
+    assert o.struct_size == C.sizeof(_lib.Opts) == 96  # 48 + 4 + 32 + 8, padded to 8
     assert o.block == o.block_focus == o.block_cohesion == 128 and o.device == -1
+    assert o.num_devices == 0 and o.exchange_focus == o.exchange_cohesion == _lib.EXCHANGE_AUTO
+    assert _lib.OPTS_V3_SIZE == 48
+    assert C.sizeof(_lib.Buffers) == 72 and C.sizeof(_lib.PlanInfo) == 40
+
+
+def test_v3_sized_options_are_accepted():
+    """A caller built against ABI v3 passes the 48-byte struct: it is read
+    as one device (argument errors still come back first, no GPU needed)."""
+    from paper_2307_16652_b200 import _lib
+
+    lib = _lib.load()
+    d = (C.c_float * 9)()
+    c = (C.c_float * 9)()
+    o = _lib.make_opts(block=0)
+    o.struct_size = _lib.OPTS_V3_SIZE
+    o.num_devices = 99  # beyond the v3 prefix: must be ignored
+    assert lib.pald_gpu_cohesion_f32(d, 3, C.byref(o), None, c, None) == _lib.ERR_VALIDATION
+    assert "block size" in _lib.last_error()
+
+
+def test_device_list_validation():
+    from paper_2307_16652_b200 import _lib
+
+    lib = _lib.load()
+    d = (C.c_float * 9)()
+    c = (C.c_float * 9)()
+    o = _lib.make_opts()
+    o.num_devices = 9
+    assert lib.pald_gpu_cohesion_f32(d, 3, C.byref(o), None, c, None) == _lib.ERR_VALIDATION
+    assert "num_devices" in _lib.last_error()
+    o = _lib.make_opts(exchange_focus=7)
+    assert lib.pald_gpu_cohesion_f32(d, 3, C.byref(o), None, c, None) == _lib.ERR_VALIDATION
+    o = _lib.make_opts(exchange_cohesion=_lib.EXCHANGE_RED)
+    assert lib.pald_gpu_cohesion_f32(d, 3, C.byref(o), None, c, None) == _lib.ERR_VALIDATION
+    assert "pass 1 only" in _lib.last_error()
+    o = _lib.make_opts(devices=[0, 64])  # not a visible device (none are, without a GPU)
+    assert lib.pald_gpu_cohesion_f32(d, 3, C.byref(o), None, c, None) == _lib.ERR_VALIDATION
+    assert "not a visible device" in _lib.last_error()
 
 
 def test_argument_validation_before_device_work():
@@ -86,5 +125,5 @@ def test_build_tracks_every_csrc_file():
     from paper_2307_16652_b200 import _build
 
     names = {p.name for p in _build.deps()}
-    for f in ("pald_gpu.cu", "pald_kernels.cuh", "pald_sym.cuh", "pald_internal.h", "pald_gpu.h"):
+    for f in ("pald_gpu.cu", "pald_kernels.cuh", "pald_sym.cuh", "pald_multi.cuh", "pald_internal.h", "pald_gpu.h"):
         assert f in names, f

@@ -59,15 +59,46 @@ def test_policy_and_block_errors_without_gpu():
     assert pg.to_string(pg.Policy.Strict) == "strict" and pg.to_string(pg.Policy.InclusiveSplit) == "split"
 
 
-def test_normalize_and_depths_semantics(oracle):
+def test_normalize_and_depths_semantics():
+    """The reference's precondition errors (reference.hpp:223-241) come
+    before any device work; the arithmetic runs on the GPU
+    (pald_gpu_normalize_f64 / pald_gpu_row_sums_f64) and is checked bit for
+    bit against the reference in tests/test_gpu_analyze.py."""
     n = 7
-    c = pg.CohesionMatrix(n, np.random.default_rng(0).random((n, n)), False)
-    ref = c.values.copy()
-    pg.normalize(c)
-    oracle.normalize(ref)
-    assert np.array_equal(c.values, ref) and c.normalized
+    vals = np.random.default_rng(0).random((n, n))
     with pytest.raises(pg.ValidationError, match="already normalized"):
-        pg.normalize(c)
-    assert np.array_equal(pg.local_depths(c).depths, oracle.local_depths(ref))
-    with pytest.raises(pg.ValidationError):
-        pg.local_depths(pg.CohesionMatrix(n, ref, False))
+        pg.normalize(pg.CohesionMatrix(n, vals.copy(), True))
+    with pytest.raises(pg.ValidationError, match="normalized"):
+        pg.local_depths(pg.CohesionMatrix(n, vals.copy(), False))
+
+
+@pytest.mark.parametrize("case", ["diag_after_offdiag", "offdiag_before_diag", "asym_then_negative", "nan", "neg_zero"])
+def test_distance_matrix_first_violation_like_reference(reference, case):
+    """The reference scans row by row (types.hpp:50-62): (x, x), then (x, y)
+    for y > x with positivity before symmetry. With several violations the
+    first in that order is reported, with the reference's exact message."""
+    n = 9
+    rng = np.random.default_rng(3)
+    d = rng.uniform(0.5, 2.0, (n, n))
+    d = np.triu(d, 1)
+    d = d + d.T
+    if case == "diag_after_offdiag":
+        d[5, 5] = 1.0
+        d[2, 7] = d[7, 2] = -1.5
+    elif case == "offdiag_before_diag":
+        d[4, 4] = 0.5
+        d[1, 8] = 0.25  # asymmetric at (1, 8)
+    elif case == "asym_then_negative":
+        d[6, 2] = 3.0  # lower entry differs: "not symmetric at (2,6)"
+        d[3, 8] = d[8, 3] = 0.0
+    elif case == "nan":
+        d[0, 4] = d[4, 0] = np.nan
+    else:
+        d[3, 3] = -0.0  # accepted: -0.0 == 0.0
+        d[2, 5] = d[5, 2] = -0.0
+    rc = reference.validate(d)
+    assert rc == 2
+    want = reference.lib.ref_last_error().decode()
+    with pytest.raises(pg.ValidationError) as ei:
+        pg.DistanceMatrix(n, d)
+    assert str(ei.value) == want

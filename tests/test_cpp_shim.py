@@ -27,6 +27,11 @@ def _build(tmp: Path, ref_types: bool) -> Path:
     return exe
 
 
+def build_shim_test(tmp: Path, ref_types: bool = False) -> Path:
+    """The shim test binary (tests/cpp/test_shim.cpp), for other test modules."""
+    return _build(tmp, ref_types)
+
+
 def test_shim_validation_cpu(tmp_path):
     exe = _build(tmp_path, False)
     out = subprocess.run([str(exe), "--cpu-only"], capture_output=True, text=True)

@@ -33,6 +33,10 @@ def _port():
     # n > 2048: pass 1 on rank codes (built on every rank), shares of its units
     (2, 2500, "pairwise", "rand", "collectives"), (3, 2500, "pairwise", "rand", "fused"),
     (2, 2500, "triplet", "rand", "fused"),
+    # per-pass transports (pass 1: peer-pull finish [default], count
+    # fan-out, NCCL/gloo all-reduce) and a non-current stream
+    (3, 1000, "pairwise", "rand", "fused:red"), (2, 2500, "pairwise", "rand", "fused:nccl"),
+    (3, 700, "triplet", "rand", "fused:peer:stream"), (2, 700, "pairwise", "ties", "collectives:stream"),
 ])
 def test_sharded_real_engine(world, n, alg, kind, mode):
     """mode "fused": pass-1 counts and pass-2 entries written into every
@@ -45,7 +49,7 @@ def test_sharded_real_engine(world, n, alg, kind, mode):
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     assert "ok [1, 1]" in out.stdout
-    if mode == "fused":
+    if mode.startswith("fused"):
         assert "fused True" in out.stdout
         if kind == "rand":
             assert "fused_c True" in out.stdout
