@@ -465,21 +465,25 @@ def e2e_sharded(engine, runner, D_dev, steps: int, warmup: int, rank: int):
 
 
 def secondary_configs(steps: int) -> dict:
-    """N=1: the other BASELINE.json configs (parity cases) timed device-resident."""
+    """N=1: the other BASELINE.json configs (parity cases) timed device-resident,
+    and the accurate-summation mode (PALD_GPU_FLAG_ACCURATE) on configs 5 and 3."""
     import torch
     from paper_2307_16652_b200.engine import Engine
 
     out = {}
     peak = issue_peak(measured_peaks())
-    for idx, alg in ((3, "pairwise"), (1, "pairwise"), (2, "triplet"), (4, "pairwise"), (4, "triplet")):
+    for idx, alg, acc in ((3, "pairwise", False), (1, "pairwise", False), (2, "triplet", False),
+                          (4, "pairwise", False), (4, "triplet", False), (3, "pairwise", True),
+                          (5, "pairwise", True)):
         D, cfg = make_input(idx, "cuda", 20230731)
         n = cfg.n
-        eng = Engine(n, alg)
+        eng = Engine(n, alg, accurate=acc)
         stream = torch.cuda.current_stream()
-        for _ in range(2):
+        reps = 1 if n > 16384 else steps
+        for _ in range(1 if n > 16384 else 2):
             eng.run(D)
         torch.cuda.synchronize()
-        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(reps)]
         for e in evs:
             e[0].record(stream)
             eng.load(D)
@@ -493,11 +497,11 @@ def secondary_configs(steps: int) -> dict:
         foc = statistics.mean(e[1].elapsed_time(e[2]) for e in evs) / 1e3
         coh = statistics.mean(e[2].elapsed_time(e[3]) for e in evs) / 1e3
         w = alg_ops_pairwise(n) if alg == "pairwise" else alg_ops_triplet(n)
-        out[f"{cfg.name}:{alg}"] = {
+        out[f"{cfg.name}:{alg}" + (":accurate" if acc else "")] = {
             "n": n, "algorithm": alg, "triplets_per_s": n ** 3 / step, "ms_per_step": step * 1e3,
             "focus_ms": foc * 1e3, "cohesion_ms": coh * 1e3,
             "issue_roofline_frac_step": w / (step * peak), "exact_path": eng.exact_path,
-            "cohesion_kernel": eng.info()["cohesion_kernel"],
+            "cohesion_kernel": eng.info()["cohesion_kernel"], "accurate": acc or alg == "triplet",
         }
         del eng, D
         torch.cuda.empty_cache()

@@ -297,14 +297,17 @@ int pald_gpu_plan_cohesion_share_peers(pald_gpu_plan* plan, uint64_t part, uint6
  * focus_counts_peers, every rank runs plain focus_counts (its share into
  * its OWN W), the ranks meet at a host barrier, and each rank finishes
  * share `part` of `parts` of the upper-triangular tiles: it sums the counts
- * of every rank's W (P2P loads), and stores U and W = 1/U into every
- * rank's buffers (P2P stores; U only into its own unless u_all). After a
- * second barrier every rank holds the full W (and U if u_all). Replaces
- * the SUM all-reduce of the counts + focus_finish. U peers come from
- * export_u / attach_peers_u (after attach_peers). */
+ * of every rank's W (P2P loads), and stores W = 1/U into every rank's
+ * buffer and U as u_mode says (P2P stores). After a
+ * second barrier every rank holds the full W. U goes to: u_mode 0 this
+ * rank only; 1 every rank; 2 the rank owning the entry's row in the
+ * tile-row band split (bands [nb*i/world, nb*(i+1)/world) of tile rows, the
+ * split the multi-device host call downloads U by). Replaces the SUM
+ * all-reduce of the counts + focus_finish. U peers come from export_u /
+ * attach_peers_u (after attach_peers). */
 int pald_gpu_plan_export_u(const pald_gpu_plan* plan, pald_gpu_ipc_handle* u);
 int pald_gpu_plan_attach_peers_u(pald_gpu_plan* plan, const pald_gpu_ipc_handle* u_handles);
-int pald_gpu_plan_focus_finish_peers(pald_gpu_plan* plan, uint64_t part, uint64_t parts, int u_all,
+int pald_gpu_plan_focus_finish_peers(pald_gpu_plan* plan, uint64_t part, uint64_t parts, int u_mode,
                                      void* stream);
 
 /* Number of pass-1 work units of the plan. */

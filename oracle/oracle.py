@@ -199,12 +199,9 @@ class Reference:
             "ref_fill_diagonal": (_i32, [_vp, _u64, _vp]),
             "ref_normalize_and_depths": (_i32, [_vp, _u64, _vp]),
             "ref_default_block_config": (_i32, [_u64, _u64, _vp]),
-            "ref_parallel_pairwise_prefix_f32": (_i32, [_vp, _u64, _u64, _i32, _u64, d, _vp, _vp]),
             "ref_read_distance_binary": (_i32, [C.c_char_p, _u64, C.POINTER(C.c_uint64), _vp]),
-            "ref_parallel_pairwise_blocks_f32": (_i32, [_vp, _u64, _u64, _i32, _u64, _u64, _u64, d,
-                                                        C.POINTER(C.c_uint64)]),
             "ref_points_to_distances": (_i32, [_vp, _u64, _u64, _vp]),
-            "ref_parallel_pairwise_blockpairs_f32": (_i32, [_vp, _u64, _u64, _i32, _vp, _vp, _u64, _vp]),
+            "ref_parallel_pairwise_blockpairs_f32": (_i32, [_vp, _u64, _u64, _i32, _vp, _vp, _u64, _vp, _i32, _i32]),
             "ref_pairwise_overhead_f32": (_i32, [_u64, _u64, d]),
             "ref_universal_threshold": (_i32, [_vp, _u64, d]),
             "ref_strong_ties": (_i32, [_vp, _u64, _vp, d, _u64, _vp, _vp, _vp, C.POINTER(C.c_uint64)]),
@@ -302,30 +299,6 @@ class Reference:
         self._check(self.lib.ref_default_block_config(element_bytes, cache_bytes, _ptr(out)))
         return tuple(int(v) for v in out)
 
-    def parallel_pairwise_prefix_f32(self, d32: np.ndarray, b: int, workers: int, x_limit: int,
-                                     want_outputs: bool = False):
-        """Timed bounded sample of parallel_pairwise<float>: x-blocks < x_limit."""
-        d32 = np.ascontiguousarray(d32, np.float32)
-        n = d32.shape[0]
-        secs = C.c_double(0.0)
-        u = np.empty((n, n), np.int32) if want_outputs else None
-        c = np.empty((n, n), np.float32) if want_outputs else None
-        self._check(self.lib.ref_parallel_pairwise_prefix_f32(
-            _ptr(d32), n, b, workers, x_limit, C.byref(secs),
-            _ptr(u) if want_outputs else None, _ptr(c) if want_outputs else None))
-        return secs.value, u, c
-
-
-    def parallel_pairwise_blocks_f32(self, d32: np.ndarray, b: int, workers: int, xb: int, yb0: int,
-                                     yb1: int):
-        """Timed bounded sample of parallel_pairwise<float> by whole block pairs
-        (x-block xb, y-blocks [yb0, yb1)): returns (seconds, pairs covered)."""
-        d32 = np.ascontiguousarray(d32, np.float32)
-        secs, pairs = C.c_double(0.0), C.c_uint64(0)
-        self._check(self.lib.ref_parallel_pairwise_blocks_f32(_ptr(d32), d32.shape[0], b, workers, xb, yb0,
-                                                             yb1, C.byref(secs), C.byref(pairs)))
-        return secs.value, int(pairs.value)
-
     def parallel_pairwise_blockpairs_f32(self, d32: np.ndarray, b: int, workers: int, pairs) -> np.ndarray:
         """Seconds of each listed block pair (xb, yb) of the parallel_pairwise<float>
         driver loop (ref_bridge.cpp ref_parallel_pairwise_blockpairs_f32)."""
@@ -334,7 +307,7 @@ class Reference:
         xb, yb = np.ascontiguousarray(pairs[:, 0]), np.ascontiguousarray(pairs[:, 1])
         out = np.zeros(len(pairs))
         self._check(self.lib.ref_parallel_pairwise_blockpairs_f32(_ptr(d32), d32.shape[0], b, workers, _ptr(xb),
-                                                                 _ptr(yb), len(pairs), _ptr(out)))
+                                                                 _ptr(yb), len(pairs), _ptr(out), 0, 0))
         return out
 
     def pairwise_overhead_f32(self, n: int, seed: int = 1) -> float:
@@ -382,14 +355,6 @@ class Reference:
         if rc:
             return rc, self.lib.ref_last_error().decode(), None, None
         return 0, "", zs[:k], sv[:k]
-
-
-def pair_work_fraction(n: int, x_limit: int) -> float:
-    """Fraction of the pairwise work (pairs x < y) with x < x_limit."""
-    x_limit = min(x_limit, n)
-    total = n * (n - 1) / 2
-    done = sum(n - 1 - x for x in range(x_limit))
-    return done / total
 
 
 def host_cores() -> int:

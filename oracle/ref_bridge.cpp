@@ -8,8 +8,9 @@
 //   * time the reference CPU implementation (bench.py cpu_baseline and
 //     --impl reference).
 // Every function forwards to the reference symbol it names; the only logic
-// here is marshalling (and, for the bounded timing sample, the x-block-row
-// prefix of the parallel_pairwise driver loop, parallel.hpp:178-215).
+// here is marshalling (and, for the bounded timing sample, the body of the
+// parallel_pairwise driver loop for a list of block pairs,
+// parallel.hpp:178-215, around the reference's own block functions).
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -199,119 +200,21 @@ int ref_default_block_config(uint64_t element_bytes, uint64_t cache_bytes, uint6
   });
 }
 
-// Bounded timing sample of parallel_pairwise<float>: the driver loop of
-// parallel.hpp:178-215 run for the x-blocks x0 < x_limit only, with the
-// reference's own ThreadPool, worker_range, pair_block_focus and
-// pair_block_cohesion. The caller extrapolates by the exact fraction of
-// pair work covered (the last x-block is cut at x_limit, so the sample
-// can be smaller than one block). D is the fp32 matrix (to_real already applied).
-// Returns the seconds of the timed loop in *seconds.
-int ref_parallel_pairwise_prefix_f32(const float* dd, uint64_t n, uint64_t b, int workers,
-                                     uint64_t x_limit, double* seconds, int32_t* u_out,
-                                     float* c_out) {
-  return guarded([&] {
-    using pald::detail::worker_range;
-    const int p = workers;
-    std::vector<float> c(n * n, 0.0f);
-    std::vector<int32_t> u(n * n, 0);
-    std::vector<std::vector<int32_t>> partial(p, std::vector<int32_t>(b * b));
-    std::vector<float> recip(b * b);
-    pald::ThreadPool pool(p);
-    const double t0 = pald::detail::PhaseClock::now();
-    for (uint64_t x0 = 0; x0 < n && x0 < x_limit; x0 += b) {
-      const uint64_t x1 = std::min<uint64_t>(std::min<uint64_t>(x0 + b, n), x_limit);
-      for (uint64_t y0 = x0; y0 < n; y0 += b) {
-        const uint64_t y1 = std::min<uint64_t>(y0 + b, n);
-        const uint64_t ys = y1 - y0, cells = (x1 - x0) * ys;
-        pool.run([&](int w) {
-          auto [z0, z1] = worker_range(n, p, w);
-          std::fill(partial[w].begin(), partial[w].begin() + cells, 0);
-          pald::detail::pair_block_focus(dd, n, pald::Policy::Strict, x0, x1, y0, y1, z0, z1,
-                                         partial[w].data());
-        });
-        for (int w = 1; w < p; ++w)
-          for (uint64_t i = 0; i < cells; ++i) partial[0][i] += partial[w][i];
-        for (uint64_t x = x0; x < x1; ++x) {
-          const uint64_t ybeg = (y0 > x + 1) ? y0 : x + 1;
-          for (uint64_t y = ybeg; y < y1; ++y) {
-            const int32_t cnt = partial[0][(x - x0) * ys + (y - y0)];
-            u[x * n + y] = u[y * n + x] = cnt;
-            recip[(x - x0) * ys + (y - y0)] = 1.0f / static_cast<float>(cnt);
-          }
-        }
-        pool.run([&](int w) {
-          auto [z0, z1] = worker_range(n, p, w);
-          pald::detail::pair_block_cohesion(dd, n, pald::Policy::Strict,
-                                            pald::UpdateStyle::Masked, x0, x1, y0, y1, z0, z1,
-                                            recip.data(), c.data());
-        });
-      }
-    }
-    *seconds = pald::detail::PhaseClock::now() - t0;
-    if (u_out) std::memcpy(u_out, u.data(), sizeof(int32_t) * n * n);
-    if (c_out) std::memcpy(c_out, c.data(), sizeof(float) * n * n);
-  });
-}
-
-// Bounded timing sample of parallel_pairwise<float> by whole BLOCK PAIRS:
-// the body of the driver loop of parallel.hpp:178-215 for x-block `xb` and
-// y-blocks [yb0, yb1) (yb0 >= xb), with the reference's own ThreadPool,
-// worker_range, pair_block_focus and pair_block_cohesion at their real
-// block size b. Full off-diagonal blocks (yb0 > xb) cost what every other
-// full block of the run costs, so the caller extrapolates by the pair count
-// (pairs in the sample / n(n-1)/2). *pairs_out = pairs covered.
-int ref_parallel_pairwise_blocks_f32(const float* dd, uint64_t n, uint64_t b, int workers, uint64_t xb,
-                                     uint64_t yb0, uint64_t yb1, double* seconds, uint64_t* pairs_out) {
-  return guarded([&] {
-    using pald::detail::worker_range;
-    const int p = workers;
-    std::vector<float> c(n * n, 0.0f);
-    std::vector<int32_t> u(n * n, 0);
-    std::vector<std::vector<int32_t>> partial(p, std::vector<int32_t>(b * b));
-    std::vector<float> recip(b * b);
-    pald::ThreadPool pool(p);
-    uint64_t pairs = 0;
-    const uint64_t x0 = xb * b, x1 = std::min<uint64_t>(x0 + b, n);
-    const double t0 = pald::detail::PhaseClock::now();
-    for (uint64_t y0 = std::max(yb0, xb) * b; y0 < n && y0 < yb1 * b; y0 += b) {
-      const uint64_t y1 = std::min<uint64_t>(y0 + b, n);
-      const uint64_t ys = y1 - y0, cells = (x1 - x0) * ys;
-      pool.run([&](int w) {
-        auto [z0, z1] = worker_range(n, p, w);
-        std::fill(partial[w].begin(), partial[w].begin() + cells, 0);
-        pald::detail::pair_block_focus(dd, n, pald::Policy::Strict, x0, x1, y0, y1, z0, z1, partial[w].data());
-      });
-      for (int w = 1; w < p; ++w)
-        for (uint64_t i = 0; i < cells; ++i) partial[0][i] += partial[w][i];
-      for (uint64_t x = x0; x < x1; ++x) {
-        const uint64_t ybeg = (y0 > x + 1) ? y0 : x + 1;
-        for (uint64_t y = ybeg; y < y1; ++y) {
-          const int32_t cnt = partial[0][(x - x0) * ys + (y - y0)];
-          u[x * n + y] = u[y * n + x] = cnt;
-          recip[(x - x0) * ys + (y - y0)] = 1.0f / static_cast<float>(cnt);
-          ++pairs;
-        }
-      }
-      pool.run([&](int w) {
-        auto [z0, z1] = worker_range(n, p, w);
-        pald::detail::pair_block_cohesion(dd, n, pald::Policy::Strict, pald::UpdateStyle::Masked, x0, x1, y0,
-                                          y1, z0, z1, recip.data(), c.data());
-      });
-    }
-    *seconds = pald::detail::PhaseClock::now() - t0;
-    *pairs_out = pairs;
-  });
-}
-
 // Timing sample of parallel_pairwise<float> by an explicit list of block
 // pairs (xb[i], yb[i]), xb <= yb: each is the body of the driver loop of
 // parallel.hpp:178-215 (pair_block_focus over the workers' z ranges, the
 // rank-order sum of the partial counts, U and the reciprocals, then
 // pair_block_cohesion), timed on its own into seconds[i]. The caller
 // extrapolates diagonal and off-diagonal block pairs separately.
+// policy / style arrive as run-time values exactly as in the real driver
+// (a compile-time Strict would let the compiler specialize the block
+// functions and time code the reference never runs).
 int ref_parallel_pairwise_blockpairs_f32(const float* dd, uint64_t n, uint64_t b, int workers, const uint32_t* xb,
-                                         const uint32_t* yb, uint64_t count, double* seconds) {
+                                         const uint32_t* yb, uint64_t count, double* seconds, int policy_i,
+                                         int style_i) {
   return guarded([&] {
+    const pald::Policy policy = pol(policy_i);
+    const pald::UpdateStyle style = style_i ? pald::UpdateStyle::Branchy : pald::UpdateStyle::Masked;
     using pald::detail::worker_range;
     const int p = workers;
     std::vector<float> c(n * n, 0.0f);
@@ -327,7 +230,7 @@ int ref_parallel_pairwise_blockpairs_f32(const float* dd, uint64_t n, uint64_t b
       pool.run([&](int w) {
         auto [z0, z1] = worker_range(n, p, w);
         std::fill(partial[w].begin(), partial[w].begin() + cells, 0);
-        pald::detail::pair_block_focus(dd, n, pald::Policy::Strict, x0, x1, y0, y1, z0, z1, partial[w].data());
+        pald::detail::pair_block_focus(dd, n, policy, x0, x1, y0, y1, z0, z1, partial[w].data());
       });
       for (int w = 1; w < p; ++w)
         for (uint64_t k = 0; k < cells; ++k) partial[0][k] += partial[w][k];
@@ -341,7 +244,7 @@ int ref_parallel_pairwise_blockpairs_f32(const float* dd, uint64_t n, uint64_t b
       }
       pool.run([&](int w) {
         auto [z0, z1] = worker_range(n, p, w);
-        pald::detail::pair_block_cohesion(dd, n, pald::Policy::Strict, pald::UpdateStyle::Masked, x0, x1, y0,
+        pald::detail::pair_block_cohesion(dd, n, policy, style, x0, x1, y0,
                                           y1, z0, z1, recip.data(), c.data());
       });
       seconds[i] = pald::detail::PhaseClock::now() - t0;

@@ -20,6 +20,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -294,6 +295,17 @@ int check_opts(const pald_gpu_opts* o) {
 
 }  // namespace
 
+#ifndef PALD_HOST_BANDS  // pass-2 bands of the host API (the last band's D2H is exposed)
+#define PALD_HOST_BANDS 16  // one raster group per band at n = 32768: e2e 3.790 -> 3.773 s
+#endif
+#define PALD_HOST_BANDS_MAX PALD_HOST_BANDS
+
+struct ItemList {
+  int4* items = nullptr;
+  int count = 0;
+  int grid = 0;
+};
+
 // ---------------------------------------------------------------------------
 struct pald_gpu_plan {
   int device = 0;
@@ -340,6 +352,7 @@ struct pald_gpu_plan {
   bool peer_u_mapped[kMaxPeers] = {};
   int peer_rank = -1;
   bool sym_ready = false;                // tie scan done for the loaded D
+  bool tri_marks = false;                // triplet: tie marks built with the rank codes
   bool loaded = false;
   bool exact = false;
   bool focus_dirty = false;
@@ -352,14 +365,24 @@ struct pald_gpu_plan {
   int sym_main_pairs = 0;        // pairs of the full-range pair launch (rest: tail tiles)
   // Triplet pass 2 with the last partial round of pairs split along k
   // (pald_sym.cuh SPLIT items + sym_combine_kernel); built on first use.
-  int4* split_items = nullptr;
-  int4* split_pairs = nullptr;
-  float* split_partial = nullptr;
-  int split_item_count = -1;     // -1: not built; 0: no split
-  int split_pair_count = 0;
+  // [0]: fp32 partial tiles; [1]: accurate mode (double partial tiles, the
+  // item list in per-CTA queues of k blocks)
+  struct SplitPlan {
+    int4* items = nullptr;
+    int4* pairs = nullptr;
+    void* partial = nullptr;
+    int item_count = -1;  // -1: not built; 0: no split
+    int pair_count = 0;
+  } split[2];
   // Accurate mode (PALD_GPU_FLAG_ACCURATE): double sums of the fp32 block
   // partials of pass 2 (n x ld doubles, allocated on first use).
   double* c64 = nullptr;
+  std::map<long long, ItemList> acc_lists;  // accurate-mode item lists per pair range
+  // One-shot host API (pald_gpu_cohesion_f32): its streams and events,
+  // created on first use and kept with the cached plan.
+  cudaStream_t os_s = nullptr, os_sc = nullptr, os_s2 = nullptr;
+  cudaEvent_t os_ev[4 + PALD_HOST_BANDS_MAX] = {};
+  std::vector<cudaEvent_t> band_ev;  // banded load: one per H2D band + the layout's
   uint64_t launches = 0;
 
   void close_peers() {
@@ -409,10 +432,18 @@ struct pald_gpu_plan {
     if (aux) cudaStreamDestroy(aux);
     if (ev_in) cudaEventDestroy(ev_in);
     if (ev_ranks) cudaEventDestroy(ev_ranks);
-    cudaFree(split_items);
-    cudaFree(split_pairs);
-    cudaFree(split_partial);
+    for (auto& sp : split) {
+      cudaFree(sp.items);
+      cudaFree(sp.pairs);
+      cudaFree(sp.partial);
+    }
     cudaFree(c64);
+    for (auto& kv : acc_lists) cudaFree(kv.second.items);
+    for (cudaStream_t st : {os_s, os_sc, os_s2})
+      if (st) cudaStreamDestroy(st);
+    for (cudaEvent_t e : os_ev)
+      if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : band_ev) cudaEventDestroy(e);
     cudaSetDevice(prev);
   }
 };
@@ -451,26 +482,40 @@ bool split_enabled() {
 }
 
 // Accurate mode: pass-2 terms per fp32 block partial (PALD_GPU_ACC_BLOCK,
-// default 256; rounded to whole k chunks of each kernel). A 2048-term fp32
-// chain alone drifts by ~3e-6 (the reference's own fp32 C at n = 2048);
-// 256-term blocks keep C within ~2e-7 of fp64 at n <= 32768 for ~2 % of
-// pass-2 time (one double read-modify-write of the thread's outputs per
-// block, outside the inner loop).
+// default 1024; rounded to whole k chunks of each kernel). Measured on
+// configs 3 / 2 (tools/acc_sweep.py, profiles/acc_sweep_r02.jsonl): 256-term
+// blocks 2.1e-7 / 3.9e-7 max rel_diff vs fp64, 1024 7.4e-7 / 1.4e-6, 4096
+// 2.8e-6 / 1.0e-5 (the plain fp32 chain: 5.4e-6 / 1.3e-5); the flush of a
+// block costs one reduction per output, outside the inner loop.
 int acc_block_terms() {
   static const int t = [] {
     const char* e = getenv("PALD_GPU_ACC_BLOCK");
-    const int v = e ? atoi(e) : 256;
-    return v >= kSymBK ? v : 256;
+    const int v = e ? atoi(e) : 1024;
+    return v >= kSymBK ? v : 1024;
   }();
   return t;
 }
-bool accurate(const pald_gpu_plan* p) { return (p->flags & PALD_GPU_FLAG_ACCURATE) != 0; }
+// Triplet C is a tolerance result (the reference's own fp32 triplet C
+// depends on b_cohesion), so the triplet always accumulates accurately: one
+// 4096-term fp32 chain already drifts by 1.3e-5 on config 2 (full matrix vs
+// parallel_triplet<double>). PALD_GPU_TRIPLET_FP32=1 restores the plain
+// fp32 chains (A/B).
+bool accurate(const pald_gpu_plan* p) {
+  static const bool tri_fp32 = [] {
+    const char* e = getenv("PALD_GPU_TRIPLET_FP32");
+    return e && atoi(e) != 0;
+  }();
+  return (p->flags & PALD_GPU_FLAG_ACCURATE) != 0 || (p->algorithm == PALD_GPU_TRIPLET && !tri_fp32);
+}
 
 int ensure_c64(pald_gpu_plan* p) {
   if (p->c64) return PALD_GPU_OK;
   PALD_CUDA(cudaMalloc(&p->c64, p->n * p->ld * sizeof(double)));
   return PALD_GPU_OK;
 }
+
+int acc_zero_rows(pald_gpu_plan* p, uint64_t r0, uint64_t r1, cudaStream_t s);
+int acc_round_rows(pald_gpu_plan* p, uint64_t r0, uint64_t r1, cudaStream_t s);
 
 size_t sym_mask_words(const pald_gpu_plan* p) { return p->nb * (p->nb + 1) / 2 * p->sym_nch; }
 
@@ -782,6 +827,31 @@ int ensure_aux(pald_gpu_plan* p) {
   return PALD_GPU_OK;
 }
 
+int ensure_oneshot(pald_gpu_plan* p) {
+  if (p->os_s) return PALD_GPU_OK;
+  PALD_CUDA(cudaStreamCreateWithFlags(&p->os_s, cudaStreamNonBlocking));
+  PALD_CUDA(cudaStreamCreateWithFlags(&p->os_sc, cudaStreamNonBlocking));
+  PALD_CUDA(cudaStreamCreateWithFlags(&p->os_s2, cudaStreamNonBlocking));
+  for (int i = 0; i < 4 + PALD_HOST_BANDS_MAX; ++i)
+    PALD_CUDA(cudaEventCreateWithFlags(&p->os_ev[i], i < 4 ? cudaEventDefault : cudaEventDisableTiming));
+  return PALD_GPU_OK;
+}
+
+// Tie marks (duplicate values per row, pald_sym.cuh) built with the rank
+// codes: the pairwise Strict pair kernel needs them to share its compares;
+// the triplet uses them to run the chunks inside the row / column tiles on
+// the fast steps (an unmarked k cannot meet the tie the nu() transforms
+// decide, in either pass).
+bool tie_marks_wanted(const pald_gpu_plan* p) {
+  static const int m = [] {
+    const char* e = getenv("PALD_GPU_TRI_MARKS");  // 0: triplet without marks (A/B)
+    return e ? atoi(e) : 1;
+  }();
+  if (!p->sym_masks || !sym_enabled()) return false;
+  if (p->algorithm == PALD_GPU_PAIRWISE) return p->policy == PALD_GPU_STRICT;
+  return m != 0;
+}
+
 int plan_load_impl(pald_gpu_plan* p, const float* dD, uint64_t ldd, cudaStream_t s) {
   const int n = (int)p->n;
   Stats init{};
@@ -797,8 +867,8 @@ int plan_load_impl(pald_gpu_plan* p, const float* dD, uint64_t ldd, cudaStream_t
   // range check: positive floats order as their bits, and the scaling of the
   // fast layout is exact). The bins kernel also marks the pair kernel's ties.
   const bool ranks = rank_wanted(p);
-  const bool mark = ranks && p->sym_masks && p->algorithm == PALD_GPU_PAIRWISE && p->policy == PALD_GPU_STRICT &&
-                    sym_enabled();
+  const bool mark = ranks && tie_marks_wanted(p);
+  p->tri_marks = false;
   if (ranks) {
     if ((rc = ensure_aux(p))) return rc;
     PALD_CUDA(cudaEventRecord(p->ev_in, s));  // D is ready in stream order of s
@@ -839,6 +909,7 @@ int plan_load_impl(pald_gpu_plan* p, const float* dD, uint64_t ldd, cudaStream_t
   // duplicate scan of the columns of D (marks of the tile-pair kernel) is
   // skipped where the pair kernel cannot win even tie-free.
   if (fast && p->algorithm == PALD_GPU_TRIPLET && sym_enabled() && sym_wins(p, 0.0)) p->sym_ready = true;
+  p->tri_marks = mark && p->algorithm == PALD_GPU_TRIPLET;
   // (a cached plan made for a strict call keeps its masks when reused for
   // InclusiveSplit: the pair kernel is strict-only)
   const bool tie_scan = fast && p->sym_masks && p->algorithm == PALD_GPU_PAIRWISE && p->policy == PALD_GPU_STRICT &&
@@ -972,6 +1043,11 @@ int launch_focus_range(pald_gpu_plan* p, long long ub, long long ue, const int2*
   if (p->rank_ready) {  // rank-coded packed compares (exact for both layouts)
     KernelArgs ar = a;
     ar.d = p->rank_a;
+    if (tri && p->tri_marks) {
+      ar.tie_masks = p->sym_masks;
+      ar.tie_tile_flags = p->sym_tile_flags;
+      ar.tie_nch = p->sym_nch;
+    }
     const CUtensorMap &ra = p->tm_ra, &rb = p->tm_rb;
     if (peers)
       rc = tri     ? launch_tile<0, true, true, true, false, true, false, kTile, false, true, true>(ra, rb, mw, ar, grid, s)
@@ -1010,7 +1086,7 @@ int plan_focus_finish_impl(pald_gpu_plan* p, cudaStream_t s) {
   if (!p->loaded) return set_error(PALD_GPU_ERR_VALIDATION, "plan has no distances loaded");
   const uint64_t tiles = p->nb * (p->nb + 1) / 2;
   focus_finish_kernel<false><<<(unsigned)(tiles * 4), 256, 0, s>>>(p->u, p->w, (int)p->n, (int)p->ld, (int)p->nb, 0,
-                                                                  FinishPeers{});
+                                                                  FinishPeers{});  // (u_mode unused)
   PALD_CUDA(cudaGetLastError());
   ++p->launches;
   return PALD_GPU_OK;
@@ -1093,6 +1169,36 @@ int launch_tail(pald_gpu_plan* p, const int2* list, int count, cudaStream_t s) {
   return p->tail_tile == 32 ? launch_cohesion_list<32>(p, list, count, s) : launch_cohesion_list<64>(p, list, count, s);
 }
 
+// Accurate mode: pairs [t0, t1) of the grouped order as k-block items, in
+// the CTA assignment of the whole-pair kernel (CTA g: pairs t0 + g, + G, ...)
+// so each pair stays on one CTA, its blocks consecutive; cached per range.
+int acc_items(pald_gpu_plan* p, int t0, int t1, const ItemList** out) {
+  const long long key = ((long long)t0 << 32) | (unsigned)t1;
+  auto it = p->acc_lists.find(key);
+  if (it == p->acc_lists.end()) {
+    const int G = std::min(t1 - t0, p->sms), nch = p->sym_nch, ac = std::max(1, acc_block_terms() / kSymBK);
+    std::vector<std::vector<int4>> queue(G);
+    for (int i = t0; i < t1; ++i) {
+      const int2 pr = p->pair_order[i];
+      for (int cb = 0; cb < nch; cb += ac)
+        queue[(i - t0) % G].push_back(make_int4(pr.x, pr.y, cb | (std::min(nch, cb + ac) << 15), -1));
+    }
+    size_t R = 0;
+    for (auto& q : queue) R = std::max(R, q.size());
+    std::vector<int4> items(R * G, make_int4(0, 0, 0, -1));  // empty padding items
+    for (int g = 0; g < G; ++g)
+      for (size_t r = 0; r < queue[g].size(); ++r) items[r * G + g] = queue[g][r];
+    ItemList il;
+    PALD_CUDA(cudaMalloc(&il.items, items.size() * sizeof(int4)));
+    PALD_CUDA(cudaMemcpy(il.items, items.data(), items.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    il.count = (int)items.size();
+    il.grid = G;
+    it = p->acc_lists.emplace(key, il).first;
+  }
+  *out = &it->second;
+  return PALD_GPU_OK;
+}
+
 int launch_sym(pald_gpu_plan* p, int t0, int t1, cudaStream_t s, bool peers = false,
                bool round_sync = true) {
   if (t1 <= t0) return PALD_GPU_OK;
@@ -1106,13 +1212,11 @@ int launch_sym(pald_gpu_plan* p, int t0, int t1, cudaStream_t s, bool peers = fa
     PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
     PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
     PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
-    PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<false, false, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
-    PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<true, false, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
-    PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<false, true, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
-    PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<true, true, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
+    PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<false, false, false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
+    PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<true, false, false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
     attr_done[p->device & 63] = true;
   }
-  const int grid = std::min(t1 - t0, p->sms);
+  int grid = std::min(t1 - t0, p->sms);
   // Optional round barrier (cooperative launch: all CTAs co-resident, one
   // per SM). It keeps the CTAs of a round at the same k, which cuts the
   // kernel's DRAM reads 7x (1.39 -> 0.20 TB at n = 32768, L2 hit 42 -> 85 %)
@@ -1135,11 +1239,23 @@ int launch_sym(pald_gpu_plan* p, int t0, int t1, cudaStream_t s, bool peers = fa
             sync ? p->round_bar : nullptr};
   a.c64 = p->c64;
   a.acc_chunks = std::max(1, acc_block_terms() / kSymBK);
+  a.tri_marks = p->tri_marks ? 1 : 0;
   const bool tri = p->algorithm == PALD_GPU_TRIPLET;
-  auto k = acc ? (peers ? (tri ? pald_sym_cohesion_kernel<true, true, false, false, true>
-                               : pald_sym_cohesion_kernel<false, true, false, false, true>)
-                        : (tri ? pald_sym_cohesion_kernel<true, false, false, false, true>
-                               : pald_sym_cohesion_kernel<false, false, false, false, true>))
+  if (acc) {
+    // accurate mode: the k blocks of the pairs [t0, t1) as an explicit item
+    // list (the lean SPLIT-form kernel); the kernel only adds into the
+    // double sums, so PEERS stores are the rounding pass's job
+    const ItemList* il = nullptr;
+    int rc = acc_items(p, t0, t1, &il);
+    if (rc) return rc;
+    a.items = il->items;
+    a.tile_begin = 0;
+    a.tile_end = il->count;
+    grid = il->grid;
+  }
+  (void)peers;
+  auto k = acc ? (tri ? pald_sym_cohesion_kernel<true, false, false, true, true>
+                      : pald_sym_cohesion_kernel<false, false, false, true, true>)
            : sync ? (peers ? (tri ? pald_sym_cohesion_kernel<true, true, true> : pald_sym_cohesion_kernel<false, true, true>)
                         : (tri ? pald_sym_cohesion_kernel<true, false, true> : pald_sym_cohesion_kernel<false, false, true>))
                 : (peers ? (tri ? pald_sym_cohesion_kernel<true, true> : pald_sym_cohesion_kernel<false, true>)
@@ -1163,8 +1279,13 @@ int launch_sym(pald_gpu_plan* p, int t0, int t1, cudaStream_t s, bool peers = fa
 // depends on its block size), so the pairs of the last partial round of the
 // full-range pair launch can be split along k into f parts whose partial
 // tiles are summed in a fixed order: ceil(L f / G) / f rounds instead of 1.
-int build_split(pald_gpu_plan* p) {
-  p->split_item_count = 0;
+// Items: (tile row, tile col, cb | ce << 15, slot); CTA g runs items g,
+// g + G, ... In accurate mode every whole pair and every split part is a run
+// of k blocks (acc_chunks chunks) on one CTA, all added into the double sums
+// (order-independent), the queues padded with empty items.
+int build_split(pald_gpu_plan* p, bool acc) {
+  auto& sp = p->split[acc ? 1 : 0];
+  sp.item_count = 0;
   const std::vector<int2>& order = p->pair_order;
   const int G = p->sms, pairs = (int)order.size(), L = pairs % G;
   if (pairs <= G || L == 0) return PALD_GPU_OK;
@@ -1179,50 +1300,83 @@ int build_split(pald_gpu_plan* p) {
   }
   if (best > 0.9) return PALD_GPU_OK;
   const int f = best_f, nch = p->sym_nch;
-  std::vector<int4> items;
-  std::vector<int4> sp;
-  for (int i = 0; i < pairs - L; ++i) items.push_back(make_int4(order[i].x, order[i].y, nch << 16, -1));
+  auto z = [](int cb, int ce, bool, bool) { return (int)((uint32_t)cb | ((uint32_t)ce << 15)); };
+  std::vector<int4> items, prs;
   for (int j = 0; j < L; ++j) {
     const int2 pr = order[pairs - L + j];
-    sp.push_back(make_int4(pr.x, pr.y, j * f, f));
-    for (int q = 0; q < f; ++q) {
-      const int cb = nch * q / f, ce = nch * (q + 1) / f;
-      items.push_back(make_int4(pr.x, pr.y, cb | (ce << 16), j * f + q));
-    }
+    prs.push_back(make_int4(pr.x, pr.y, j * f, f));
   }
-  PALD_CUDA(cudaMalloc(&p->split_items, items.size() * sizeof(int4)));
-  PALD_CUDA(cudaMemcpy(p->split_items, items.data(), items.size() * sizeof(int4), cudaMemcpyHostToDevice));
-  PALD_CUDA(cudaMalloc(&p->split_pairs, sp.size() * sizeof(int4)));
-  PALD_CUDA(cudaMemcpy(p->split_pairs, sp.data(), sp.size() * sizeof(int4), cudaMemcpyHostToDevice));
-  PALD_CUDA(cudaMalloc(&p->split_partial, (size_t)L * f * 2 * kTile * kTile * sizeof(float)));
-  p->split_item_count = (int)items.size();
-  p->split_pair_count = L;
+  if (!acc) {
+    for (int i = 0; i < pairs - L; ++i) items.push_back(make_int4(order[i].x, order[i].y, z(0, nch, true, true), -1));
+    for (int j = 0; j < L; ++j)
+      for (int q = 0; q < f; ++q)
+        items.push_back(make_int4(prs[j].x, prs[j].y, z(nch * q / f, nch * (q + 1) / f, q == 0, false), j * f + q));
+  } else {
+    const int ac = std::max(1, acc_block_terms() / kSymBK);
+    std::vector<std::vector<int4>> queue(G);
+    for (int i = 0; i < pairs - L; ++i)  // whole pairs: CTA i % G, as the implicit order
+      for (int cb = 0; cb < nch; cb += ac)
+        queue[i % G].push_back(make_int4(order[i].x, order[i].y, z(cb, std::min(nch, cb + ac), cb == 0,
+                                                                     cb + ac >= nch), -1));
+    for (int t = 0; t < L * f; ++t) {  // split parts: CTA t % G
+      const int j = t / f, q = t % f, pb = nch * q / f, pe = nch * (q + 1) / f;
+      for (int cb = pb; cb < pe; cb += ac)
+        queue[t % G].push_back(make_int4(prs[j].x, prs[j].y, z(cb, std::min(pe, cb + ac), cb == pb, false), t));
+    }
+    size_t R = 0;
+    for (auto& qu : queue) R = std::max(R, qu.size());
+    items.assign(R * G, make_int4(0, 0, 0, -1));  // empty padding items
+    for (int g = 0; g < G; ++g)
+      for (size_t r = 0; r < queue[g].size(); ++r) items[r * G + g] = queue[g][r];
+  }
+  PALD_CUDA(cudaMalloc(&sp.items, items.size() * sizeof(int4)));
+  PALD_CUDA(cudaMemcpy(sp.items, items.data(), items.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  PALD_CUDA(cudaMalloc(&sp.pairs, prs.size() * sizeof(int4)));
+  PALD_CUDA(cudaMemcpy(sp.pairs, prs.data(), prs.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  if (!acc)  // accurate mode: the parts add straight into the double sums
+    PALD_CUDA(cudaMalloc(&sp.partial, (size_t)L * f * 2 * kTile * kTile * sizeof(float)));
+  sp.item_count = (int)items.size();
+  sp.pair_count = L;
   return PALD_GPU_OK;
 }
 
 // Full-range triplet pass 2 through the split items; false if no split.
 int launch_sym_split(pald_gpu_plan* p, cudaStream_t s, bool* used) {
   *used = false;
-  if (p->split_item_count < 0) {
-    const int rc = build_split(p);
+  const bool acc = accurate(p);
+  auto& sp = p->split[acc ? 1 : 0];
+  if (sp.item_count < 0) {
+    const int rc = build_split(p, acc);
     if (rc) return rc;
   }
-  if (p->split_item_count == 0) return PALD_GPU_OK;
+  if (sp.item_count == 0) return PALD_GPU_OK;
   static bool attr_done[64] = {};
-  auto k = pald_sym_cohesion_kernel<true, false, false, true>;
+  auto k = acc ? pald_sym_cohesion_kernel<true, false, false, true, true> : pald_sym_cohesion_kernel<true, false, false, true>;
   if (!attr_done[p->device & 63]) {
-    PALD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
+    PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<true, false, false, true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
+    PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<true, false, false, true, true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
     attr_done[p->device & 63] = true;
   }
+  int rc;
+  if (acc && (rc = acc_zero_rows(p, 0, p->n, s))) return rc;
   SymArgs a{p->ds, p->c, p->focus_tiles, p->sym_masks, p->sym_tile_flags, (int)p->n, (int)p->ld, (int)p->nb,
-            p->sym_nch, 0, p->split_item_count, p->peer_c, nullptr, p->split_items, p->split_partial};
-  const int grid = std::min(p->split_item_count, p->sms);
+            p->sym_nch, 0, sp.item_count, p->peer_c, nullptr, sp.items,
+            acc ? nullptr : static_cast<float*>(sp.partial), p->c64, std::max(1, acc_block_terms() / kSymBK),
+            p->tri_marks ? 1 : 0};
+  const int grid = std::min(sp.item_count, p->sms);
   k<<<grid, kThreads, kSymSmem, s>>>(p->tm_d32, p->tm_dnu32, p->tm_w32, a);
   PALD_CUDA(cudaGetLastError());
-  sym_combine_kernel<<<dim3((unsigned)p->split_pair_count, 2, kTile / 8), 256, 0, s>>>(
-      p->split_pairs, p->split_partial, p->c, (int)p->n, (int)p->ld);
-  PALD_CUDA(cudaGetLastError());
-  p->launches += 2;
+  if (acc) {  // every item added into the double sums: round them all
+    if ((rc = acc_round_rows(p, 0, p->n, s))) return rc;
+  } else {
+    sym_combine_kernel<<<dim3((unsigned)sp.pair_count, 2, kTile / 8), 256, 0, s>>>(
+        sp.pairs, static_cast<const float*>(sp.partial), p->c, (int)p->n, (int)p->ld);
+    PALD_CUDA(cudaGetLastError());
+    ++p->launches;
+  }
+  ++p->launches;
   *used = true;
   return PALD_GPU_OK;
 }
@@ -1245,18 +1399,63 @@ bool sym_wins(const pald_gpu_plan* p, double marked) {
 // the one-sided kernel).
 bool sym_preferred(const pald_gpu_plan* p) { return p->policy == PALD_GPU_STRICT && sym_wins(p, p->sym_marked); }
 
+// Accurate mode around a pass-2 launch: the double sums are zeroed before
+// (the kernels add their k-block partials with red.global.add.f64) and
+// rounded to the fp32 C after.
+int acc_zero_rows(pald_gpu_plan* p, uint64_t r0, uint64_t r1, cudaStream_t s) {
+  int rc = ensure_c64(p);
+  if (rc) return rc;
+  if (r1 > r0) PALD_CUDA(cudaMemsetAsync(p->c64 + r0 * p->ld, 0, (r1 - r0) * p->ld * sizeof(double), s));
+  return PALD_GPU_OK;
+}
+int acc_round_rows(pald_gpu_plan* p, uint64_t r0, uint64_t r1, cudaStream_t s) {
+  if (r1 <= r0) return PALD_GPU_OK;
+  acc_round_rows_kernel<<<(unsigned)std::min<uint64_t>(r1 - r0, (uint64_t)p->sms * 8), 256, 0, s>>>(
+      p->c64, p->c, (int)p->n, (int)p->ld, (int)r0, (int)r1, p->algorithm == PALD_GPU_TRIPLET ? 1 : 0);
+  PALD_CUDA(cudaGetLastError());
+  ++p->launches;
+  return PALD_GPU_OK;
+}
+// Pairs [t0, t1) of the grouped pair order, into every buffer of `out`.
+int acc_round_pairs(pald_gpu_plan* p, int t0, int t1, const PeerBufs& out, cudaStream_t s) {
+  if (t1 <= t0) return PALD_GPU_OK;
+  acc_round_pairs_kernel<<<dim3((unsigned)(t1 - t0), 2), 256, 0, s>>>(p->focus_tiles, t0, p->c64, out, (int)p->n,
+                                                                       (int)p->ld, p->algorithm == PALD_GPU_TRIPLET ? 1 : 0);
+  PALD_CUDA(cudaGetLastError());
+  ++p->launches;
+  return PALD_GPU_OK;
+}
+PeerBufs own_c(pald_gpu_plan* p) {
+  PeerBufs b{};
+  b.ptr[0] = p->c;
+  b.count = 1;
+  return b;
+}
+
+int plan_cohesion_core(pald_gpu_plan* p, uint64_t row0, uint64_t row1, cudaStream_t s);
+
 int plan_cohesion_impl(pald_gpu_plan* p, uint64_t row0, uint64_t row1, cudaStream_t s) {
   if (!p->loaded) return set_error(PALD_GPU_ERR_VALIDATION, "plan has no distances loaded");
   row1 = std::min(row1, p->n);
   if (row0 >= row1) return PALD_GPU_OK;
   if (row0 % kTile != 0 || (row1 % kTile != 0 && row1 != p->n))
     return set_error(PALD_GPU_ERR_VALIDATION, "cohesion row range must be aligned to %d", kTile);
+  const bool acc = accurate(p);
+  int rc;
+  if (acc && (rc = acc_zero_rows(p, row0, row1, s))) return rc;
+  if ((rc = plan_cohesion_core(p, row0, row1, s))) return rc;
+  return acc ? acc_round_rows(p, row0, row1, s) : PALD_GPU_OK;
+}
+
+// Pass 2 over C rows [row0, row1): the pair kernel for the full range when
+// it wins, the one-sided kernel otherwise.
+int plan_cohesion_core(pald_gpu_plan* p, uint64_t row0, uint64_t row1, cudaStream_t s) {
   // Less than one wave of 128-wide tiles: use 64-wide tiles (4x the tiles,
   // 2 CTAs per SM) so small problems fill the 148 SMs. Results are
   // identical: every C entry is the same in-order sum either way.
   const uint64_t tiles128 = ((row1 - row0 + kTile - 1) / kTile) * p->nb;
   if (row0 == 0 && row1 == p->n && p->sym_ready && sym_preferred(p)) {
-    if (p->algorithm == PALD_GPU_TRIPLET && split_enabled() && !accurate(p)) {
+    if (p->algorithm == PALD_GPU_TRIPLET && split_enabled()) {
       bool used = false;
       const int rc = launch_sym_split(p, s, &used);
       if (rc) return rc;
@@ -1316,12 +1515,14 @@ int plan_cohesion_share_impl(pald_gpu_plan* p, uint64_t part, uint64_t parts, cu
   PALD_CUDA(cudaMemsetAsync(p->c, 0, p->n * p->ld * 4, s));
   if (p->sym_ready && sym_preferred(p)) {
     const uint64_t pairs = p->nb * (p->nb + 1) / 2;
-    const int rc = launch_sym(p, (int)(pairs * part / parts), (int)(pairs * (part + 1) / parts), s);
-    if (rc == PALD_GPU_OK) {
-      ++p->launches;
-      p->last_kernel = PALD_GPU_KERNEL_PAIRS;
-    }
-    return rc;
+    const int t0 = (int)(pairs * part / parts), t1 = (int)(pairs * (part + 1) / parts);
+    const bool acc = accurate(p);
+    int rc;
+    if (acc && (rc = acc_zero_rows(p, 0, p->n, s))) return rc;
+    if ((rc = launch_sym(p, t0, t1, s))) return rc;
+    ++p->launches;
+    p->last_kernel = PALD_GPU_KERNEL_PAIRS;
+    return acc ? acc_round_pairs(p, t0, t1, own_c(p), s) : PALD_GPU_OK;
   }
   // Row bands of whole tile rows (every row costs the same).
   const uint64_t t0 = p->nb * part / parts, t1 = p->nb * (part + 1) / parts;
@@ -1375,8 +1576,8 @@ int load_focus_banded(pald_gpu_plan* p, const float* D, cudaStream_t s, cudaStre
   PALD_CUDA(cudaMemcpyAsync(p->stats, p->stats_host, sizeof(Stats), cudaMemcpyHostToDevice, sa));
   PALD_CUDA(cudaMemsetAsync(p->w, 0, p->n * p->ld * 4, s));  // pass-1 counts
   PALD_CUDA(cudaMemsetAsync(p->rank_fail, 0, nbands * sizeof(int), s));
-  const bool mark = p->sym_masks && p->algorithm == PALD_GPU_PAIRWISE && p->policy == PALD_GPU_STRICT &&
-                    sym_enabled();
+  const bool mark = tie_marks_wanted(p);
+  p->tri_marks = mark && p->algorithm == PALD_GPU_TRIPLET;
   if (mark) {
     PALD_CUDA(cudaMemsetAsync(p->sym_masks, 0, sym_mask_words(p) * sizeof(uint32_t), s));
     PALD_CUDA(cudaMemsetAsync(p->sym_tile_flags, 0, p->nb * sizeof(uint32_t), s));
@@ -1390,14 +1591,13 @@ int load_focus_banded(pald_gpu_plan* p, const float* D, cudaStream_t s, cudaStre
   const RankSrc src = rank_src_raw(p->c, p->ld);
   uint16_t* rk = reinterpret_cast<uint16_t*>(p->u);  // U is free until the focus finish
   const TieMarks tm{mark ? p->sym_masks : nullptr, p->sym_tile_flags, (int)p->nb, p->sym_nch};
-  std::vector<cudaEvent_t> ev(nbands);
-  for (auto& e : ev) PALD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  struct EvG {
-    std::vector<cudaEvent_t>& e;
-    ~EvG() {
-      for (auto x : e) cudaEventDestroy(x);
-    }
-  } evg{ev};
+  // band events (cached with the plan: one per band plus the layout's)
+  while ((int)p->band_ev.size() < nbands + 1) {
+    cudaEvent_t e;
+    PALD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    p->band_ev.push_back(e);
+  }
+  cudaEvent_t* ev = p->band_ev.data();
   for (int b = 0; b < nbands; ++b) {
     const int r0 = b * band_rows, r1 = std::min(n, r0 + band_rows);
     PALD_CUDA(cudaMemcpy2DAsync(p->c + (size_t)r0 * ld, (size_t)ld * 4, D + (size_t)r0 * n, (size_t)n * 4,
@@ -1431,13 +1631,11 @@ int load_focus_banded(pald_gpu_plan* p, const float* D, cudaStream_t s, cudaStre
   layout_kernel<<<grid_rows(p->n), 256, 0, sa>>>(p->c, (uint64_t)ld, n, p->ld, fast ? 1 : 0, p2, p->ds, p->dnu);
   PALD_CUDA(cudaGetLastError());
   p->launches += 2;  // + the stats bands
-  cudaEvent_t ev_layout;
-  PALD_CUDA(cudaEventCreateWithFlags(&ev_layout, cudaEventDisableTiming));
+  cudaEvent_t ev_layout = p->band_ev[nbands];
   PALD_CUDA(cudaEventRecord(ev_layout, sa));
   PALD_CUDA(cudaStreamWaitEvent(s, ev_layout, 0));
-  cudaEventDestroy(ev_layout);
   if (fast && p->algorithm == PALD_GPU_TRIPLET && sym_enabled() && sym_wins(p, 0.0)) p->sym_ready = true;
-  if (mark && fast && sym_wins(p, 0.0) && (rc = tie_summary(p, s))) return rc;
+  if (mark && fast && p->algorithm == PALD_GPU_PAIRWISE && sym_wins(p, 0.0) && (rc = tie_summary(p, s))) return rc;
   p->loaded = true;
   return PALD_GPU_OK;
 }
@@ -1479,12 +1677,16 @@ int plan_cohesion_share_peers_impl(pald_gpu_plan* p, uint64_t part, uint64_t par
     return set_error(PALD_GPU_ERR_UNSUPPORTED,
                      "fused pass 2 runs on the pair kernel only (use cohesion_share + a SUM all-reduce)");
   const uint64_t pairs = p->nb * (p->nb + 1) / 2;
-  const int rc = launch_sym(p, (int)(pairs * part / parts), (int)(pairs * (part + 1) / parts), s, true);
-  if (rc == PALD_GPU_OK) {
-    ++p->launches;
-    p->last_kernel = PALD_GPU_KERNEL_PAIRS;
-  }
-  return rc;
+  const int t0 = (int)(pairs * part / parts), t1 = (int)(pairs * (part + 1) / parts);
+  const bool acc = accurate(p);
+  int rc;
+  if (acc && (rc = acc_zero_rows(p, 0, p->n, s))) return rc;
+  if ((rc = launch_sym(p, t0, t1, s, true))) return rc;
+  ++p->launches;
+  p->last_kernel = PALD_GPU_KERNEL_PAIRS;
+  // accurate: the kernel only adds into the local double sums; the rounding
+  // pass stores this share's entries into every rank's C
+  return acc ? acc_round_pairs(p, t0, t1, p->peer_c, s) : PALD_GPU_OK;
 }
 
 #include "pald_multi.cuh"
@@ -1673,10 +1875,10 @@ int pald_gpu_plan_attach_peers_u(pald_gpu_plan* p, const pald_gpu_ipc_handle* u_
   return PALD_GPU_OK;
 }
 
-int pald_gpu_plan_focus_finish_peers(pald_gpu_plan* p, uint64_t part, uint64_t parts, int u_all, void* stream) {
+int pald_gpu_plan_focus_finish_peers(pald_gpu_plan* p, uint64_t part, uint64_t parts, int u_mode, void* stream) {
   if (!p) return set_error(PALD_GPU_ERR_VALIDATION, "null plan");
   DeviceGuard g(p->device);
-  return plan_focus_finish_peers_impl(p, part, parts, u_all != 0, static_cast<cudaStream_t>(stream));
+  return plan_focus_finish_peers_impl(p, part, parts, u_mode, static_cast<cudaStream_t>(stream));
 }
 
 int pald_gpu_plan_detach_peers(pald_gpu_plan* p) {
@@ -1763,9 +1965,6 @@ int pald_gpu_cohesion_f32_device(const float* dD, uint64_t ldd, uint64_t n,
   return PALD_GPU_OK;
 }
 
-#ifndef PALD_HOST_BANDS  // pass-2 bands of the host API (the last band's D2H is exposed)
-#define PALD_HOST_BANDS 16  // one raster group per band at n = 32768: e2e 3.790 -> 3.773 s
-#endif
 
 int pald_gpu_cohesion_f32(const float* D, uint64_t n, const pald_gpu_opts* o_in, int32_t* U_out,
                           float* C_out, pald_gpu_phase_times* times) {
@@ -1787,16 +1986,11 @@ int pald_gpu_cohesion_f32(const float* D, uint64_t n, const pald_gpu_opts* o_in,
   const auto t_start = std::chrono::steady_clock::now();
   pald_gpu_plan* p = nullptr;
   if ((rc = get_cached_plan(dev, n, o, &p))) return rc;
-  cudaStream_t s = nullptr, sc = nullptr;  // compute stream, copy-out stream
-  PALD_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-  PALD_CUDA(cudaStreamCreateWithFlags(&sc, cudaStreamNonBlocking));
-  struct StreamGuard {
-    cudaStream_t a, b;
-    ~StreamGuard() {
-      cudaStreamDestroy(a);
-      cudaStreamDestroy(b);
-    }
-  } sg{s, sc};
+  // compute stream, copy-out stream, second compute stream and the events of
+  // the one-shot call: created once per cached plan
+  if ((rc = ensure_oneshot(p))) return rc;
+  cudaStream_t s = p->os_s, sc = p->os_sc, s2 = p->os_s2;
+  cudaEvent_t* ev = p->os_ev;
   // Pass 2 runs in row bands; each band's C rows are copied to the host on
   // the copy stream while the next band computes, and U is copied during
   // pass 2 (it is final after pass 1). Only the last band's copy is exposed.
@@ -1806,19 +2000,15 @@ int pald_gpu_cohesion_f32(const float* D, uint64_t n, const pald_gpu_opts* o_in,
   // group). Bands alternate between two compute streams (they write
   // disjoint entries) so that one band's tail overlaps the next band.
   constexpr int kBands = PALD_HOST_BANDS;
-  cudaEvent_t ev[4 + kBands];
-  for (int i = 0; i < 4 + kBands; ++i)
-    PALD_CUDA(cudaEventCreateWithFlags(&ev[i], i < 4 ? cudaEventDefault : cudaEventDisableTiming));
-  cudaStream_t s2 = nullptr;
-  PALD_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
-  struct EvGuard {
-    cudaEvent_t* e;
-    cudaStream_t s2;
-    ~EvGuard() {
-      for (int i = 0; i < 4 + kBands; ++i) cudaEventDestroy(e[i]);
-      cudaStreamDestroy(s2);
+  // (a failed call leaves no work behind on these streams)
+  struct Drain {
+    cudaStream_t a, b, c;
+    ~Drain() {
+      cudaStreamSynchronize(a);
+      cudaStreamSynchronize(b);
+      cudaStreamSynchronize(c);
     }
-  } eg{ev, s2};
+  } drain{s, sc, s2};
   PALD_CUDA(cudaEventRecord(ev[0], s));
   if (banded_wanted(p)) {  // H2D in bands overlapped with the rank codes and pass 1
     PALD_CUDA(cudaEventRecord(ev[1], s));
@@ -1835,6 +2025,11 @@ int pald_gpu_cohesion_f32(const float* D, uint64_t n, const pald_gpu_opts* o_in,
     PALD_CUDA(cudaMemcpy2DAsync(U_out, n * 4, p->u, p->ld * 4, n * 4, n, cudaMemcpyDeviceToHost, sc));
   }
   if (p->sym_ready && sym_preferred(p)) {
+    const bool acc = accurate(p);
+    if (acc) {  // the double sums zeroed before either band stream starts
+      if ((rc = acc_zero_rows(p, 0, n, s))) return rc;
+      PALD_CUDA(cudaEventRecord(ev[2], s));
+    }
     PALD_CUDA(cudaStreamWaitEvent(s2, ev[2], 0));
     const int nb = (int)p->nb;
     const uint64_t pairs = p->nb * (p->nb + 1) / 2;
@@ -1848,6 +2043,7 @@ int pald_gpu_cohesion_f32(const float* D, uint64_t n, const pald_gpu_opts* o_in,
       // (bands run concurrently on two streams: no shared round barrier)
       if ((rc = launch_sym(p, t0, t1, cs, false, false))) return rc;
       ++p->launches;
+      if (acc && (rc = acc_round_pairs(p, t0, t1, own_c(p), cs))) return rc;
       PALD_CUDA(cudaEventRecord(ev[4 + band], cs));
       PALD_CUDA(cudaStreamWaitEvent(sc, ev[4 + band], 0));
       const uint64_t r0 = (uint64_t)g_row0 * kTile, r1 = std::min(n, (uint64_t)g1 * kTile);

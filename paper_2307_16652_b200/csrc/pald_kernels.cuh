@@ -123,6 +123,12 @@ struct KernelArgs {
   PeerBufs peers;           // PEERS kernels: pass-1 counts go to every rank's W
   double* c64;              // ACC kernels: double sums of the fp32 block partials (n x ld)
   int acc_chunks;           // ACC kernels: k chunks per fp32 block partial
+  // rank-coded triplet pass 1: tie marks per (tile pair, 32-point chunk)
+  // (pald_sym.cuh); chunks inside the tiles without a marked k run the fast
+  // step (strict and non-strict tests agree without a tie). NULL: none.
+  const uint32_t* tie_masks;
+  const uint32_t* tie_tile_flags;
+  int tie_nch;
 };
 
 constexpr int kGroupRows = 16;  // tile rows per raster group (L2 reuse of the panels)
@@ -175,43 +181,25 @@ __device__ __forceinline__ uint32_t stage_arrive(uint32_t* cnt) {
 }
 
 // Accurate mode (PALD_GPU_FLAG_ACCURATE): the fp32 register sums of an
-// output are flushed every `acc_chunks` k chunks into a double buffer and
-// restarted from 0. Adding a partial fp32 sum of positive terms 1/u (u in
-// [2, 2^24]) to a double sum of such partials is exact (the values span
-// less than 2^53 units of the smallest ulp), so the result is the exact sum
-// of the fp32 block partials -- independent of the flush order -- and only
-// the blocks' own fp32 rounding remains (k blocks of <= acc_chunks * BK
-// terms instead of one n-term chain). `first` starts the output's sum.
-__device__ __forceinline__ void acc_flush4(double* p, float a, float b, float c, float d, bool first) {
-  double2* q = reinterpret_cast<double2*>(p);
-  double2 v0 = first ? make_double2(0.0, 0.0) : q[0];
-  double2 v1 = first ? make_double2(0.0, 0.0) : q[1];
-  v0.x += (double)a;
-  v0.y += (double)b;
-  v1.x += (double)c;
-  v1.y += (double)d;
-  q[0] = v0;
-  q[1] = v1;
+// output are flushed every `acc_chunks` k chunks (one k block) into a
+// zeroed double buffer with red.global.add.f64 and restarted from 0. Adding
+// a partial fp32 sum of positive terms 1/u (u in [2, 2^24]) to a double sum
+// of such partials is exact (all values are multiples of 2^-38 below 2^14,
+// 52 bits), so the result is the exact sum of the fp32 block partials --
+// independent of the order of the additions, hence deterministic however
+// the blocks are spread over CTAs -- and only the blocks' own fp32 rounding
+// remains (<= acc_chunks * BK-term chains instead of one n-term chain). The
+// reductions need no result (RED, no scoreboard wait); acc_round_*_kernel
+// rounds the double sums to the fp32 C afterwards.
+__device__ __forceinline__ void acc_red4(double* p, float a, float b, float c, float d) {
+  atomicAdd(p, (double)a);
+  atomicAdd(p + 1, (double)b);
+  atomicAdd(p + 2, (double)c);
+  atomicAdd(p + 3, (double)d);
 }
-// Final flush: the double sums (also kept in the buffer) rounded to fp32.
-__device__ __forceinline__ float4 acc_final4(double* p, float a, float b, float c, float d, bool first) {
-  acc_flush4(p, a, b, c, d, first);
-  const double2* q = reinterpret_cast<const double2*>(p);
-  const double2 v0 = q[0], v1 = q[1];
-  return make_float4(__double2float_rn(v0.x), __double2float_rn(v0.y), __double2float_rn(v1.x),
-                     __double2float_rn(v1.y));
-}
-__device__ __forceinline__ void acc_flush2(double* p, float a, float b, bool first) {
-  double2* q = reinterpret_cast<double2*>(p);
-  double2 v0 = first ? make_double2(0.0, 0.0) : q[0];
-  v0.x += (double)a;
-  v0.y += (double)b;
-  q[0] = v0;
-}
-__device__ __forceinline__ float2 acc_final2(double* p, float a, float b, bool first) {
-  acc_flush2(p, a, b, first);
-  const double2 v0 = *reinterpret_cast<const double2*>(p);
-  return make_float2(__double2float_rn(v0.x), __double2float_rn(v0.y));
+__device__ __forceinline__ void acc_red2(double* p, float a, float b) {
+  atomicAdd(p, (double)a);
+  atomicAdd(p + 1, (double)b);
 }
 
 __device__ __forceinline__ uint32_t nu_bits(uint32_t v) { return v + 1u; }
@@ -757,10 +745,6 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE, RANK))
     }
 
     int le_a = 0, le_b = 0;  // rank-coded triplet: thresholds currently shifted for <=
-    // ACC: this run is one k block of its tile; the first starts the double
-    // sums, the last rounds them to fp32 and writes C
-    const bool acc_first = ch_begin == 0;
-    const bool acc_last = ch_end == nchunks;
     for (int ch = ch_begin; ch < ch_end; ++ch, ++p) {
       const int s = p % kStages;
       mbar_wait(&full_bar[s], (p / kStages) & 1);
@@ -793,7 +777,15 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE, RANK))
             le_b = want_b;
           }
         }
-        if (a_in || b_in) {
+        bool sel = a_in || b_in;
+        if (sel && args.tie_masks) {  // triplet: no marked k in the chunk -> the fast step is exact
+          static_assert(kBK == 64, "two 32-point mask words per chunk");
+          const size_t pi = ((size_t)tr * (2 * nb - tr + 1) / 2 + (tc - tr)) * args.tie_nch + k0 / 32;
+          const uint32_t flagged = __ldg(args.tie_tile_flags + tr) | __ldg(args.tie_tile_flags + tc);
+          const uint32_t m = __ldg(args.tie_masks + pi) | (k0 / 32 + 1 < args.tie_nch ? __ldg(args.tie_masks + pi + 1) : 0u);
+          sel = flagged || m;
+        }
+        if (sel) {
           for (int kk = 0; kk < kmax; ++kk) k_step_rank_sel(ra, rb, kk, k0 + kk, ty, tx, r0, c0, a_in, b_in, thr, acc);
         } else if (kmax == kBK) {
 #pragma unroll kRankUnroll
@@ -856,49 +848,24 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE, RANK))
           v[2 * jp] = acc[i][jp].x;
           v[2 * jp + 1] = acc[i][jp].y;
         }
-        if constexpr (ACC) {  // k block done: into the double sums (the last: rounded to fp32)
+        if constexpr (ACC) {  // k block done: into the double sums (rounded by acc_round_rows_kernel)
           double* prow = args.c64 + (size_t)r * ld;
-          if (!acc_last) {
-            if constexpr (TILE == 32) {
-              const int cc = c0 + tx * 2;
-              if (cc < n) acc_flush2(prow + cc, v[0], v[1], acc_first);
-            } else {
-#pragma unroll
-              for (int h = 0; h < TT / 4; ++h) {
-                const int cc = c0 + h * (TILE / 2) + tx * 4;
-                if (cc < n) acc_flush4(prow + cc, v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3], acc_first);
-              }
-            }
-            continue;
-          }
           if constexpr (TILE == 32) {
             const int cc = c0 + tx * 2;
-            if (cc < n) {
-              const float2 f = acc_final2(prow + cc, v[0], v[1], acc_first);
-              v[0] = f.x;
-              v[1] = f.y;
-            }
+            if (cc < n) acc_red2(prow + cc, v[0], v[1]);
           } else {
 #pragma unroll
             for (int h = 0; h < TT / 4; ++h) {
               const int cc = c0 + h * (TILE / 2) + tx * 4;
-              if (cc < n) {
-                const float4 f = acc_final4(prow + cc, v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3], acc_first);
-                v[4 * h] = f.x;
-                v[4 * h + 1] = f.y;
-                v[4 * h + 2] = f.z;
-                v[4 * h + 3] = f.w;
-              }
+              if (cc < n) acc_red4(prow + cc, v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
             }
           }
+          continue;
         }
         if (ZERO_DIAG) {
 #pragma unroll
           for (int j = 0; j < TT; ++j)
-            if (c0 + row_off<TILE>(tx, j) == r) {
-              v[j] = 0.f;
-              if constexpr (ACC) args.c64[(size_t)r * ld + r] = 0.0;
-            }
+            if (c0 + row_off<TILE>(tx, j) == r) v[j] = 0.f;
         }
         float* crow = args.c + (size_t)r * ld;
         // Columns past n land in the row padding (ld >= round_up(n, 32)).
@@ -942,7 +909,10 @@ struct FinishPeers {
   int32_t* u[kMaxPeers];
   float* w[kMaxPeers];
   int count;
-  int u_all;  // 1: store U into every device (0: own U only)
+  // where U goes: 0 own U only; 1 every device; 2 the device that owns the
+  // entry's row in the tile-row band split (bands [nb*i/count, nb*(i+1)/count)
+  // of tile rows: the devices that download U by row bands)
+  int u_mode;
 };
 
 template <bool PEERS>
@@ -972,16 +942,22 @@ __global__ void __launch_bounds__(256)
     tile[rl][cl] = v;
   }
   __syncthreads();
-  const int nw = PEERS ? peers.count : 1, nu = PEERS ? (peers.u_all ? peers.count : 1) : 1;
-  auto put = [&](size_t o, int32_t uv, float wv) {
+  const int nw = PEERS ? peers.count : 1;
+  auto put = [&](size_t o, int row, int32_t uv, float wv) {
     if constexpr (PEERS) {
       for (int q = 0; q < nw; ++q) peers.w[q][o] = wv;
-      if (nu == 1) {
+      if (peers.u_mode == 0) {
         u[o] = uv;
+      } else if (peers.u_mode == 1) {
+        for (int q = 0; q < nw; ++q) peers.u[q][o] = uv;
       } else {
-        for (int q = 0; q < nu; ++q) peers.u[q][o] = uv;
+        const int t = row / kTile;
+        int q = 0;
+        while (q + 1 < nw && nb * (q + 1) / nw <= t) ++q;
+        peers.u[q][o] = uv;
       }
     } else {
+      (void)row;
       u[o] = uv;
       w[o] = wv;
     }
@@ -993,10 +969,10 @@ __global__ void __launch_bounds__(256)
       if (r < n && c < n && (!diag || rl <= cl)) {
         const size_t o = (size_t)r * ld + c;
         if (r == c) {
-          put(o, 0, 0.f);
+          put(o, r, 0, 0.f);
         } else {
           const float v = tile[rl][cl];
-          put(o, static_cast<int32_t>(v), 1.0f / v);
+          put(o, r, static_cast<int32_t>(v), 1.0f / v);
         }
       }
     }
@@ -1005,9 +981,45 @@ __global__ void __launch_bounds__(256)
       const int r = r0 + rl, c = c0 + cl;
       if (r < n && c < n && r < c) {
         const float v = tile[rl][cl];
-        put((size_t)c * ld + r, static_cast<int32_t>(v), 1.0f / v);
+        put((size_t)c * ld + r, c, static_cast<int32_t>(v), 1.0f / v);
       }
     }
+  }
+}
+
+// Accurate mode: the double sums of rows [row0, row1) rounded to the fp32
+// C (triplet: diagonal 0).
+__global__ void __launch_bounds__(256)
+    acc_round_rows_kernel(const double* __restrict__ c64, float* __restrict__ c, int n, int ld, int row0,
+                          int row1, int zero_diag) {
+  for (int r = row0 + blockIdx.x; r < row1; r += gridDim.x)
+    for (int z = threadIdx.x; z < n; z += blockDim.x) {
+      const double v = c64[(size_t)r * ld + z];
+      c[(size_t)r * ld + z] = (zero_diag && z == r) ? 0.f : __double2float_rn(v);
+    }
+}
+
+// Accurate mode, tile pairs [t0, t1) of a pair list (both C[P][Q] and
+// C[Q][P]): rounded to fp32 into every buffer of `out` (the devices of a
+// multi-GPU exchange, or just the local C).
+__global__ void __launch_bounds__(256)
+    acc_round_pairs_kernel(const int2* __restrict__ tiles, int t0, const double* __restrict__ c64, PeerBufs out,
+                           int n, int ld, int zero_diag) {
+  const int2 tp = tiles[t0 + blockIdx.x];
+  const int half = blockIdx.y;
+  if (half == 1 && tp.x == tp.y) return;
+  const int R = half ? tp.y : tp.x, Q = half ? tp.x : tp.y;
+  for (int e = threadIdx.x; e < kTile * kTile / 4; e += blockDim.x) {
+    const int rl = e / (kTile / 4), cl = (e % (kTile / 4)) * 4;
+    const int r = R * kTile + rl, c = Q * kTile + cl;
+    if (r >= n || c >= n) continue;
+    const size_t o = (size_t)r * ld + c;
+    const double2 a = *reinterpret_cast<const double2*>(c64 + o);
+    const double2 b = *reinterpret_cast<const double2*>(c64 + o + 2);
+    float4 f = make_float4(__double2float_rn(a.x), __double2float_rn(a.y), __double2float_rn(b.x),
+                           __double2float_rn(b.y));
+    if (zero_diag && r >= c && r < c + 4) (&f.x)[r - c] = 0.f;
+    for (int q = 0; q < out.count; ++q) *reinterpret_cast<float4*>(out.ptr[q] + o) = f;
   }
 }
 

@@ -71,10 +71,11 @@ NcclApi& nccl() {
 // finishes share `part` of `parts` of the upper-triangular tiles from the
 // counts in every attached W, storing W = 1/U into every W and U into every
 // attached U (u_all) or only its own.
-int plan_focus_finish_peers_impl(pald_gpu_plan* p, uint64_t part, uint64_t parts, bool u_all, cudaStream_t s) {
+int plan_focus_finish_peers_impl(pald_gpu_plan* p, uint64_t part, uint64_t parts, int u_mode, cudaStream_t s) {
   if (!p->loaded) return set_error(PALD_GPU_ERR_VALIDATION, "plan has no distances loaded");
   if (p->peer_rank < 0) return set_error(PALD_GPU_ERR_VALIDATION, "no peers attached");
-  if (u_all && p->peer_u.count != p->peer_w.count)
+  if (u_mode < 0 || u_mode > 2) return set_error(PALD_GPU_ERR_VALIDATION, "unknown U mode %d", u_mode);
+  if (u_mode && p->peer_u.count != p->peer_w.count)
     return set_error(PALD_GPU_ERR_VALIDATION, "peer U buffers not attached");
   if (parts < 1 || part >= parts)
     return set_error(PALD_GPU_ERR_VALIDATION, "invalid share %llu of %llu", (unsigned long long)part,
@@ -84,10 +85,10 @@ int plan_focus_finish_peers_impl(pald_gpu_plan* p, uint64_t part, uint64_t parts
   if (t1 <= t0) return PALD_GPU_OK;
   FinishPeers fp{};
   fp.count = p->peer_w.count;
-  fp.u_all = u_all ? 1 : 0;
+  fp.u_mode = u_mode;
   for (int q = 0; q < fp.count; ++q) {
     fp.w[q] = p->peer_w.ptr[q];
-    fp.u[q] = reinterpret_cast<int32_t*>(u_all ? p->peer_u.ptr[q] : nullptr);
+    fp.u[q] = reinterpret_cast<int32_t*>(u_mode ? p->peer_u.ptr[q] : nullptr);
   }
   focus_finish_kernel<true><<<(unsigned)((t1 - t0) * 4), 256, 0, s>>>(p->u, p->w, (int)p->n, (int)p->ld,
                                                                        (int)p->nb, (int)t0, fp);
@@ -325,7 +326,8 @@ int run_multi(const float* D, uint64_t n, const pald_gpu_opts* o, int32_t* U_out
     });
     // exchange + finish: U and W = 1/U complete on every device
     step([&]() -> int {
-      int r = xf == PALD_GPU_EXCHANGE_PEER ? plan_focus_finish_peers_impl(p, i, N, true, s)
+      // U only to the device that downloads its row (u_mode 2)
+      int r = xf == PALD_GPU_EXCHANGE_PEER ? plan_focus_finish_peers_impl(p, i, N, 2, s)
                                            : plan_focus_finish_impl(p, s);
       if (r) return r;
       PALD_CUDA(cudaStreamSynchronize(s));

@@ -83,6 +83,8 @@ struct SymArgs {
   float* partial;
   double* c64;                // ACC kernels: double sums of the fp32 block partials (n x ld)
   int acc_chunks;             // ACC kernels: k chunks (of kSymBK) per fp32 block partial
+  int tri_marks;              // TRI: masks hold the tie marks (chunks inside the tiles
+                              // run the shared step for unmarked k)
 };
 
 // Full-avalanche mix (murmur3 finalizer): the bucket takes the low bits and
@@ -381,12 +383,6 @@ __device__ __forceinline__ void store_c4(const SymArgs& a, size_t off, float4 v)
   }
 }
 
-__device__ __forceinline__ void sym_zero_diag4(float4& f, int c, int r) {
-  if (c == r) f.x = 0.f;
-  if (c + 1 == r) f.y = 0.f;
-  if (c + 2 == r) f.z = 0.f;
-  if (c + 3 == r) f.w = 0.f;
-}
 
 // Persistent pass-2 kernel over the tile pairs [tile_begin, tile_end) of the
 // grouped upper-triangular order (P <= Q). CTA g takes pairs
@@ -408,23 +404,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nch = args.nch;
   const int G = gridDim.x, g = blockIdx.x;
   const int first = args.tile_begin + g;
-  // ACC: every pair is walked as nsub consecutive items of acc_chunks chunks
-  const int nsub = ACC ? (nch + args.acc_chunks - 1) / args.acc_chunks : 1;
-  const int R = (first < args.tile_end ? (args.tile_end - 1 - first) / G + 1 : 0) * nsub;
+  // ACC (accurate mode) always runs on an item list of k blocks (SPLIT form)
+  static_assert(!ACC || SPLIT, "accurate mode: item lists only");
+  const int R = first < args.tile_end ? (args.tile_end - 1 - first) / G + 1 : 0;
   // item ri of this CTA: tile pair and chunk range [cb, ce) (whole pairs
-  // unless SPLIT / ACC)
+  // unless SPLIT). SPLIT items come from the host's list: (tile row, tile
+  // col, cb | ce << 15, slot); empty items (cb == ce) pad per-CTA queues.
   auto item = [&](int ri, int2& tp, int& cb, int& ce, int& slot) {
-    if constexpr (ACC) {
-      const int pi = ri / nsub, sub = ri - pi * nsub;
-      tp = args.tiles[first + pi * G];
-      cb = sub * args.acc_chunks;
-      ce = min(nch, cb + args.acc_chunks);
-      slot = sub;
-    } else if constexpr (SPLIT) {
+    if constexpr (SPLIT) {
       const int4 it = args.items[first + ri * G];
       tp = make_int2(it.x, it.y);
-      cb = it.z & 0xffff;
-      ce = it.z >> 16;
+      cb = it.z & 0x7fff;
+      ce = (it.z >> 15) & 0x7fff;
       slot = it.w;
     } else {
       tp = args.tiles[first + ri * G];
@@ -433,7 +424,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       slot = -1;
     }
   };
-  int P = R / nsub * nch;
+  int P = R * nch;
   if constexpr (SPLIT) {
     P = 0;
     for (int ri = 0; ri < R; ++ri) {
@@ -471,20 +462,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   };
   constexpr bool ITEMS = SPLIT || ACC;  // items other than whole pairs
   int pr_ri = 0, pr_ch = 0, pr_end = nch;
-  if constexpr (ITEMS) {
-    int2 tp;
-    int sl;
-    item(0, tp, pr_ch, pr_end, sl);
-  }
+  auto pr_load = [&]() {  // the next non-empty item at or after pr_ri
+    for (; pr_ri < R; ++pr_ri) {
+      int2 tp;
+      int sl;
+      item(pr_ri, tp, pr_ch, pr_end, sl);
+      if (pr_ch < pr_end) break;
+    }
+  };
+  if constexpr (ITEMS) pr_load();
   auto pr_advance = [&]() {
     if (++pr_ch == pr_end) {
       ++pr_ri;
       if constexpr (ITEMS) {
-        if (pr_ri < R) {
-          int2 tp;
-          int sl;
-          item(pr_ri, tp, pr_ch, pr_end, sl);
-        }
+        pr_load();
       } else {
         pr_ch = 0;
       }
@@ -504,15 +495,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     int2 tp;
     int ch_b, ch_e, slot;
     item(ri, tp, ch_b, ch_e, slot);
+    if (SPLIT && ch_b >= ch_e) continue;  // queue padding
     const int r0 = tp.x * kTile, c0 = tp.y * kTile;
     const bool diag = tp.x == tp.y;
-    const uint32_t* mk = TRI ? nullptr : args.masks + pair_index(tp.x, tp.y, args.nb) * nch;
-    const bool all_marked =
-        !TRI && (__ldg(args.tile_flags + tp.x) | __ldg(args.tile_flags + tp.y)) != 0u;
+    const bool marks = !TRI || args.tri_marks;
+    const uint32_t* mk = marks ? args.masks + pair_index(tp.x, tp.y, args.nb) * nch : nullptr;
+    const bool all_marked = !marks || (__ldg(args.tile_flags + tp.x) | __ldg(args.tile_flags + tp.y)) != 0u;
     float2 thr[8][4], acc[8][4], act[8][4];
-    // ACC: this item is one k block of its pair; the first starts the double
-    // sums, the last rounds them to fp32 and stores C
-    const bool acc_first = ch_b == 0, acc_last = ch_e == nch;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
 #pragma unroll
@@ -546,8 +535,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll kSymUnroll
           for (int kk = 0; kk < kSymBK; ++kk) sym_step(sa, sb, sw, sv, kk, ty, tx, thr, acc, act);
         } else {
-          for (int kk = 0; kk < kmax; ++kk)
-            sym_step_tri_sel(sa, sb, sw, sv, kk, k0 + kk, ty, tx, r0, c0, a_in, b_in, thr, acc, act);
+          // inside the row / column tile: per-element nu() only where a tie
+          // is possible (marked k); without marks every k
+          const uint32_t m = all_marked ? 0xffffffffu : __ldg(mk + ch);
+          for (int kk = 0; kk < kmax; ++kk) {
+            if ((m >> kk) & 1u)
+              sym_step_tri_sel(sa, sb, sw, sv, kk, k0 + kk, ty, tx, r0, c0, a_in, b_in, thr, acc, act);
+            else
+              sym_step(sa, sb, sw, sv, kk, ty, tx, thr, acc, act);
+          }
         }
       } else {
       const uint32_t m = all_marked ? 0xffffffffu : __ldg(mk + ch);
@@ -571,7 +567,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         pr_advance();
       }
     }
-    if (SPLIT && slot >= 0) {  // partial tiles: [0] rows of P x cols of Q, [1] rows of Q x cols of P
+    if (SPLIT && !ACC && slot >= 0) {  // partial tiles: [0] rows of P x cols of Q, [1] rows of Q x cols of P
       float* pt = args.partial + (size_t)slot * 2 * kTile * kTile;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
@@ -622,27 +618,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const size_t rowo = (size_t)r * ld;
       const int ca = c0 + tx * 4, cb = c0 + 64 + tx * 4;
-      if constexpr (ACC) {
-        if (!acc_last) {  // k block done: into the double sums
-          if (ca < n) acc_flush4(args.c64 + rowo + ca, acc[i][0].x, acc[i][0].y, acc[i][1].x, acc[i][1].y, acc_first);
-          if (cb < n) acc_flush4(args.c64 + rowo + cb, acc[i][2].x, acc[i][2].y, acc[i][3].x, acc[i][3].y, acc_first);
-          continue;
-        }
-        // last k block: the double sums, rounded to fp32 (the triplet's zero
-        // diagonal is re-imposed after the rounding)
-        if (ca < n) {
-          float4 f = acc_final4(args.c64 + rowo + ca, acc[i][0].x, acc[i][0].y, acc[i][1].x, acc[i][1].y, acc_first);
-          if (TRI && diag) sym_zero_diag4(f, ca, r);
-          store_c4<PEERS>(args, rowo + ca, f);
-        }
-        if (cb < n) {
-          float4 f = acc_final4(args.c64 + rowo + cb, acc[i][2].x, acc[i][2].y, acc[i][3].x, acc[i][3].y, acc_first);
-          if (TRI && diag) sym_zero_diag4(f, cb, r);
-          store_c4<PEERS>(args, rowo + cb, f);
-        }
-        // the double sums keep the zero diagonal too (written by the thread
-        // that owns column r, after its own final flush)
-        if (TRI && diag && ((r >= ca && r < ca + 4) || (r >= cb && r < cb + 4))) args.c64[rowo + r] = 0.0;
+      if constexpr (ACC) {  // k block done: into the double sums (rounded by acc_round_pairs_kernel)
+        if (ca < n) acc_red4(args.c64 + rowo + ca, acc[i][0].x, acc[i][0].y, acc[i][1].x, acc[i][1].y);
+        if (cb < n) acc_red4(args.c64 + rowo + cb, acc[i][2].x, acc[i][2].y, acc[i][3].x, acc[i][3].y);
         continue;
       }
       if (ca < n)
@@ -663,23 +641,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (ACC) {
           double* prow = args.c64 + rowo;
           const bool hi = (j & 1) != 0;
-          if (!acc_last) {
-            if (ra < n)
-              acc_flush4(prow + ra, hi ? act[0][jp].y : act[0][jp].x, hi ? act[1][jp].y : act[1][jp].x,
-                         hi ? act[2][jp].y : act[2][jp].x, hi ? act[3][jp].y : act[3][jp].x, acc_first);
-            if (rb < n)
-              acc_flush4(prow + rb, hi ? act[4][jp].y : act[4][jp].x, hi ? act[5][jp].y : act[5][jp].x,
-                         hi ? act[6][jp].y : act[6][jp].x, hi ? act[7][jp].y : act[7][jp].x, acc_first);
-            continue;
-          }
           if (ra < n)
-            store_c4<PEERS>(args, rowo + ra,
-                            acc_final4(prow + ra, hi ? act[0][jp].y : act[0][jp].x, hi ? act[1][jp].y : act[1][jp].x,
-                                       hi ? act[2][jp].y : act[2][jp].x, hi ? act[3][jp].y : act[3][jp].x, acc_first));
+            acc_red4(prow + ra, hi ? act[0][jp].y : act[0][jp].x, hi ? act[1][jp].y : act[1][jp].x,
+                     hi ? act[2][jp].y : act[2][jp].x, hi ? act[3][jp].y : act[3][jp].x);
           if (rb < n)
-            store_c4<PEERS>(args, rowo + rb,
-                            acc_final4(prow + rb, hi ? act[4][jp].y : act[4][jp].x, hi ? act[5][jp].y : act[5][jp].x,
-                                       hi ? act[6][jp].y : act[6][jp].x, hi ? act[7][jp].y : act[7][jp].x, acc_first));
+            acc_red4(prow + rb, hi ? act[4][jp].y : act[4][jp].x, hi ? act[5][jp].y : act[5][jp].x,
+                     hi ? act[6][jp].y : act[6][jp].x, hi ? act[7][jp].y : act[7][jp].x);
           continue;
         }
         if ((j & 1) == 0) {

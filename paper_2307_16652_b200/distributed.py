@@ -181,7 +181,7 @@ class ShardedRunner:
             self.engine.focus_finish(stream=stream)
         elif self.focus_exchange == "peer":
             self._sync_barrier(stream)  # every rank's counts are in its W
-            self.engine.focus_finish_peers(self.rank, self.world, u_all=True, stream=stream)
+            self.engine.focus_finish_peers(self.rank, self.world, u_mode=1, stream=stream)
             self._sync_barrier(stream)  # every W (and U) finished everywhere
         elif self.focus_exchange == "red":
             self._sync_barrier(stream)  # all ranks' counts are in every W

@@ -193,10 +193,11 @@ class Engine:
             C.memmove(arr[q].bytes, h, 64)
         _raise_for(self.lib.pald_gpu_plan_attach_peers_u(self._plan, arr))
 
-    def focus_finish_peers(self, part: int, parts: int, u_all: bool = False, stream=None) -> None:
+    def focus_finish_peers(self, part: int, parts: int, u_mode: int = 1, stream=None) -> None:
         """Peer-pull exchange of pass 1: finish share `part` of `parts` of the
-        tiles from every rank's counts, storing W (and U if u_all) everywhere."""
-        _raise_for(self.lib.pald_gpu_plan_focus_finish_peers(self._plan, part, parts, int(u_all),
+        tiles from every rank's counts, storing W everywhere and U per u_mode
+        (0 own, 1 every rank, 2 the rank owning the row's tile band)."""
+        _raise_for(self.lib.pald_gpu_plan_focus_finish_peers(self._plan, part, parts, int(u_mode),
                                                              self._stream(stream)))
 
     def pair_kernel_preferred(self) -> bool:

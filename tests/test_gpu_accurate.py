@@ -1,5 +1,5 @@
 """Accurate mode (PALD_GPU_FLAG_ACCURATE, include/pald_gpu.h): pass 2 keeps
-each output's fp32 running sum only over k blocks of 256 terms and adds
+each output's fp32 running sum only over k blocks of 1024 terms and adds
 the block partials into a double sum (exact, order-independent), rounded to
 fp32 at the end. U is unchanged (pass 1 is integer work); C is compared
 with the fp64-accumulated oracle (oracle/pald_oracle.c *_f64), which the
@@ -30,9 +30,10 @@ def engine(D, alg, accurate, policy="strict"):
 
 def test_accurate_pairwise_pair_kernel(oracle):
     """Random D at n = 2304 (pair kernel + tail tiles): U identical to the
-    default mode, C within 1e-6 of fp64, the double sums likewise (both
-    differ from the fp64 oracle only by the fp32 rounding of each
-    <= 256-term block partial), and C = the double sums rounded once."""
+    default mode, C within 3e-6 of fp64 (one 1024-term fp32 chain alone
+    reaches ~2e-6: config 1), the double sums likewise (both differ from the
+    fp64 oracle only by the fp32 rounding of each block partial), and C = the
+    double sums rounded once."""
     n = 2304
     d = random_upper(n, 11)
     D = torch.from_numpy(d).cuda()
@@ -44,9 +45,9 @@ def test_accurate_pairwise_pair_kernel(oracle):
     u64, c64 = oracle.pairwise_f64(d)
     assert np.array_equal(U, u64)
     C = acc.C.cpu().numpy()
-    assert max_rel_diff(C, c64) <= 1e-6
-    # the double sums: only the fp32 rounding of each <= 256-term partial
-    assert max_rel_diff(acc.C64.cpu().numpy(), c64) <= 1e-6
+    assert max_rel_diff(C, c64) <= 3e-6
+    # the double sums: only the fp32 rounding of each <= 1024-term partial
+    assert max_rel_diff(acc.C64.cpu().numpy(), c64) <= 3e-6
     # C is the double sum rounded once to fp32
     assert np.array_equal(C, acc.C64.cpu().numpy().astype(np.float32))
 
@@ -63,7 +64,7 @@ def test_accurate_one_sided_and_ties(oracle):
     acc = engine(D, "pairwise", True)
     assert acc.info()["cohesion_kernel"].startswith("pald_tile_kernel")
     assert np.array_equal(acc.U.cpu().numpy(), u64)
-    assert max_rel_diff(acc.C.cpu().numpy(), c64) <= 1e-6
+    assert max_rel_diff(acc.C.cpu().numpy(), c64) <= 3e-6
     ex = Engine(n, "pairwise", force_exact=True, accurate=True)
     ex.run(D)
     torch.cuda.synchronize()
@@ -78,7 +79,7 @@ def test_accurate_one_sided_and_ties(oracle):
 
 def test_accurate_triplet(oracle):
     """Triplet pass 2 (pair kernel, no k split in accurate mode): U exact,
-    C within 1e-6 of fp64, diagonal 0 in C and in the double sums."""
+    C within 3e-6 of fp64, diagonal 0 in C and in the double sums."""
     n = 1700
     d = random_upper(n, 5)
     D = torch.from_numpy(d).cuda()
@@ -86,7 +87,7 @@ def test_accurate_triplet(oracle):
     u64, c64 = oracle.triplet_f64(d)
     assert np.array_equal(acc.U.cpu().numpy(), u64)
     C = acc.C.cpu().numpy()
-    assert max_rel_diff(C, c64) <= 1e-6
+    assert max_rel_diff(C, c64) <= 3e-6
     assert np.all(np.diagonal(C) == 0) and np.all(np.diagonal(acc.C64.cpu().numpy()) == 0)
 
 
@@ -107,7 +108,7 @@ def test_accurate_through_c_abi(oracle):
         _raise_for(lib.pald_gpu_cohesion_f32(d.ctypes.data, n, C.byref(o), u.ctypes.data, c.ctypes.data, None))
         u64, c64 = orc(d)
         assert np.array_equal(u, u64)
-        assert max_rel_diff(c, c64) <= 1e-6
+        assert max_rel_diff(c, c64) <= 3e-6
 
 
 def test_accurate_small_blocks_subprocess():
@@ -120,3 +121,25 @@ def test_accurate_small_blocks_subprocess():
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "ok" in r.stdout
+
+
+def test_triplet_tie_marks_on_quantized_data(oracle):
+    """Triplet with tie marks (n > 2048: rank codes; pald_sym.cuh tri_marks):
+    chunks inside the row / column tiles run the fast steps for unmarked k.
+    Distances on a 2^-14 grid: every row holds duplicates, so marks are
+    mixed. Sampled rows (tile edges included) against the fp64 oracle: U
+    exact, C within 3e-6 (accurate double sums)."""
+    from helpers import boundary_rows, rows_parallel
+
+    n = 2600
+    rng = np.random.default_rng(12)
+    d = np.zeros((n, n), np.float32)
+    iu = np.triu_indices(n, 1)
+    d[iu] = (np.floor(rng.uniform(1.0, 2.0, iu[0].size) * 2 ** 14) / 2 ** 14).astype(np.float32)
+    d[(iu[1], iu[0])] = d[iu]
+    e = engine(torch.from_numpy(d).cuda(), "triplet", False)
+    assert e.info()["rank_codes"] and e.info()["cohesion_kernel"] == "pald_sym_cohesion_kernel"
+    rows = boundary_rows(n, extra=10, seed=3)
+    ur, cr = rows_parallel(oracle.triplet_rows_f64, d, rows)
+    assert np.array_equal(e.U[rows.tolist()].cpu().numpy(), ur)
+    assert max_rel_diff(e.C[rows.tolist()].cpu().numpy(), cr) <= 3e-6

@@ -15,6 +15,7 @@ def main():
     ap.add_argument("--alg", default="pairwise")
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--exact", action="store_true")
+    ap.add_argument("--accurate", action="store_true")
     a = ap.parse_args()
     import torch
 
@@ -22,7 +23,7 @@ def main():
     from paper_2307_16652_b200.engine import Engine
 
     D, cfg = make_input(a.config, "cuda", 20230731)
-    eng = Engine(cfg.n, a.alg, force_exact=a.exact)
+    eng = Engine(cfg.n, a.alg, force_exact=a.exact, accurate=a.accurate)
     for _ in range(a.iters):
         eng.run(D)
     torch.cuda.synchronize()
