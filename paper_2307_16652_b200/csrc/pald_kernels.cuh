@@ -988,14 +988,19 @@ __global__ void __launch_bounds__(256)
 }
 
 // Accurate mode: the double sums of rows [row0, row1) rounded to the fp32
-// C (triplet: diagonal 0).
+// C (triplet: diagonal 0, in the double sums too).
 __global__ void __launch_bounds__(256)
-    acc_round_rows_kernel(const double* __restrict__ c64, float* __restrict__ c, int n, int ld, int row0,
+    acc_round_rows_kernel(double* __restrict__ c64, float* __restrict__ c, int n, int ld, int row0,
                           int row1, int zero_diag) {
   for (int r = row0 + blockIdx.x; r < row1; r += gridDim.x)
     for (int z = threadIdx.x; z < n; z += blockDim.x) {
-      const double v = c64[(size_t)r * ld + z];
-      c[(size_t)r * ld + z] = (zero_diag && z == r) ? 0.f : __double2float_rn(v);
+      const size_t o = (size_t)r * ld + z;
+      if (zero_diag && z == r) {
+        c64[o] = 0.0;
+        c[o] = 0.f;
+      } else {
+        c[o] = __double2float_rn(c64[o]);
+      }
     }
 }
 
@@ -1003,7 +1008,7 @@ __global__ void __launch_bounds__(256)
 // C[Q][P]): rounded to fp32 into every buffer of `out` (the devices of a
 // multi-GPU exchange, or just the local C).
 __global__ void __launch_bounds__(256)
-    acc_round_pairs_kernel(const int2* __restrict__ tiles, int t0, const double* __restrict__ c64, PeerBufs out,
+    acc_round_pairs_kernel(const int2* __restrict__ tiles, int t0, double* __restrict__ c64, PeerBufs out,
                            int n, int ld, int zero_diag) {
   const int2 tp = tiles[t0 + blockIdx.x];
   const int half = blockIdx.y;
@@ -1018,7 +1023,10 @@ __global__ void __launch_bounds__(256)
     const double2 b = *reinterpret_cast<const double2*>(c64 + o + 2);
     float4 f = make_float4(__double2float_rn(a.x), __double2float_rn(a.y), __double2float_rn(b.x),
                            __double2float_rn(b.y));
-    if (zero_diag && r >= c && r < c + 4) (&f.x)[r - c] = 0.f;
+    if (zero_diag && r >= c && r < c + 4) {
+      (&f.x)[r - c] = 0.f;
+      c64[(size_t)r * ld + r] = 0.0;
+    }
     for (int q = 0; q < out.count; ++q) *reinterpret_cast<float4*>(out.ptr[q] + o) = f;
   }
 }
