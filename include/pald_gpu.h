@@ -70,7 +70,7 @@ enum pald_gpu_flags {
    * FFMA.SAT compare path (testing). */
   PALD_GPU_FLAG_FORCE_EXACT = 2u,
   /* Accurate mode: pass 2 keeps each output's fp32 running sum only over
-   * blocks of PALD_GPU_ACC_BLOCK (default 256) third points and adds the
+   * blocks of PALD_GPU_ACC_BLOCK (default 1024) third points and adds the
    * block partials into a double sum (exact: see csrc/pald_kernels.cuh
    * acc_flush4), rounded to fp32 at the end. C then stays within ~1e-6 of
    * the fp64-accumulated result at n = 32768 (the default single fp32 chain

@@ -170,7 +170,8 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 // after __syncwarp (which orders the warp's shared-memory reads of the
 // stage before it); the arrival that completes the count refills the stage
 // with TMA. acq_rel: every warp's reads happen-before the refill issued by
-// the last arriver (the async-proxy write of the next TMA load).
+// the last arriver, which then crosses to the async proxy
+// (fence.proxy.async in issue()) for the write of the next TMA load.
 __device__ __forceinline__ uint32_t stage_arrive(uint32_t* cnt) {
   uint32_t old;
   asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
@@ -667,6 +668,9 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE, RANK))
     const CUtensorMap* ma = ((PASS == 1 && SPLIT) || (A_NU && k1 <= c0)) ? &tm_dnu : &tm_d;
     const CUtensorMap* mb = (B_NU && k1 <= r0) ? &tm_dnu : &tm_d;
     uint8_t* st = smem + s * SB;
+    // generic-proxy reads of the stage (ordered before this point by the
+    // acq_rel arrivals) -> async-proxy write of the refill
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_expect_tx(&full_bar[s], SB);
     if (RANK) {  // tm_d: RA (uint32 codes, rows R), tm_dnu: RB (uint16 codes, columns Q)
       tma_load_2d(st, &tm_d, r0, k0, &full_bar[s]);

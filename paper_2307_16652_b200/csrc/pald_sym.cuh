@@ -454,6 +454,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // triplet: a chunk wholly below the column (row) tile takes nu() on A (B)
     const CUtensorMap* ma = (TRI && k1 <= c0) ? &tm_dnu : &tm_d;
     const CUtensorMap* mb = (TRI && k1 <= r0) ? &tm_dnu : &tm_d;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // stage reads -> TMA refill
     mbar_expect_tx(&full_bar[s], kSymStageBytes);
     tma_load_2d(st, ma, r0, k0, &full_bar[s]);
     tma_load_2d(st + kSymBox, mb, c0, k0, &full_bar[s]);

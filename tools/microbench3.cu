@@ -74,6 +74,41 @@ __global__ void __launch_bounds__(128 * 128 / (TM * TN), 1) tile_kernel(float* o
         }
         continue;
       }
+      if (ORD == 3 || ORD == 4) {  // column-pair outer; the 8 transposed-output FFMA2s of a column pair in ONE asm block
+        float2 kv[TM][TN / 2];
+#pragma unroll
+        for (int p = 0; p < TN / 2; ++p) {
+#pragma unroll
+          for (int i = 0; i < TM; ++i) {
+            const float m0 = fminf(a[i], b[2 * p]), m1 = fminf(a[i], b[2 * p + 1]);
+            kv[i][p] = make_float2(__saturatef(__fmaf_rn(m0, 0x1p20f, thr[i][p].x)),
+                                   __saturatef(__fmaf_rn(m1, 0x1p20f, thr[i][p].y)));
+          }
+          unsigned long long vv = (unsigned long long)__float_as_uint(v[2 * p]) | ((unsigned long long)__float_as_uint(v[2 * p + 1]) << 32);
+          unsigned long long* A = reinterpret_cast<unsigned long long*>(&act[0][0]);
+          unsigned long long* K = reinterpret_cast<unsigned long long*>(&kv[0][0]);
+          asm volatile(
+              "fma.rn.f32x2 %0, %8, %16, %0;\n\tfma.rn.f32x2 %1, %9, %16, %1;\n\t"
+              "fma.rn.f32x2 %2, %10, %16, %2;\n\tfma.rn.f32x2 %3, %11, %16, %3;\n\t"
+              "fma.rn.f32x2 %4, %12, %16, %4;\n\tfma.rn.f32x2 %5, %13, %16, %5;\n\t"
+              "fma.rn.f32x2 %6, %14, %16, %6;\n\tfma.rn.f32x2 %7, %15, %16, %7;"
+              : "+l"(A[0 * (TN / 2) + p]), "+l"(A[1 * (TN / 2) + p]), "+l"(A[2 * (TN / 2) + p]), "+l"(A[3 * (TN / 2) + p]),
+                "+l"(A[4 * (TN / 2) + p]), "+l"(A[5 * (TN / 2) + p]), "+l"(A[6 * (TN / 2) + p]), "+l"(A[7 * (TN / 2) + p])
+              : "l"(K[0 * (TN / 2) + p]), "l"(K[1 * (TN / 2) + p]), "l"(K[2 * (TN / 2) + p]), "l"(K[3 * (TN / 2) + p]),
+                "l"(K[4 * (TN / 2) + p]), "l"(K[5 * (TN / 2) + p]), "l"(K[6 * (TN / 2) + p]), "l"(K[7 * (TN / 2) + p]), "l"(vv));
+          if (ORD == 3) {
+#pragma unroll
+            for (int i = 0; i < TM; ++i) acc[i][p] = __ffma2_rn(kv[i][p], make_float2(w[i], w[i]), acc[i][p]);
+          }
+        }
+        if (ORD == 4) {
+#pragma unroll
+          for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int p = 0; p < TN / 2; ++p) acc[i][p] = __ffma2_rn(kv[i][p], make_float2(w[i], w[i]), acc[i][p]);
+        }
+        continue;
+      }
       if (ORD == 2) {  // column-pair outer, rows inner
 #pragma unroll
         for (int p = 0; p < TN / 2; ++p)
@@ -167,5 +202,7 @@ int main() {
   run<8, 8, true, 0, 0, 1>("cohesion_8x8_sym_rowbatch", out, thr, nsm);
   run<8, 8, true, 0, 0, 2>("cohesion_8x8_sym_colouter", out, thr, nsm);
   run<8, 8, true, 0, 2>("cohesion_8x8_sym_pred_select", out, thr, nsm);
+  run<8, 8, true, 0, 0, 3>("cohesion_8x8_sym_colblock", out, thr, nsm);
+  run<8, 8, true, 0, 0, 4>("cohesion_8x8_sym_colblock_rowbcast", out, thr, nsm);
   return 0;
 }
