@@ -125,6 +125,26 @@ int read_header(FILE* f, const std::string& path, int* width, uint64_t* n) {
   return PALD_GPU_OK;
 }
 
+// A corrupt header must not wrap n * n * width or truncate (int)n: check the
+// payload against the file before anything is allocated. A file too short
+// for its header is the reference's "truncated payload" (ingest.hpp:243-278
+// fails on the read); a complete file beyond the engine's limit (n > 2^24:
+// counts no longer exact in fp32) is refused. Leaves the file position
+// unchanged.
+int check_payload(FILE* f, const std::string& path, uint64_t n, int width) {
+  const long pos = ftell(f);
+  if (pos < 0 || fseek(f, 0, SEEK_END) != 0) return io_error(PALD_GPU_ERR_IO, path + ": cannot seek");
+  const long end = ftell(f);
+  if (end < 0 || fseek(f, pos, SEEK_SET) != 0) return io_error(PALD_GPU_ERR_IO, path + ": cannot seek");
+  const unsigned __int128 need = (unsigned __int128)n * n * (unsigned)width;
+  if (need > (unsigned __int128)(uint64_t)(end - pos))
+    return io_error(PALD_GPU_ERR_VALIDATION, path + ": truncated payload");
+  if (n > (1ull << 24))
+    return io_error(PALD_GPU_ERR_UNSUPPORTED,
+                    path + ": n = " + std::to_string(n) + " exceeds the engine limit 2^24");
+  return PALD_GPU_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -135,7 +155,9 @@ int pald_gpu_read_binary_header(const char* path, uint64_t* n_out, int32_t* widt
   file.f = fopen(path, "rb");
   if (!file.f) return io_error(PALD_GPU_ERR_IO, std::string("cannot open ") + path);
   int w = 0;
-  const int rc = read_header(file.f, path, &w, n_out);
+  int rc = read_header(file.f, path, &w, n_out);
+  // callers size their buffers from n: refuse a header the payload cannot back
+  if (rc == PALD_GPU_OK && *n_out >= 2) rc = check_payload(file.f, path, *n_out, w);
   if (rc == PALD_GPU_OK && width_out) *width_out = w;
   return rc;
 }
@@ -157,6 +179,7 @@ int pald_gpu_read_distance_binary(const char* path, float* dD, uint64_t ldd, voi
       return io_error(PALD_GPU_ERR_VALIDATION, std::string(path) + ": truncated payload");
     return io_error(PALD_GPU_ERR_VALIDATION, std::string(path) + ": need at least 2 points");
   }
+  if ((rc = check_payload(file.f, path, n, width))) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   // Raw payload on the device (row-major, dense), streamed through a pinned
   // double buffer.

@@ -62,6 +62,16 @@ def test_binary_io_errors(tmp_path):
     p.write_bytes(p.read_bytes()[:-7])
     with pytest.raises(ValidationError, match="truncated payload"):
         read_distance_binary(str(p))
+    # corrupt header: n = 2^32 (n * n * width wraps to 0 in 64 bits) and
+    # n = 2^20 with a 20-point payload -- refused before anything is allocated
+    import struct
+
+    body = p.read_bytes()[14:]
+    for n_bad in (1 << 32, 1 << 20):
+        h = tmp_path / "hdr.bin"
+        h.write_bytes(b"PALD" + struct.pack("<BBQ", 1, 4, n_bad) + body)
+        with pytest.raises(ValidationError, match="truncated payload"):
+            read_distance_binary(str(h))
 
 
 def test_binary_to_engine_end_to_end(oracle, tmp_path):
