@@ -174,14 +174,26 @@ int pald_gpu_cohesion_f32(const float* D, uint64_t n, const pald_gpu_opts* opts,
  * pald_gpu_cohesion_f32 and widening C like collect_result
  * (blocked.hpp:352-359); the conversions run on all host cores into / out
  * of pinned staging buffers that the library keeps between calls
- * (pald_gpu_release_host_staging frees them). begin() returns at once (a
- * worker thread converts D and runs the GPU call) so the caller can build
- * its result storage meanwhile; end() waits and writes U_out (nullable)
- * and C_out. One job at a time per process (begin blocks until the
- * previous job's end). Errors of the GPU call are returned by end(). */
+ * (pald_gpu_release_host_staging frees them), and they are pipelined with
+ * the transfers: each row band of D is converted just before its H2D copy
+ * (which itself overlaps pass 1), and C is widened band by band as the D2H
+ * copies land during pass 2. begin() returns at once (a worker thread runs
+ * the GPU call) so the caller can build its result storage meanwhile;
+ * outputs() (optional, once, any time before end) hands over U_out
+ * (nullable) and C_out so that the widening can start before end();
+ * end() waits for the rest and -- if outputs() was not called -- takes
+ * U_out / C_out itself (its pointer arguments are ignored otherwise). One
+ * job at a time per process (begin blocks until the previous job's end).
+ * Errors of the GPU call are returned by end(). */
 typedef struct pald_gpu_job pald_gpu_job;
 int pald_gpu_cohesion_f64io_begin(const double* D, uint64_t n, const pald_gpu_opts* opts, pald_gpu_job** job);
+int pald_gpu_cohesion_f64io_outputs(pald_gpu_job* job, int32_t* U_out, double* C_out);
 int pald_gpu_cohesion_f64io_end(pald_gpu_job* job, int32_t* U_out, double* C_out, pald_gpu_phase_times* times);
+/* First-touches [p, p + bytes) from all host cores (writes zeros): a caller
+ * that has to build a large zero-filled result (std::vector value-
+ * initialisation is one thread taking one page fault per 4 KiB) can reserve
+ * the storage, prefault it here and then resize. Host memory only. */
+int pald_gpu_host_prefault(void* p, uint64_t bytes);
 int pald_gpu_cohesion_f64io(const double* D, uint64_t n, const pald_gpu_opts* opts, int32_t* U_out,
                             double* C_out, pald_gpu_phase_times* times);
 int pald_gpu_release_host_staging(void);

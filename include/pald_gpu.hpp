@@ -237,10 +237,25 @@ inline PaldResult run(const DistanceMatrix& d, int algorithm, Policy policy, std
       if (j) pald_gpu_cohesion_f64io_end(j, nullptr, nullptr, nullptr);
     }
   } join{job};
-  PaldResult r{FocusSizeMatrix(n), CohesionMatrix(n)};
+  // The result as the reference's types build it (n * n zero-filled
+  // entries): the storage is reserved, first-touched by all host cores
+  // inside the library, then value-initialised by resize() on the resident
+  // pages -- the single-threaded page faults of a fresh 12 GiB result at
+  // n = 32768 would otherwise outlast the GPU work.
+  PaldResult r{FocusSizeMatrix(0), CohesionMatrix(0)};
+  r.focus.n = n;
+  r.cohesion.n = n;
+  r.focus.sizes.reserve(n * n);
+  r.cohesion.values.reserve(n * n);
+  pald_gpu_host_prefault(r.focus.sizes.data(), n * n * sizeof(r.focus.sizes[0]));
+  pald_gpu_host_prefault(r.cohesion.values.data(), n * n * sizeof(r.cohesion.values[0]));
+  r.focus.sizes.resize(n * n);
+  r.cohesion.values.resize(n * n);
+  // C rows are widened into the result as their copies land during pass 2
+  throw_status(pald_gpu_cohesion_f64io_outputs(job, r.focus.sizes.data(), r.cohesion.values.data()));
   pald_gpu_phase_times t{};
   join.j = nullptr;
-  throw_status(pald_gpu_cohesion_f64io_end(job, r.focus.sizes.data(), r.cohesion.values.data(), &t));
+  throw_status(pald_gpu_cohesion_f64io_end(job, nullptr, nullptr, &t));
   if (times) {
     times->focus_seconds += t.focus_seconds;
     times->cohesion_seconds += t.cohesion_seconds;

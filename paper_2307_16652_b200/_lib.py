@@ -47,7 +47,9 @@ EXPORTED_SYMBOLS = (
     "pald_gpu_plan_focus_counts_peers",
     "pald_gpu_plan_cohesion_share_peers",
     "pald_gpu_cohesion_f64io_begin",
+    "pald_gpu_cohesion_f64io_outputs",
     "pald_gpu_cohesion_f64io_end",
+    "pald_gpu_host_prefault",
     "pald_gpu_cohesion_f64io",
     "pald_gpu_release_host_staging",
     "pald_gpu_plan_export_u",
@@ -174,7 +176,9 @@ def load(path: Path | None = None) -> C.CDLL:
         "pald_gpu_plan_focus_counts_peers": (i32, [vp, u64, u64, vp]),
         "pald_gpu_plan_cohesion_share_peers": (i32, [vp, u64, u64, vp]),
         "pald_gpu_cohesion_f64io_begin": (i32, [vp, u64, C.POINTER(Opts), C.POINTER(vp)]),
+        "pald_gpu_cohesion_f64io_outputs": (i32, [vp, vp, vp]),
         "pald_gpu_cohesion_f64io_end": (i32, [vp, vp, vp, C.POINTER(PhaseTimes)]),
+        "pald_gpu_host_prefault": (i32, [vp, u64]),
         "pald_gpu_cohesion_f64io": (i32, [vp, u64, C.POINTER(Opts), vp, vp, C.POINTER(PhaseTimes)]),
         "pald_gpu_release_host_staging": (i32, []),
         "pald_gpu_plan_export_u": (i32, [vp, C.POINTER(IpcHandle)]),

@@ -38,6 +38,40 @@ namespace {
 
 thread_local std::string g_last_error;
 
+// Hooks of the f64io entry points (pald_internal.h), per calling thread.
+thread_local pald_gpu_host_hooks t_hooks{nullptr, nullptr, nullptr, nullptr};
+inline void hook_rows_needed(uint64_t r0, uint64_t r1) {
+  if (t_hooks.rows_needed) t_hooks.rows_needed(t_hooks.ctx, r0, r1);
+}
+// Host callbacks queued behind the D2H copies (payloads live in the plan-independent
+// static pool below: one call at a time per thread, <= 64 bands).
+struct LandedMsg {
+  pald_gpu_host_hooks hooks;
+  uint64_t r1;
+};
+void CUDART_CB cb_c_rows_landed(void* m) {
+  auto* msg = static_cast<LandedMsg*>(m);
+  msg->hooks.c_rows_landed(msg->hooks.ctx, msg->r1);
+}
+void CUDART_CB cb_u_landed(void* m) {
+  auto* msg = static_cast<LandedMsg*>(m);
+  msg->hooks.u_landed(msg->hooks.ctx);
+}
+thread_local LandedMsg t_msgs[80];
+thread_local int t_msg_next = 0;
+// Queue "rows [0, r1) of C_out landed" (r1 > 0) or "U_out landed" (r1 == 0)
+// behind the copies already on `sc`.
+int queue_landed(cudaStream_t sc, uint64_t r1) {
+  if (r1 ? !t_hooks.c_rows_landed : !t_hooks.u_landed) return PALD_GPU_OK;
+  LandedMsg* m = &t_msgs[t_msg_next++ % 80];
+  m->hooks = t_hooks;
+  m->r1 = r1;
+  if (cudaLaunchHostFunc(sc, r1 ? cb_c_rows_landed : cb_u_landed, m) != cudaSuccess) {
+    cudaGetLastError();  // hooks are an optimisation: the caller converts the rest at the end
+  }
+  return PALD_GPU_OK;
+}
+
 int set_error(int code, const char* fmt, ...) {
   char buf[512];
   va_list ap;
@@ -1600,6 +1634,7 @@ int load_focus_banded(pald_gpu_plan* p, const float* D, cudaStream_t s, cudaStre
   cudaEvent_t* ev = p->band_ev.data();
   for (int b = 0; b < nbands; ++b) {
     const int r0 = b * band_rows, r1 = std::min(n, r0 + band_rows);
+    hook_rows_needed((uint64_t)r0, (uint64_t)r1);  // f64io: this band converted just in time
     PALD_CUDA(cudaMemcpy2DAsync(p->c + (size_t)r0 * ld, (size_t)ld * 4, D + (size_t)r0 * n, (size_t)n * 4,
                                 (size_t)n * 4, r1 - r0, cudaMemcpyHostToDevice, sc));
     PALD_CUDA(cudaEventRecord(ev[b], sc));
@@ -2015,14 +2050,17 @@ int pald_gpu_cohesion_f32(const float* D, uint64_t n, const pald_gpu_opts* o_in,
     if ((rc = load_focus_banded(p, D, s, sc, s2))) return rc;
     if ((rc = plan_focus_finish_impl(p, s))) return rc;
   } else {
+    hook_rows_needed(0, n);
     if ((rc = pald_gpu_plan_load_host(p, D, s))) return rc;
     PALD_CUDA(cudaEventRecord(ev[1], s));
     if ((rc = plan_focus_impl(p, s))) return rc;
   }
   PALD_CUDA(cudaEventRecord(ev[2], s));
+  t_msg_next = 0;
   if (U_out) {
     PALD_CUDA(cudaStreamWaitEvent(sc, ev[2], 0));
     PALD_CUDA(cudaMemcpy2DAsync(U_out, n * 4, p->u, p->ld * 4, n * 4, n, cudaMemcpyDeviceToHost, sc));
+    queue_landed(sc, 0);
   }
   if (p->sym_ready && sym_preferred(p)) {
     const bool acc = accurate(p);
@@ -2049,6 +2087,7 @@ int pald_gpu_cohesion_f32(const float* D, uint64_t n, const pald_gpu_opts* o_in,
       const uint64_t r0 = (uint64_t)g_row0 * kTile, r1 = std::min(n, (uint64_t)g1 * kTile);
       PALD_CUDA(cudaMemcpy2DAsync(C_out + r0 * n, n * 4, p->c + r0 * p->ld, p->ld * 4, n * 4, r1 - r0,
                                   cudaMemcpyDeviceToHost, sc));
+      queue_landed(sc, r1);
       t0 = t1;
       g_row0 = g1;
       ++band;
@@ -2065,6 +2104,7 @@ int pald_gpu_cohesion_f32(const float* D, uint64_t n, const pald_gpu_opts* o_in,
       PALD_CUDA(cudaStreamWaitEvent(sc, ev[4 + nb_used], 0));
       PALD_CUDA(cudaMemcpy2DAsync(C_out + r0 * n, n * 4, p->c + r0 * p->ld, p->ld * 4, n * 4, r1 - r0,
                                   cudaMemcpyDeviceToHost, sc));
+      queue_landed(sc, r1);
     }
   }
   PALD_CUDA(cudaEventRecord(ev[3], s));
@@ -2115,6 +2155,10 @@ int pald_gpu_points_to_distances(const double* dP, uint64_t n, uint64_t dim, flo
 }
 
 }  // extern "C"
+
+void pald_gpu_set_host_hooks(const pald_gpu_host_hooks* hooks) {
+  t_hooks = hooks ? *hooks : pald_gpu_host_hooks{nullptr, nullptr, nullptr, nullptr};
+}
 
 int pald_gpu_set_error(int code, const char* message) {
   g_last_error = message;
