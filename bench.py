@@ -226,11 +226,25 @@ def cpu_reference_sample(d_host: np.ndarray, budget_s: float, cores: int, anchor
         if rc:
             raise RuntimeError(msg)
         da = da64.astype(np.float32)
-        t_est, asmp = ref_estimate(ref, da, b, cores, 8.0, ref.pairwise_overhead_f32(anchor_n))
-        _, _, tt = ref.parallel_pairwise(da.astype(np.float64), b, cores, use_float=True)
-        full = float(tt[3])
-        info["anchor"] = {"n": anchor_n, "full_run_s": full, "phase_times_s": [float(x) for x in tt],
-                          "estimate_s": t_est, "estimate_blocks": asmp["block_pairs"],
+        # estimate / full / estimate / full / estimate: the host's speed
+        # drifts by several per cent between runs (shared box:
+        # profiles/anchor_repeat_r02.jsonl), so the full calls are interleaved
+        # with estimates over different block pairs and the means compared
+        ov = ref.pairwise_overhead_f32(anchor_n)
+        ests, fulls, blocks, t1a, tt = [], [], [], None, None
+        for rep in range(3):
+            t_e, asmp = ref_estimate(ref, da, b, cores, 5.0, ov, rotate=2 * rep, t1=t1a)
+            t1a = asmp["t1"]
+            ests.append(t_e)
+            blocks.append(asmp["block_pairs"])
+            if rep < 2:
+                _, _, tt = ref.parallel_pairwise(da.astype(np.float64), b, cores, use_float=True)
+                fulls.append(float(tt[3]))
+        t_est, full = statistics.mean(ests), statistics.mean(fulls)
+        info["anchor"] = {"n": anchor_n, "full_run_s": full, "full_runs_s": fulls,
+                          "phase_times_s": [float(x) for x in tt],
+                          "estimate_s": t_est, "estimates_s": ests, "estimate_blocks": blocks,
+                          "order": "estimate, full, estimate, full, estimate",
                           "rel_error": (t_est - full) / full,
                           "input": "points i.i.d. U[0,1)^3 (config-5 generator at n=%d), reference "
                                    "points_to_distances" % anchor_n}
@@ -516,7 +530,7 @@ def main() -> None:
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=5, help="BASELINE.json config index (1-5)")
     ap.add_argument("--seed", type=int, default=20230731)
-    ap.add_argument("--cpu-budget", type=float, default=30.0, help="seconds of CPU baseline sample")
+    ap.add_argument("--cpu-budget", type=float, default=24.0, help="seconds of CPU baseline sample")
     ap.add_argument("--ref-step-s", type=float, default=4.0, help="seconds per --impl reference step")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--alg", default="pairwise")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--oneshot", action="store_true", help="time pald_gpu_cohesion_f32_device instead")
+    ap.add_argument("--accurate", action="store_true", help="PALD_GPU_FLAG_ACCURATE (k-block items)")
     a = ap.parse_args()
     import ctypes as C
 
@@ -51,7 +52,7 @@ def main():
         print(json.dumps({"config": a.config, "alg": a.alg, "oneshot_ms": e0.elapsed_time(e1) / a.iters,
                           "env": {k: v for k, v in os.environ.items() if k.startswith("PALD_GPU")}}))
         return
-    eng = Engine(n, a.alg)
+    eng = Engine(n, a.alg, accurate=a.accurate)
     for _ in range(3):
         eng.run(D)
     torch.cuda.synchronize()
@@ -67,7 +68,7 @@ def main():
     torch.cuda.synchronize()
     med = lambda i, j: statistics.median(e[i].elapsed_time(e[j]) for e in evs)  # noqa: E731
     print(json.dumps({"config": a.config, "alg": a.alg, "n": n, "step_ms": med(0, 3), "load_ms": med(0, 1),
-                      "focus_ms": med(1, 2), "cohesion_ms": med(2, 3), "info": eng.info(),
+                      "focus_ms": med(1, 2), "cohesion_ms": med(2, 3), "accurate": a.accurate, "info": eng.info(),
                       "env": {k: v for k, v in os.environ.items() if k.startswith("PALD_GPU")}}))
 
 
