@@ -334,12 +334,6 @@ int check_opts(const pald_gpu_opts* o) {
 #endif
 #define PALD_HOST_BANDS_MAX PALD_HOST_BANDS
 
-struct ItemList {
-  int4* items = nullptr;
-  int count = 0;
-  int grid = 0;
-};
-
 // ---------------------------------------------------------------------------
 struct pald_gpu_plan {
   int device = 0;
@@ -411,7 +405,6 @@ struct pald_gpu_plan {
   // Accurate mode (PALD_GPU_FLAG_ACCURATE): double sums of the fp32 block
   // partials of pass 2 (n x ld doubles, allocated on first use).
   double* c64 = nullptr;
-  std::map<long long, ItemList> acc_lists;  // accurate-mode item lists per pair range
   // One-shot host API (pald_gpu_cohesion_f32): its streams and events,
   // created on first use and kept with the cached plan.
   cudaStream_t os_s = nullptr, os_sc = nullptr, os_s2 = nullptr;
@@ -472,7 +465,6 @@ struct pald_gpu_plan {
       cudaFree(sp.partial);
     }
     cudaFree(c64);
-    for (auto& kv : acc_lists) cudaFree(kv.second.items);
     for (cudaStream_t st : {os_s, os_sc, os_s2})
       if (st) cudaStreamDestroy(st);
     for (cudaEvent_t e : os_ev)
@@ -521,14 +513,10 @@ bool split_enabled() {
 // blocks 2.1e-7 / 3.9e-7 max rel_diff vs fp64, 1024 7.4e-7 / 1.4e-6, 4096
 // 2.8e-6 / 1.0e-5 (the plain fp32 chain: 5.4e-6 / 1.3e-5); the flush of a
 // block costs one reduction per output, outside the inner loop.
-int acc_block_terms() {
-  static const int t = [] {
-    const char* e = getenv("PALD_GPU_ACC_BLOCK");
-    const int v = e ? atoi(e) : 1024;
-    return v >= kSymBK ? v : 1024;
-  }();
-  return t;
-}
+// Longer blocks were measured at n = 32768 (profiles/acc_block_cfg5_r02.txt):
+// 4096-term blocks save 1.5 % of pass 2 but triple the error (1.3e-6) and
+// lose the 1e-7 conservation of sum(C); the default stays 1024 for every n.
+int acc_block_terms(const pald_gpu_plan* p);
 // Triplet C is a tolerance result (the reference's own fp32 triplet C
 // depends on b_cohesion), so the triplet always accumulates accurately: one
 // 4096-term fp32 chain already drifts by 1.3e-5 on config 2 (full matrix vs
@@ -540,6 +528,15 @@ bool accurate(const pald_gpu_plan* p) {
     return e && atoi(e) != 0;
   }();
   return (p->flags & PALD_GPU_FLAG_ACCURATE) != 0 || (p->algorithm == PALD_GPU_TRIPLET && !tri_fp32);
+}
+
+int acc_block_terms(const pald_gpu_plan* p) {
+  static const int env = [] {
+    const char* e = getenv("PALD_GPU_ACC_BLOCK");
+    return e ? atoi(e) : 0;
+  }();
+  (void)p;
+  return env >= kSymBK ? env : 1024;
 }
 
 int ensure_c64(pald_gpu_plan* p) {
@@ -1154,7 +1151,7 @@ int launch_cohesion(pald_gpu_plan* p, uint64_t row0, uint64_t row1, cudaStream_t
     int rc = ensure_c64(p);
     if (rc) return rc;
     a.c64 = p->c64;
-    a.acc_chunks = std::max(1, acc_block_terms() / kBK);
+    a.acc_chunks = std::max(1, acc_block_terms(p) / kBK);
     if (!p->exact) {
       return tri     ? launch_tile<1, true, true, false, true, true, false, TILE, false, false, false, true>(md, mn, mw, a, grid, s)
              : split ? launch_tile<1, false, false, false, false, true, true, TILE, false, false, false, true>(md, mn, mw, a, grid, s)
@@ -1192,7 +1189,7 @@ int launch_cohesion_list(pald_gpu_plan* p, const int2* list, int count, cudaStre
     int rc = ensure_c64(p);
     if (rc) return rc;
     a.c64 = p->c64;
-    a.acc_chunks = std::max(1, acc_block_terms() / kBK);
+    a.acc_chunks = std::max(1, acc_block_terms(p) / kBK);
     if (tri) return launch_tile<1, true, true, false, true, true, false, TILE, true, false, false, true>(md, mn, mw, a, grid, s);
     return launch_tile<1, false, true, false, false, true, false, TILE, true, false, false, true>(md, mn, mw, a, grid, s);
   }
@@ -1201,36 +1198,6 @@ int launch_cohesion_list(pald_gpu_plan* p, const int2* list, int count, cudaStre
 }
 int launch_tail(pald_gpu_plan* p, const int2* list, int count, cudaStream_t s) {
   return p->tail_tile == 32 ? launch_cohesion_list<32>(p, list, count, s) : launch_cohesion_list<64>(p, list, count, s);
-}
-
-// Accurate mode: pairs [t0, t1) of the grouped order as k-block items, in
-// the CTA assignment of the whole-pair kernel (CTA g: pairs t0 + g, + G, ...)
-// so each pair stays on one CTA, its blocks consecutive; cached per range.
-int acc_items(pald_gpu_plan* p, int t0, int t1, const ItemList** out) {
-  const long long key = ((long long)t0 << 32) | (unsigned)t1;
-  auto it = p->acc_lists.find(key);
-  if (it == p->acc_lists.end()) {
-    const int G = std::min(t1 - t0, p->sms), nch = p->sym_nch, ac = std::max(1, acc_block_terms() / kSymBK);
-    std::vector<std::vector<int4>> queue(G);
-    for (int i = t0; i < t1; ++i) {
-      const int2 pr = p->pair_order[i];
-      for (int cb = 0; cb < nch; cb += ac)
-        queue[(i - t0) % G].push_back(make_int4(pr.x, pr.y, cb | (std::min(nch, cb + ac) << 15), -1));
-    }
-    size_t R = 0;
-    for (auto& q : queue) R = std::max(R, q.size());
-    std::vector<int4> items(R * G, make_int4(0, 0, 0, -1));  // empty padding items
-    for (int g = 0; g < G; ++g)
-      for (size_t r = 0; r < queue[g].size(); ++r) items[r * G + g] = queue[g][r];
-    ItemList il;
-    PALD_CUDA(cudaMalloc(&il.items, items.size() * sizeof(int4)));
-    PALD_CUDA(cudaMemcpy(il.items, items.data(), items.size() * sizeof(int4), cudaMemcpyHostToDevice));
-    il.count = (int)items.size();
-    il.grid = G;
-    it = p->acc_lists.emplace(key, il).first;
-  }
-  *out = &it->second;
-  return PALD_GPU_OK;
 }
 
 int launch_sym(pald_gpu_plan* p, int t0, int t1, cudaStream_t s, bool peers = false,
@@ -1246,8 +1213,8 @@ int launch_sym(pald_gpu_plan* p, int t0, int t1, cudaStream_t s, bool peers = fa
     PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
     PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
     PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
-    PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<false, false, false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
-    PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<true, false, false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
+    PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<false, false, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
+    PALD_CUDA(cudaFuncSetAttribute(pald_sym_cohesion_kernel<true, false, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem));
     attr_done[p->device & 63] = true;
   }
   int grid = std::min(t1 - t0, p->sms);
@@ -1272,24 +1239,16 @@ int launch_sym(pald_gpu_plan* p, int t0, int t1, cudaStream_t s, bool peers = fa
             (int)p->n, (int)p->ld, (int)p->nb, p->sym_nch, t0, t1, p->peer_c,
             sync ? p->round_bar : nullptr};
   a.c64 = p->c64;
-  a.acc_chunks = std::max(1, acc_block_terms() / kSymBK);
+  a.acc_chunks = std::max(1, acc_block_terms(p) / kSymBK);
   a.tri_marks = p->tri_marks ? 1 : 0;
   const bool tri = p->algorithm == PALD_GPU_TRIPLET;
-  if (acc) {
-    // accurate mode: the k blocks of the pairs [t0, t1) as an explicit item
-    // list (the lean SPLIT-form kernel); the kernel only adds into the
-    // double sums, so PEERS stores are the rounding pass's job
-    const ItemList* il = nullptr;
-    int rc = acc_items(p, t0, t1, &il);
-    if (rc) return rc;
-    a.items = il->items;
-    a.tile_begin = 0;
-    a.tile_end = il->count;
-    grid = il->grid;
-  }
+  // accurate mode: whole pairs on the same persistent schedule; the kernel
+  // flushes its fp32 sums into the double sums every acc_chunks chunks (the
+  // chunk loop stays uniform, so the main loop is the plain kernel's) and
+  // only adds into c64: PEERS stores are the rounding pass's job
   (void)peers;
-  auto k = acc ? (tri ? pald_sym_cohesion_kernel<true, false, false, true, true>
-                      : pald_sym_cohesion_kernel<false, false, false, true, true>)
+  auto k = acc ? (tri ? pald_sym_cohesion_kernel<true, false, false, false, true>
+                      : pald_sym_cohesion_kernel<false, false, false, false, true>)
            : sync ? (peers ? (tri ? pald_sym_cohesion_kernel<true, true, true> : pald_sym_cohesion_kernel<false, true, true>)
                         : (tri ? pald_sym_cohesion_kernel<true, false, true> : pald_sym_cohesion_kernel<false, false, true>))
                 : (peers ? (tri ? pald_sym_cohesion_kernel<true, true> : pald_sym_cohesion_kernel<false, true>)
@@ -1314,8 +1273,9 @@ int launch_sym(pald_gpu_plan* p, int t0, int t1, cudaStream_t s, bool peers = fa
 // full-range pair launch can be split along k into f parts whose partial
 // tiles are summed in a fixed order: ceil(L f / G) / f rounds instead of 1.
 // Items: (tile row, tile col, cb | ce << 15, slot); CTA g runs items g,
-// g + G, ... In accurate mode every whole pair and every split part is a run
-// of k blocks (acc_chunks chunks) on one CTA, all added into the double sums
+// g + G, ... In accurate mode the whole pairs of the full rounds run on the
+// whole-pair kernel and the list holds only the split parts, each a run of k
+// blocks (acc_chunks chunks) on one CTA, all added into the double sums
 // (order-independent), the queues padded with empty items.
 int build_split(pald_gpu_plan* p, bool acc) {
   auto& sp = p->split[acc ? 1 : 0];
@@ -1346,12 +1306,11 @@ int build_split(pald_gpu_plan* p, bool acc) {
       for (int q = 0; q < f; ++q)
         items.push_back(make_int4(prs[j].x, prs[j].y, z(nch * q / f, nch * (q + 1) / f, q == 0, false), j * f + q));
   } else {
-    const int ac = std::max(1, acc_block_terms() / kSymBK);
+    // accurate mode: the whole pairs of the full rounds run on the whole-pair
+    // kernel (launch_sym); the list holds only the split parts, each cut
+    // into k blocks (acc_chunks chunks) that flush into the double sums
+    const int ac = std::max(1, acc_block_terms(p) / kSymBK);
     std::vector<std::vector<int4>> queue(G);
-    for (int i = 0; i < pairs - L; ++i)  // whole pairs: CTA i % G, as the implicit order
-      for (int cb = 0; cb < nch; cb += ac)
-        queue[i % G].push_back(make_int4(order[i].x, order[i].y, z(cb, std::min(nch, cb + ac), cb == 0,
-                                                                     cb + ac >= nch), -1));
     for (int t = 0; t < L * f; ++t) {  // split parts: CTA t % G
       const int j = t / f, q = t % f, pb = nch * q / f, pe = nch * (q + 1) / f;
       for (int cb = pb; cb < pe; cb += ac)
@@ -1394,10 +1353,15 @@ int launch_sym_split(pald_gpu_plan* p, cudaStream_t s, bool* used) {
     attr_done[p->device & 63] = true;
   }
   int rc;
-  if (acc && (rc = acc_zero_rows(p, 0, p->n, s))) return rc;
+  if (acc) {  // full rounds on the whole-pair kernel, then the split parts of the last round
+    if ((rc = acc_zero_rows(p, 0, p->n, s))) return rc;
+    const int pairs = (int)p->pair_order.size();
+    if ((rc = launch_sym(p, 0, pairs - sp.pair_count, s, false, false))) return rc;
+    ++p->launches;
+  }
   SymArgs a{p->ds, p->c, p->focus_tiles, p->sym_masks, p->sym_tile_flags, (int)p->n, (int)p->ld, (int)p->nb,
             p->sym_nch, 0, sp.item_count, p->peer_c, nullptr, sp.items,
-            acc ? nullptr : static_cast<float*>(sp.partial), p->c64, std::max(1, acc_block_terms() / kSymBK),
+            acc ? nullptr : static_cast<float*>(sp.partial), p->c64, std::max(1, acc_block_terms(p) / kSymBK),
             p->tri_marks ? 1 : 0};
   const int grid = std::min(sp.item_count, p->sms);
   k<<<grid, kThreads, kSymSmem, s>>>(p->tm_d32, p->tm_dnu32, p->tm_w32, a);

@@ -404,8 +404,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nch = args.nch;
   const int G = gridDim.x, g = blockIdx.x;
   const int first = args.tile_begin + g;
-  // ACC (accurate mode) always runs on an item list of k blocks (SPLIT form)
-  static_assert(!ACC || SPLIT, "accurate mode: item lists only");
+  // ACC (accurate mode): whole pairs flush their fp32 sums into the double
+  // sums every acc_chunks chunks inside the (uniform) chunk loop; SPLIT item
+  // lists (the triplet's split last round) are cut into k blocks by the host
+  // and flush at the end of each item.
   const int R = first < args.tile_end ? (args.tile_end - 1 - first) / G + 1 : 0;
   // item ri of this CTA: tile pair and chunk range [cb, ce) (whole pairs
   // unless SPLIT). SPLIT items come from the host's list: (tile row, tile
@@ -461,7 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_load_2d(st + 2 * kSymBox, &tm_w, r0, k0, &full_bar[s]);
     tma_load_2d(st + 3 * kSymBox, &tm_w, c0, k0, &full_bar[s]);
   };
-  constexpr bool ITEMS = SPLIT || ACC;  // items other than whole pairs
+  constexpr bool ITEMS = SPLIT;  // items other than whole pairs
   int pr_ri = 0, pr_ch = 0, pr_end = nch;
   auto pr_load = [&]() {  // the next non-empty item at or after pr_ri
     for (; pr_ri < R; ++pr_ri) {
@@ -490,6 +492,43 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = tid >> 5, lane = tid & 31;
   const int ty = (warp >> 1) * 4 + (lane >> 3);
   const int tx = (warp & 1) * 8 + (lane & 7);
+
+  // Accurate mode: the thread's fp32 partial sums of both output tiles added
+  // into the double sums with red.global.add.f64 (exact, order-independent,
+  // no result to wait for). Measured alternatives at n = 32768 (pass 2, plain
+  // kernel 2479 ms): these reductions 2637 ms; a plain vectorised load / add /
+  // store (a whole pair owns its tiles) 2701 ms -- the loads' latency shows as
+  // long-scoreboard stalls; sector-coalesced reductions after a 4 x 4 shuffle
+  // transpose 2685 ms.
+  auto add4 = [&](double* p4, float a, float b, float c, float d) { acc_red4(p4, a, b, c, d); };
+  auto flush64 = [&](float2 (&acc)[8][4], float2 (&act)[8][4], int r0, int c0, bool diag) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = r0 + row_off<kTile>(ty, i);
+      if (r >= n) continue;
+      double* prow = args.c64 + (size_t)r * ld;
+      const int ca = c0 + tx * 4, cb = c0 + 64 + tx * 4;
+      if (ca < n) add4(prow + ca, acc[i][0].x, acc[i][0].y, acc[i][1].x, acc[i][1].y);
+      if (cb < n) add4(prow + cb, acc[i][2].x, acc[i][2].y, acc[i][3].x, acc[i][3].y);
+    }
+    if (!diag) {  // the diagonal pair's direct tile holds every entry
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int c = c0 + row_off<kTile>(tx, j);
+        if (c >= n) continue;
+        double* prow = args.c64 + (size_t)c * ld;
+        const int ra = r0 + ty * 4, rb = r0 + 64 + ty * 4;
+        const int jp = j >> 1;
+        const bool hi = (j & 1) != 0;
+        if (ra < n)
+          add4(prow + ra, hi ? act[0][jp].y : act[0][jp].x, hi ? act[1][jp].y : act[1][jp].x,
+               hi ? act[2][jp].y : act[2][jp].x, hi ? act[3][jp].y : act[3][jp].x);
+        if (rb < n)
+          add4(prow + rb, hi ? act[4][jp].y : act[4][jp].x, hi ? act[5][jp].y : act[5][jp].x,
+               hi ? act[6][jp].y : act[6][jp].x, hi ? act[7][jp].y : act[7][jp].x);
+      }
+    }
+  };
 
   int p = 0;
   for (int ri = 0; ri < R; ++ri) {
@@ -567,6 +606,22 @@ __global__ void __launch_bounds__(kThreads, 1)
           issue(pr_ri, pr_ch, s);
         pr_advance();
       }
+      if constexpr (ACC && !SPLIT) {  // k block done (not the last: that is the flush below)
+        if ((ch + 1) % args.acc_chunks == 0 && ch + 1 < ch_e) {
+          flush64(acc, act, r0, c0, diag);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int jp = 0; jp < 4; ++jp) {
+              acc[i][jp] = make_float2(0.f, 0.f);
+              act[i][jp] = make_float2(0.f, 0.f);
+            }
+        }
+      }
+    }
+    if constexpr (ACC) {  // into the double sums (rounded by acc_round_*_kernel)
+      flush64(acc, act, r0, c0, diag);
+      continue;
     }
     if (SPLIT && !ACC && slot >= 0) {  // partial tiles: [0] rows of P x cols of Q, [1] rows of Q x cols of P
       float* pt = args.partial + (size_t)slot * 2 * kTile * kTile;
@@ -619,11 +674,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const size_t rowo = (size_t)r * ld;
       const int ca = c0 + tx * 4, cb = c0 + 64 + tx * 4;
-      if constexpr (ACC) {  // k block done: into the double sums (rounded by acc_round_pairs_kernel)
-        if (ca < n) acc_red4(args.c64 + rowo + ca, acc[i][0].x, acc[i][0].y, acc[i][1].x, acc[i][1].y);
-        if (cb < n) acc_red4(args.c64 + rowo + cb, acc[i][2].x, acc[i][2].y, acc[i][3].x, acc[i][3].y);
-        continue;
-      }
       if (ca < n)
         store_c4<PEERS>(args, rowo + ca, make_float4(acc[i][0].x, acc[i][0].y, acc[i][1].x, acc[i][1].y));
       if (cb < n)
@@ -639,17 +689,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         const size_t rowo = (size_t)c * ld;
         const int ra = r0 + ty * 4, rb = r0 + 64 + ty * 4;
         const int jp = j >> 1;
-        if constexpr (ACC) {
-          double* prow = args.c64 + rowo;
-          const bool hi = (j & 1) != 0;
-          if (ra < n)
-            acc_red4(prow + ra, hi ? act[0][jp].y : act[0][jp].x, hi ? act[1][jp].y : act[1][jp].x,
-                     hi ? act[2][jp].y : act[2][jp].x, hi ? act[3][jp].y : act[3][jp].x);
-          if (rb < n)
-            acc_red4(prow + rb, hi ? act[4][jp].y : act[4][jp].x, hi ? act[5][jp].y : act[5][jp].x,
-                     hi ? act[6][jp].y : act[6][jp].x, hi ? act[7][jp].y : act[7][jp].x);
-          continue;
-        }
         if ((j & 1) == 0) {
           if (ra < n)
             store_c4<PEERS>(args, rowo + ra, make_float4(act[0][jp].x, act[1][jp].x, act[2][jp].x, act[3][jp].x));
