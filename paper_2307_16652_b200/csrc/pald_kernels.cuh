@@ -417,14 +417,17 @@ __device__ __forceinline__ void k_step_split(const float* __restrict__ sa, const
 // = 4 integer instructions per 2 output combos (vs 5 on the fp32 path).
 // thr[i][jp] holds -RR (.x) and -CR (.y) packed per column pair, acc .x the
 // packed counts.
+// (pa, pb: the thread's first A / B words of the chunk, i.e. the stage's
+// RA rows + ty and RB rows + tx: the k loop then only adds constants to two
+// pointers -- the stage base is not a uniform value in the stream-K kernel)
 template <int TT = 8>
-__device__ __forceinline__ void k_step_rank(const uint32_t* __restrict__ sa, const uint16_t* __restrict__ sb,
-                                            int kk, int ty, int tx, const float2 (&thr)[TT][TT / 2],
+__device__ __forceinline__ void k_step_rank(const uint4* __restrict__ pa, const uint2* __restrict__ pb,
+                                            int kk, const float2 (&thr)[TT][TT / 2],
                                             float2 (&acc)[TT][TT / 2]) {
-  const uint4 a0 = reinterpret_cast<const uint4*>(sa + kk * kTile)[ty];
-  const uint4 a1 = reinterpret_cast<const uint4*>(sa + kk * kTile)[16 + ty];
-  const uint2 b0 = reinterpret_cast<const uint2*>(sb + kk * kTile)[tx];
-  const uint2 b1 = reinterpret_cast<const uint2*>(sb + kk * kTile)[16 + tx];
+  const uint4 a0 = pa[kk * (kTile / 4)];
+  const uint4 a1 = pa[kk * (kTile / 4) + 16];
+  const uint2 b0 = pb[kk * (kTile / 4)];
+  const uint2 b1 = pb[kk * (kTile / 4) + 16];
   const uint32_t a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
   const uint32_t b[4] = {b0.x, b0.y, b1.x, b1.y};
 #pragma unroll
@@ -791,11 +794,15 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE, RANK))
         }
         if (sel) {
           for (int kk = 0; kk < kmax; ++kk) k_step_rank_sel(ra, rb, kk, k0 + kk, ty, tx, r0, c0, a_in, b_in, thr, acc);
-        } else if (kmax == kBK) {
-#pragma unroll kRankUnroll
-          for (int kk = 0; kk < kBK; ++kk) k_step_rank(ra, rb, kk, ty, tx, thr, acc);
         } else {
-          for (int kk = 0; kk < kmax; ++kk) k_step_rank(ra, rb, kk, ty, tx, thr, acc);
+          const uint4* pa = reinterpret_cast<const uint4*>(ra) + ty;
+          const uint2* pb = reinterpret_cast<const uint2*>(rb) + tx;
+          if (kmax == kBK) {
+#pragma unroll kRankUnroll
+            for (int kk = 0; kk < kBK; ++kk) k_step_rank(pa, pb, kk, thr, acc);
+          } else {
+            for (int kk = 0; kk < kmax; ++kk) k_step_rank(pa, pb, kk, thr, acc);
+          }
         }
       } else if (PASS == 1 && SPLIT) {
         for (int kk = 0; kk < kmax; ++kk) k_step_split<FAST, TILE>(sa, sb, sw, kk, ty, tx, thr, acc);
