@@ -57,6 +57,9 @@ constexpr int kKUnroll = PALD_KUNROLL;
 #define PALD_RANK_UNROLL 2  // (tools/microbench4.cu), the 255-register kernel 2-4 (8: -1.2 %)
 #endif
 constexpr int kRankUnroll = PALD_RANK_UNROLL;
+#ifndef PALD_RANK_BUMP  // 1: the k loop bumps the two operand pointers instead of indexing by kk
+#define PALD_RANK_BUMP 1  // n = 32768 pass 1: 1236 -> 1202 ms (unroll 4: 1218, 4 + bump: 1273;
+#endif                    // profiles/rank_loop_variants_r02.txt)
 #ifndef PALD_K_ORDER  // k-step instruction order: 0 rows outer, 1 column pairs outer
 #define PALD_K_ORDER 0
 #endif
@@ -798,8 +801,18 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(TILE, RANK))
           const uint4* pa = reinterpret_cast<const uint4*>(ra) + ty;
           const uint2* pb = reinterpret_cast<const uint2*>(rb) + tx;
           if (kmax == kBK) {
+#if PALD_RANK_BUMP
+#pragma unroll 1
+            for (int it = 0; it < kBK / kRankUnroll; ++it) {
+#pragma unroll
+              for (int u = 0; u < kRankUnroll; ++u) k_step_rank(pa, pb, u, thr, acc);
+              pa += kRankUnroll * (kTile / 4);
+              pb += kRankUnroll * (kTile / 4);
+            }
+#else
 #pragma unroll kRankUnroll
             for (int kk = 0; kk < kBK; ++kk) k_step_rank(pa, pb, kk, thr, acc);
+#endif
           } else {
             for (int kk = 0; kk < kmax; ++kk) k_step_rank(pa, pb, kk, thr, acc);
           }
