@@ -233,7 +233,7 @@ def cpu_reference_sample(d_host: np.ndarray, budget_s: float, cores: int, anchor
         ov = ref.pairwise_overhead_f32(anchor_n)
         ests, fulls, blocks, t1a, tt = [], [], [], None, None
         for rep in range(3):
-            t_e, asmp = ref_estimate(ref, da, b, cores, 5.0, ov, rotate=2 * rep, t1=t1a)
+            t_e, asmp = ref_estimate(ref, da, b, cores, 4.0, ov, rotate=2 * rep, t1=t1a)
             t1a = asmp["t1"]
             ests.append(t_e)
             blocks.append(asmp["block_pairs"])
@@ -412,8 +412,9 @@ def shim_e2e(cfg, seed: int, steps: int, warmup: int, devices=None):
     pald::gpu::parallel_pairwise<float>(pald::DistanceMatrix, b, plan) built
     against the reference's own types (tools/_bin/shim_bench): double D in,
     a freshly allocated PaldResult (int32 U, double C) out, wall clock per
-    call. D is built from the same seeded points with the reference's own
-    points_to_distances (outside the timed region)."""
+    call. D is built from the same seeded points with the arithmetic of the
+    reference's points_to_distances on all host cores and validated by the
+    reference's DistanceMatrix constructor (outside the timed region)."""
     from paper_2307_16652_b200 import datagen
 
     exe = ROOT / "tools" / "_bin" / "shim_bench"
@@ -533,7 +534,7 @@ def main() -> None:
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=5, help="BASELINE.json config index (1-5)")
     ap.add_argument("--seed", type=int, default=20230731)
-    ap.add_argument("--cpu-budget", type=float, default=24.0, help="seconds of CPU baseline sample")
+    ap.add_argument("--cpu-budget", type=float, default=16.0, help="seconds of CPU baseline sample")
     ap.add_argument("--ref-step-s", type=float, default=4.0, help="seconds per --impl reference step")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -546,6 +547,7 @@ def main() -> None:
         run_reference_arm(args)
         return
 
+    t_main0 = time.perf_counter()
     import torch
     import torch.distributed as dist
     from paper_2307_16652_b200.distributed import ShardedRunner
@@ -632,8 +634,10 @@ def main() -> None:
                      "note": "share of (tile pair, k) steps of the pair kernel on the per-element exact step"},
     }
 
+    sections = {"setup_and_timed_steps": time.perf_counter() - t_main0}
     if rank == 0 and world == 1:
         if not args.no_e2e:
+            t_sec = time.perf_counter()
             try:
                 ev, et, _ = e2e_host(n, D, max(1, min(args.steps, 3)), 1)
                 line["e2e"] = {"value": ev, "unit": "triplets/s", "seconds_per_step": et,
@@ -641,11 +645,15 @@ def main() -> None:
                                "path": "pald_gpu_cohesion_f32 (C ABI), pinned host buffers"}
             except Exception as e:  # report, never hide
                 line["e2e"] = {"value": None, "error": repr(e)}
+            sections["e2e"] = time.perf_counter() - t_sec
+            t_sec = time.perf_counter()
             try:
                 line["shim_e2e"] = shim_e2e(cfg, args.seed, max(1, min(args.steps, 2)), 1)
             except Exception as e:
                 line["shim_e2e"] = {"value": None, "error": repr(e)}
+            sections["shim_e2e"] = time.perf_counter() - t_sec
         if not args.no_cpu_baseline:
+            t_sec = time.perf_counter()
             try:
                 from oracle.oracle import host_cores
 
@@ -657,10 +665,14 @@ def main() -> None:
                 del d_host
             except Exception as e:
                 line["cpu_baseline"] = {"value": None, "error": repr(e)}
+            sections["cpu_baseline"] = time.perf_counter() - t_sec
         if not args.no_secondary:
+            t_sec = time.perf_counter()
             del engine, runner
             torch.cuda.empty_cache()
             line["secondary_configs"] = secondary_configs(3)
+            sections["secondary_configs"] = time.perf_counter() - t_sec
+        line["wall_seconds_by_section"] = {k: round(v, 1) for k, v in sections.items()}
     elif not args.no_e2e:
         try:
             ev, et = e2e_sharded(engine, runner, D, max(1, min(args.steps, 3)), 1, rank)
