@@ -569,6 +569,10 @@ def main() -> None:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
+        # host-side barriers for the phases in which only rank 0 works: an NCCL
+        # barrier would park a spinning kernel on the other ranks' GPUs, which
+        # rank 0's multi-device call is about to use
+        host_group = dist.new_group(backend="gloo")
 
     D, cfg = make_input(args.config, torch.device("cuda", local), args.seed)
     n = cfg.n
@@ -686,7 +690,8 @@ def main() -> None:
         # (pald_gpu_opts.devices; the call pald::gpu::parallel_pairwise makes)
         del runner, engine
         torch.cuda.empty_cache()
-        dist.barrier()
+        torch.cuda.synchronize()
+        dist.barrier(group=host_group)
         if rank == 0:
             try:
                 # the ranks' GPUs (PALD_BENCH_BACKEND=gloo test runs share the visible ones)
@@ -698,7 +703,7 @@ def main() -> None:
                                        "pinned host buffers"}
             except Exception as e:
                 line["e2e"] = {"value": None, "error": repr(e)}
-        dist.barrier()
+        dist.barrier(group=host_group)  # the other ranks wait on the host, their GPUs idle
 
     if rank == 0:
         print(json.dumps(line), flush=True)
